@@ -1,0 +1,250 @@
+// TEST INFRASTRUCTURE ONLY — C-ABI wrapper around the UNMODIFIED reference.
+//
+// Compiles the reference colorq headers where they lie
+// (/root/reference/proj/include, passed with -I by oracle/Makefile; nothing is
+// copied into this repo) and exposes the hot-path functions through extern "C"
+// so tests can (1) pin the C restatement oracle/wsm_oracle.c and (2) generate
+// the golden vectors under tests/golden/. The built library lands in
+// oracle/_ref/ (git-ignored, travels to the GPU box) and also serves as the
+// reference CPU arm of bench.py (`--impl reference`, cpu_baseline kind
+// "reference"). The product library never links or calls it.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <thread>
+#include <vector>
+
+#include "colorq/histogram.hpp"
+#include "colorq/image_ops.hpp"
+#include "colorq/kmeans.hpp"
+#include "colorq/methods.hpp"
+#include "colorq/metrics.hpp"
+
+using namespace colorq;
+
+namespace {
+
+RgbImage make_image(const std::uint8_t* rgb, std::uint64_t w, std::uint64_t h) {
+  RgbImage img{int(w), int(h)};
+  std::memcpy(img.pixels.data(), rgb, 3 * w * h);
+  return img;
+}
+
+ColorHistogram make_hist(const std::uint32_t* keys, const std::uint32_t* counts, std::uint64_t n,
+                         std::uint64_t total) {
+  ColorHistogram h;
+  h.total_pixels = total;
+  h.colors.resize(n);
+  h.counts.assign(counts, counts + n);
+  h.weights.resize(n);
+  const double inv_total = 1.0 / double(total);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    h.colors[i] = to_vec3(unpack_rgb(keys[i]));
+    h.weights[i] = double(counts[i]) * inv_total;  // histogram.hpp:95-97
+  }
+  return h;
+}
+
+Palette make_palette(const double* C, int k) {
+  Palette p;
+  p.centers.resize(std::size_t(k));
+  for (int i = 0; i < k; ++i) p.centers[std::size_t(i)] = Vec3{C[3 * i], C[3 * i + 1], C[3 * i + 2]};
+  return p;
+}
+
+void store_palette(const Palette& p, double* C) {
+  for (std::size_t i = 0; i < p.size(); ++i)
+    for (int d = 0; d < 3; ++d) C[3 * i + std::size_t(d)] = p[i][std::size_t(d)];
+}
+
+Termination make_term(int mode, int max_iters, double eps, int cap) {
+  if (mode == 0) return Termination::fixed(max_iters);
+  return Termination::convergent(eps, cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_mt64_stream(std::uint64_t seed, std::uint64_t* out, int n) {
+  std::mt19937_64 g(seed);
+  for (int i = 0; i < n; ++i) out[i] = g();
+}
+
+std::uint64_t ref_next_prime(std::uint64_t n) { return next_prime(n); }
+
+std::uint64_t ref_universal_hash(std::uint8_t r, std::uint8_t g, std::uint8_t b, std::uint64_t m,
+                                 std::uint64_t a0, std::uint64_t a1, std::uint64_t a2) {
+  UniversalHashParams p{m, {a0, a1, a2}};
+  return universal_hash(RgbColor{r, g, b}, p);
+}
+
+// build_histogram(img) with the reference's default hash sizing
+// (histogram.hpp:105-108), or explicit params when hash_expected > 0.
+std::int64_t ref_build_histogram(const std::uint8_t* rgb, std::uint64_t n, std::uint32_t* keys,
+                                 std::uint32_t* counts, double* weights, std::uint64_t hash_expected,
+                                 std::uint64_t hash_seed) {
+  try {
+    const RgbImage img = make_image(rgb, n, 1);
+    const ColorHistogram h = hash_expected ? build_histogram(img, make_hash_params(hash_expected, hash_seed))
+                                           : build_histogram(img);
+    for (std::size_t i = 0; i < h.size(); ++i) {
+      keys[i] = pack_rgb(round_to_rgb(h.colors[i]));
+      counts[i] = h.counts[i];
+      if (weights) weights[i] = h.weights[i];
+    }
+    return std::int64_t(h.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+int ref_init_centers(const std::uint32_t* keys, std::uint64_t n, int k, std::uint64_t seed, double* C) {
+  try {
+    std::vector<Vec3> pts(n);
+    for (std::uint64_t i = 0; i < n; ++i) pts[i] = to_vec3(unpack_rgb(keys[i]));
+    store_palette(init_centers(std::span<const Vec3>(pts), k, seed), C);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// One fresh update_center_tables + assign_sort_means (kmeans.hpp:132-239).
+int ref_sort_means_step(const std::uint32_t* keys, const std::uint32_t* counts, std::uint64_t n,
+                        std::uint64_t total, const double* C, int k, std::int32_t* labels,
+                        double* sse, std::uint64_t* evals, double* D, std::int32_t* order) {
+  try {
+    const ColorHistogram h = make_hist(keys, counts, n, total);
+    const Palette pal = make_palette(C, k);
+    ClusterState st;
+    st.memberships.assign(labels, labels + n);
+    st.update_center_tables(pal);
+    const AssignResult ar = assign_sort_means(h.colors, h.weights, pal, st);
+    std::copy(st.memberships.begin(), st.memberships.end(), labels);
+    *sse = ar.weighted_sse;
+    *evals = ar.dist_evals;
+    if (D) std::copy(st.center_dists.begin(), st.center_dists.end(), D);
+    if (order) std::copy(st.sorted_order.begin(), st.sorted_order.end(), order);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+int ref_update_centers(const std::uint32_t* keys, const std::uint32_t* counts, std::uint64_t n,
+                       std::uint64_t total, const std::int32_t* labels, const double* prev, int k,
+                       double* next) {
+  try {
+    const ColorHistogram h = make_hist(keys, counts, n, total);
+    Memberships m(labels, labels + n);
+    store_palette(update_centers(h, m, make_palette(prev, k)), next);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// run_wsm (kmeans.hpp:394-404) with the trajectory hook. Returns iterations.
+int ref_run_wsm(const std::uint32_t* keys, const std::uint32_t* counts, std::uint64_t n, std::uint64_t total,
+                int k, int mode, int max_iters, double eps, int cap, std::uint64_t seed, double* C_out,
+                double* sse_out, std::uint64_t* evals_out, double* sse_hist, int hist_cap, double* traj,
+                int traj_cap) {
+  try {
+    const ColorHistogram h = make_hist(keys, counts, n, total);
+    std::vector<Palette> trajectory;
+    const KmRunResult r = run_wsm(h, k, make_term(mode, max_iters, eps, cap), seed, traj ? &trajectory : nullptr);
+    store_palette(r.palette, C_out);
+    *sse_out = r.report.sse;
+    *evals_out = r.report.dist_evals;
+    if (sse_hist)
+      for (std::size_t i = 0; i < r.report.sse_history.size() && int(i) < hist_cap; ++i)
+        sse_hist[i] = r.report.sse_history[i];
+    if (traj)
+      for (std::size_t t = 0; t < trajectory.size() && int(t) < traj_cap; ++t)
+        store_palette(trajectory[t], traj + t * std::size_t(3 * k));
+    return r.report.iterations;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+int ref_map_pixels(const std::uint8_t* rgb, std::uint64_t n, const double* C, int k, std::uint8_t* out_rgb) {
+  try {
+    const RgbImage out = map_pixels(make_image(rgb, n, 1), make_palette(C, k));
+    std::memcpy(out_rgb, out.pixels.data(), 3 * n);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+double ref_mse(const std::uint8_t* a, const std::uint8_t* b, std::uint64_t n) {
+  return mse(make_image(a, n, 1), make_image(b, n, 1));
+}
+
+// The reference hot path end to end as the CLI composes it
+// (tools/colorq.cpp:96-102): generate_palette's WSM branch
+// (methods.hpp:182-189: build_histogram + run_wsm) + map_pixels + mse.
+// Termination is passed explicitly so BASELINE's convergent(1e-4, 100) is
+// reachable (the CLI always uses cap 1000). Times in ms.
+int ref_quantize(const std::uint8_t* rgb, int w, int h, int k, int mode, int max_iters, double eps, int cap,
+                 std::uint64_t seed, double* C_out, int* iterations, double* sse, std::uint64_t* evals,
+                 std::uint8_t* out_rgb, double* mse_out, double* palette_ms, double* map_ms) {
+  try {
+    const RgbImage img = make_image(rgb, std::uint64_t(w), std::uint64_t(h));
+    StopWatch watch;
+    const ColorHistogram hist = build_histogram(img);
+    const KmRunResult r = run_wsm(hist, k, make_term(mode, max_iters, eps, cap), seed);
+    if (palette_ms) *palette_ms = watch.elapsed_ms();
+    StopWatch mwatch;
+    const RgbImage mapped = map_pixels(img, r.palette);
+    const double m = mse(img, mapped);
+    if (map_ms) *map_ms = mwatch.elapsed_ms();
+    store_palette(r.palette, C_out);
+    *iterations = r.report.iterations;
+    *sse = r.report.sse;
+    *evals = r.report.dist_evals;
+    *mse_out = m;
+    if (out_rgb) std::memcpy(out_rgb, mapped.pixels.data(), 3 * std::size_t(w) * std::size_t(h));
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// Many independent images on a thread pool, one image per worker at a time
+// (the bench.hpp:187-223 pattern). Returns wall ms for the whole batch.
+double ref_quantize_many(const std::uint8_t* const* imgs, int count, int w, int h, int k, int mode,
+                         int max_iters, double eps, int cap, std::uint64_t seed, int nthreads,
+                         double* mse_out, int* iters_out) {
+  std::atomic<int> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      const int i = next.fetch_add(1);
+      if (i >= count) return;
+      double C[3 * 256 * 16];
+      std::vector<double> cbuf(std::size_t(3 * k));
+      int it = 0;
+      double s = 0, m = 0;
+      std::uint64_t ev = 0;
+      ref_quantize(imgs[i], w, h, k, mode, max_iters, eps, cap, seed, cbuf.data(), &it, &s, &ev, nullptr, &m,
+                   nullptr, nullptr);
+      (void)C;
+      if (mse_out) mse_out[i] = m;
+      if (iters_out) iters_out[i] = it;
+    }
+  };
+  StopWatch watch;
+  std::vector<std::thread> pool;
+  const int nt = std::max(1, std::min(nthreads, count));
+  for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  return watch.elapsed_ms();
+}
+
+}  // extern "C"
