@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 WSM quantize path (BASELINE.json metric
+"WSM quantize Mpixel/s at K=256").
+
+Workload (default): BASELINE config 2 (768x512 GMM-256 image, K=256,
+convergent(1e-4, cap 100), init seed 1) — configs[1], the config the metric is
+quoted on. One step = one full quantize (histogram + WSM-C + map + MSE) of one
+image per rank. N > 1 (torchrun): every rank quantizes its own image (replica
+/ weak scaling, no data-path collective). `--config cfg4` selects the
+4096x4096 uniform config instead.
+
+  value : P * ranks / (max over ranks of the per-step device time), image
+          resident in HBM, CUDA events on the library stream, L2 flushed
+          (256 MiB write) between timed steps.
+  e2e   : the same metric through the public C-ABI call (cqb_quantize) with
+          pinned HOST buffers: H2D of the image and D2H of the index map,
+          mapped raster, palette and report inside the timed region.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref: the unmodified colorq headers compiled here) on all host cores,
+one image per worker thread (the bench.hpp:187-223 pool pattern).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1011_0093_b200.configs import CONFIGS, EPSILON, HARD_CAP, INIT_SEED  # noqa: E402
+
+METRIC = "WSM quantize Mpixel/s at K=256"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--k", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    return ap.parse_args()
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _workload(cfg, k):
+    return (f"{cfg.name}: {cfg.width}x{cfg.height} {cfg.description}; K={k}; "
+            f"convergent(eps={EPSILON}, cap={HARD_CAP}); init seed {INIT_SEED}")
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(a, cfg, world, rank):
+    if rank != 0:
+        return None
+    from oracle.oracle import Oracle, available
+
+    if not available("reference"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcolorq_ref.so not built"}))
+        return None
+    ref = Oracle("reference")
+    cores = _host_cores()
+    img = cfg.image()
+    P = cfg.pixels
+    imgs = [img] * cores
+    for _ in range(a.warmup):
+        ref.quantize_many(imgs, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
+    walls = []
+    for _ in range(a.steps):
+        ms, mses, its = ref.quantize_many(imgs, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
+        walls.append(ms)
+    total_ms = sum(walls)
+    value = P * cores * a.steps / (total_ms * 1e-3) / 1e6
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpixel/s", "impl": "reference", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload(cfg, a.k), "pixels": P, "images_per_step": cores},
+        "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": cores, "kind": "reference",
+                         "sample": f"{cores} copies of the {cfg.name} image per step, one per thread "
+                                   f"(oracle/_ref, g++ -O2), iterations={int(its[0])}"},
+        "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return line
+
+
+def cpu_baseline_sample(cfg, k, img):
+    """oracle/_ref on all host cores, one image per thread (~seconds)."""
+    from oracle.oracle import Oracle, available
+
+    if not available("reference"):
+        return None
+    ref = Oracle("reference")
+    cores = _host_cores()
+    imgs = [img] * cores
+    ms, _, its = ref.quantize_many(imgs, k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
+    return {"value": cfg.pixels * cores / (ms * 1e-3) / 1e6, "unit": "Mpixel/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"{cores} concurrent copies of the {cfg.name} image (one per thread), full quantize "
+                      f"(histogram+WSM-C+map+mse), {int(its[0])} iterations, wall {ms:.0f} ms"}
+
+
+# --------------------------------------------------------------------------- our arm
+def measure_device(lib, ctx, torch, d_img, P, k, steps, warmup, stream, flush, profile=False):
+    """Per-step device time (ms) with CUDA events on the library stream."""
+    from paper_1011_0093_b200 import _native as N
+
+    term = N.Termination(1, 10, EPSILON, HARD_CAP)
+    d_idx = torch.empty(P, dtype=torch.uint8, device=d_img.device)
+    d_out = torch.empty(3 * P, dtype=torch.uint8, device=d_img.device)
+    rep = N.Report()
+    hist = np.zeros(HARD_CAP)
+    cent = np.zeros(3 * k)
+
+    def one(sync):
+        rc = lib.cqb_quantize_device(ctx.h, C.c_void_p(d_img.data_ptr()), P, k, C.byref(term), INIT_SEED,
+                                     C.c_void_p(d_idx.data_ptr()), C.c_void_p(d_out.data_ptr()), sync,
+                                     cent.ctypes.data_as(C.POINTER(C.c_double)),
+                                     hist.ctypes.data_as(C.POINTER(C.c_double)), HARD_CAP, C.byref(rep))
+        ctx.check(rc)
+
+    times, stage = [], []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    launches = 0
+    with torch.cuda.stream(stream):  # flush, events and the library share one stream
+        for _ in range(warmup):
+            flush()
+            one(1)
+        for i in range(steps):
+            flush()
+            evs[i][0].record(stream)
+            one(0)
+            evs[i][1].record(stream)
+            launches += 7
+            if profile:
+                ms = (C.c_float * 7)()
+                ctx.check(lib.cqb_stage_times(ctx.h, ms, 7))
+                stage.append(list(ms))
+    torch.cuda.synchronize()
+    for a, b in evs:
+        times.append(a.elapsed_time(b))
+    ctx.check(lib.cqb_fetch_results(ctx.h, cent.ctypes.data_as(C.POINTER(C.c_double)),
+                                    hist.ctypes.data_as(C.POINTER(C.c_double)), HARD_CAP, C.byref(rep)))
+    return times, stage, rep, cent.reshape(k, 3).copy(), launches
+
+
+def run_ours(a, cfg, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200 import _native as N
+    from paper_1011_0093_b200 import api
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = N.context(local)
+    lib = ctx.lib
+    stream = torch.cuda.Stream(device=dev)
+    ctx.check(lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
+    img = cfg.image()  # every rank: its own replica of the config image
+    P = cfg.pixels
+    k = a.k
+    d_img = torch.from_numpy(img.reshape(-1)).to(dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)  # > L2 (126 MB): evicts the previous step's working set
+
+    # ---- device-resident timing (value) ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_wall0 = time.perf_counter()
+    times, _, rep, centers, launches = measure_device(lib, ctx, torch, d_img, P, k, a.steps, a.warmup, stream, flush)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = P * world * a.steps / (total_ms * 1e-3) / 1e6
+
+    # ---- per-stage attribution + roofline of the dominant kernel ----
+    ctx.check(lib.cqb_set_profiling(ctx.h, 1))
+    _, stage, rep_p, _, _ = measure_device(lib, ctx, torch, d_img, P, k, max(3, min(a.steps, 5)), 1, stream, flush,
+                                           profile=True)
+    ctx.check(lib.cqb_set_profiling(ctx.h, 0))
+    st = np.median(np.array(stage), axis=0)
+    names = N.STAGES
+    stage_ms = {n: float(v) for n, v in zip(names, st)}
+    n_unique = int(rep.n_unique)
+    iters = int(rep.iterations)
+    peaks = _peaks()
+    dom = max(stage_ms, key=stage_ms.get)
+    roof = _roofline(dom, stage_ms[dom], P, n_unique, iters, k, peaks, int(rep.dist_evals))
+
+    # ---- e2e through the public C-ABI call with pinned host buffers ----
+    pin_img = torch.from_numpy(img.reshape(-1)).pin_memory()
+    pin_idx = torch.empty(P, dtype=torch.uint8).pin_memory()
+    pin_out = torch.empty(3 * P, dtype=torch.uint8).pin_memory()
+    h_img = pin_img.numpy().reshape(img.shape)
+    h_idx = pin_idx.numpy().reshape(img.shape[:2])
+    h_out = pin_out.numpy().reshape(img.shape)
+    term = api.Termination.convergent(EPSILON, HARD_CAP)
+    ctx.check(lib.cqb_set_stream(ctx.h, None))
+    for _ in range(a.warmup):
+        flush()
+        torch.cuda.synchronize()
+        api.quantize(h_img, k, term, INIT_SEED, out_index=h_idx, out_mapped=h_out, device=local)
+    e2e_times = []
+    for _ in range(a.steps):
+        flush()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        q = api.quantize(h_img, k, term, INIT_SEED, out_index=h_idx, out_mapped=h_out, device=local)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = P * world * a.steps / e2e_s / 1e6
+    assert np.array_equal(q.palette, centers), "e2e and device-resident paths disagree"
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload(cfg, k), "pixels": P, "n_unique": n_unique, "iterations": iters,
+                       "k": k, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "timed": "per-step CUDA events on the library stream; value = P*ranks*steps / max-rank sum",
+                       "wall_bracket_s": round(t_wall, 4)},
+            "e2e": {"value": e2e_value, "unit": "Mpixel/s", "h2d_bytes_per_step": 3 * P,
+                    "d2h_bytes_per_step": 4 * P + 8 * 3 * k + 8 * HARD_CAP + 64,
+                    "path": "cqb_quantize (C ABI) with pinned host buffers, wall clock"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "stages_ms": {kk: round(v, 5) for kk, v in stage_ms.items()},
+            "dist_evals": int(rep.dist_evals),
+            "clocks": clk,
+        }
+        if world == 1 and not a.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample(cfg, k, img)
+        if world == 1 and not a.no_secondary and cfg.name == "cfg2":
+            line["secondary"] = secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks)
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
+    """Config 4 (4096^2 uniform, ~10.6M unique colors, K=256), device-resident."""
+    from paper_1011_0093_b200 import _native as N
+
+    cfg = CONFIGS["cfg4"]
+    img = cfg.image()
+    d = torch.from_numpy(img.reshape(-1)).to(dev)
+    ctx.check(lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
+    times, _, rep, _, _ = measure_device(lib, ctx, torch, d, cfg.pixels, 256, 3, 2, stream, flush)
+    ctx.check(lib.cqb_set_profiling(ctx.h, 1))
+    _, stage, _, _, _ = measure_device(lib, ctx, torch, d, cfg.pixels, 256, 2, 0, stream, flush, profile=True)
+    ctx.check(lib.cqb_set_profiling(ctx.h, 0))
+    st = np.median(np.array(stage), axis=0)
+    stage_ms = {n: float(v) for n, v in zip(N.STAGES, st)}
+    ms = sum(times) / len(times)
+    dom = max(stage_ms, key=stage_ms.get)
+    return {"workload": _workload(cfg, 256), "value": cfg.pixels / (ms * 1e-3) / 1e6, "unit": "Mpixel/s",
+            "ms_per_step": ms, "n_unique": int(rep.n_unique), "iterations": int(rep.iterations),
+            "dist_evals": int(rep.dist_evals), "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "roofline": _roofline(dom, stage_ms[dom], cfg.pixels, int(rep.n_unique), int(rep.iterations), 256, peaks,
+                                  int(rep.dist_evals))}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
+    """Algorithmic bytes per launch of the dominant kernel."""
+    if stage == "wsm_loop":
+        # per iteration per sample: u32 key + u32 count + u8 label read + u8 label write
+        traffic_alg = 10.0 * n_unique * iters
+        note = (f"10 B/sample/iteration x N'={n_unique} x {iters} iterations; "
+                f"{evals / (ms * 1e-3) / 1e9:.2f} G dist evals/s")
+    elif stage in ("hist_count",):
+        traffic_alg = 3.0 * P
+        note = "3P bytes (u8x3 raster read); bin atomics not counted"
+    elif stage == "hist_compact":
+        traffic_alg = 3.0 * P + 8.0 * n_unique
+        note = "3P raster read + 8 B per unique color written"
+    elif stage == "map_pixels":
+        traffic_alg = 7.0 * P
+        note = "3P read + P index + 3P RGB written"
+    else:
+        traffic_alg = 8.0 * n_unique
+        note = "8 B per unique color"
+    achieved = traffic_alg / (ms * 1e-3) / 1e9
+    return {"kernel": stage, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel_ms": ms, "algorithmic_bytes": traffic_alg,
+            "peak_source": peaks["source"], "note": note}
+
+
+def main():
+    a = _args()
+    world, rank, local = _dist()
+    cfg = CONFIGS[a.config]
+    if a.impl == "reference":
+        run_reference(a, cfg, world, rank)
+        return
+    run_ours(a, cfg, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * colorq_b200 — C ABI of the B200-native WSM color-quantization hot path.
+ *
+ * Plain pointers and sizes only (no CUDA or torch types in the signatures;
+ * streams are passed as void*). Every entry point returns a status code
+ * (CQB_OK = 0) and leaves a message retrievable with cqb_last_error().
+ *
+ * Each entry point replaces one reference function of the colorq C++ API
+ * (/root/reference/proj/include/colorq, header-only C++20); the drop-in C++
+ * shim with the reference's own signatures is include/colorq_b200/colorq.hpp.
+ *
+ * Threading: one cqb_ctx per host thread (the shim keeps a thread_local one);
+ * a context owns its CUDA stream and device arena, so concurrent calls on
+ * distinct contexts are safe (bench.hpp:187-223).
+ */
+#ifndef COLORQ_B200_H
+#define COLORQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The shim maps INVALID_ARGUMENT to std::invalid_argument
+ * (the reference's error type; CLI exit code 4) and the rest to
+ * std::runtime_error. */
+#define CQB_OK 0
+#define CQB_ERR_INVALID_ARGUMENT 1
+#define CQB_ERR_UNSUPPORTED 2
+#define CQB_ERR_CUDA 3
+#define CQB_ERR_OOM 4
+#define CQB_ERR_NCCL 5
+#define CQB_ERR_INTERNAL 6
+
+#define CQB_MAX_K 256
+
+typedef struct cqb_ctx cqb_ctx;
+
+/* Termination — replaces colorq::Termination (kmeans.hpp:25-38).
+ * mode 0 = FixedIterations(max_iters); mode 1 = Convergent(epsilon, hard_cap). */
+typedef struct {
+  int mode;
+  int max_iters;
+  double epsilon;
+  int hard_cap;
+} cqb_termination;
+
+/* Run report — the fields of colorq::RunReport (report.hpp:33-53) the WSM
+ * path fills, plus device-side extras. */
+typedef struct {
+  int iterations;       /* number of assignment passes (kmeans.hpp:358) */
+  int k;
+  uint64_t seed;
+  double sse;           /* weighted SSE at the last assignment (kmeans.hpp:373) */
+  double mse;           /* full-image MSE of the mapped result (quantize only) */
+  double elapsed_ms;    /* palette generation, device time (methods.hpp:111,195) */
+  double map_ms;        /* map + mse, device time */
+  uint64_t dist_evals;  /* point + pair distance evaluations (kmeans.hpp:353,356) */
+  uint64_t n_unique;    /* N' */
+  int empty_events;     /* clusters re-seeded (kmeans.hpp:272-294) */
+  int gpu_launches;     /* kernels this call launched */
+} cqb_report;
+
+/* ---- context ---------------------------------------------------------- */
+int cqb_create(int device, cqb_ctx** out);
+int cqb_destroy(cqb_ctx* ctx);
+const char* cqb_last_error(const cqb_ctx* ctx);
+/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the
+ * context's own stream. */
+int cqb_set_stream(cqb_ctx* ctx, void* stream);
+/* Cap the persistent WSM grid (0 = one full wave: 148 SMs x occupancy), for
+ * running several images concurrently on one GPU (config 5). */
+int cqb_set_grid_limit(cqb_ctx* ctx, int max_blocks);
+int cqb_device_info(cqb_ctx* ctx, int* num_sms, int* loop_blocks);
+/* Per-stage CUDA-event timing of cqb_quantize* (off by default). Stages:
+ * [0] state reset, [1] K1 histogram count, [2] K2 compaction, [3] init,
+ * [4] WSM loop (tables+assign+update, all iterations), [5] map tables +
+ * unique-color map + MSE, [6] per-pixel map. */
+int cqb_set_profiling(cqb_ctx* ctx, int on);
+int cqb_stage_times(cqb_ctx* ctx, float* ms, int n);
+
+/* ---- histogram ---------------------------------------------------------
+ * Replaces build_histogram(const RgbImage&) (histogram.hpp:65-99,105-108).
+ * rgb: n_pixels x {r,g,b} host bytes, row-major. Outputs (host, capacity
+ * `cap` entries, entries in FIRST-OCCURRENCE order): packed keys
+ * r<<16|g<<8|b, counts, optional weights = count*(1/P), optional first pixel
+ * index. *n_unique = N'. Empty image -> CQB_ERR_INVALID_ARGUMENT (:66). */
+int cqb_build_histogram(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, uint32_t* keys, uint32_t* counts,
+                        double* weights, uint32_t* first_index, uint64_t cap, uint64_t* n_unique);
+
+/* ---- clustering --------------------------------------------------------
+ * Replaces run_wsm(const ColorHistogram&, k, Termination, seed, trajectory*)
+ * (kmeans.hpp:394-404): init_centers (:53-74) + the sort-means loop
+ * (:336-376) over a histogram given as packed keys + counts (total = P).
+ * centers_out: k x 3 doubles (post-update palette of the last iteration).
+ * sse_history: hist_cap doubles (one per iteration). trajectory (nullable):
+ * traj_cap x k x 3 doubles, the palette after every update (:361).
+ * labels_out (nullable): final memberships, u8. k in [1, 256]; k > N' ->
+ * CQB_ERR_INVALID_ARGUMENT (:54-56). */
+int cqb_run_wsm(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* counts, uint64_t n_unique, uint64_t total,
+                int k, const cqb_termination* term, uint64_t seed, double* centers_out, double* sse_history,
+                int hist_cap, double* trajectory, int traj_cap, uint8_t* labels_out, cqb_report* report);
+
+/* Teacher-forced iteration hook (parity tests): from the given centers and
+ * memberships run `term` iterations of the same device loop (tables ->
+ * assign_sort_means -> update_centers). dense_first = 1 only for the
+ * reference's bootstrap pass (labels all 0, integer centers). Replaces one
+ * update_center_tables + assign_sort_means + update_centers
+ * (kmeans.hpp:132-296). labels_inout: u8 memberships in/out. */
+int cqb_wsm_iterate(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* counts, uint64_t n_unique, uint64_t total,
+                    int k, const double* centers_in, uint8_t* labels_inout, int dense_first,
+                    const cqb_termination* term, double* centers_out, double* sse_history, int hist_cap,
+                    cqb_report* report);
+
+/* ---- end to end --------------------------------------------------------
+ * generate_palette's WSM / WSM-C branch (methods.hpp:182-189) + map_pixels
+ * (image_ops.hpp:18-51) + mse (metrics.hpp:18-29) in one device pass.
+ * rgb: width*height pixels (host). index_out (nullable): u8 palette index
+ * per pixel (new output; the reference has none). rgb_out (nullable): the
+ * mapped image. report->mse is filled. */
+int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                 uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
+                 uint8_t* rgb_out, cqb_report* report);
+
+/* Same pipeline with DEVICE-resident image and outputs (all pointers are
+ * device pointers on the context's device; outputs nullable). Enqueued on
+ * the context stream; when `sync` is 0 the call returns without waiting and
+ * report/centers/sse_history are NOT filled (use cqb_fetch_results). */
+int cqb_quantize_device(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int k, const cqb_termination* term,
+                        uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, int sync, double* centers_out,
+                        double* sse_history, int hist_cap, cqb_report* report);
+/* Waits for the last enqueued quantize on this context and copies its results. */
+int cqb_fetch_results(cqb_ctx* ctx, double* centers_out, double* sse_history, int hist_cap, cqb_report* report);
+
+/* ---- post-processing ---------------------------------------------------
+ * Replaces map_pixels(img, palette) (image_ops.hpp:18-51): nearest ROUNDED
+ * palette entry, lowest index on ties. centers: k x 3 doubles, k in [1,256];
+ * k < 1 -> CQB_ERR_INVALID_ARGUMENT (:19). Outputs nullable; sq_err_sum
+ * (nullable) = Σ squared error vs the input (mse numerator). */
+int cqb_map_pixels(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, const double* centers, int k,
+                   uint8_t* rgb_out, uint8_t* index_out, uint64_t* sq_err_sum);
+
+/* Replaces mse(a, b) (metrics.hpp:18-29): exact u64 sum / P. */
+int cqb_mse(cqb_ctx* ctx, const uint8_t* a, const uint8_t* b, uint64_t n_pixels, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COLORQ_B200_H */

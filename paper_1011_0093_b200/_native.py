@@ -1,0 +1,144 @@
+"""ctypes binding of the C ABI (include/colorq_b200.h).
+
+The CUDA library is built in-tree by ``__graft_entry__.build()`` (or
+``make``) into ``paper_1011_0093_b200/lib/libcolorq_b200.so``. There is no
+fallback: if the library is missing or no sm_100 device is present, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libcolorq_b200.so")
+
+CQB_OK = 0
+CQB_ERR_INVALID_ARGUMENT = 1
+CQB_ERR_UNSUPPORTED = 2
+CQB_ERR_CUDA = 3
+CQB_ERR_OOM = 4
+CQB_ERR_NCCL = 5
+CQB_ERR_INTERNAL = 6
+MAX_K = 256
+
+# Every symbol the header declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "cqb_create", "cqb_destroy", "cqb_last_error", "cqb_set_stream", "cqb_set_grid_limit", "cqb_device_info",
+    "cqb_build_histogram", "cqb_run_wsm", "cqb_wsm_iterate", "cqb_quantize", "cqb_quantize_device",
+    "cqb_fetch_results", "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
+)
+STAGES = ("reset", "hist_count", "hist_compact", "init", "wsm_loop", "map_unique", "map_pixels")
+
+
+class Termination(C.Structure):
+    _fields_ = [("mode", C.c_int), ("max_iters", C.c_int), ("epsilon", C.c_double), ("hard_cap", C.c_int)]
+
+
+class Report(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int), ("k", C.c_int), ("seed", C.c_uint64), ("sse", C.c_double), ("mse", C.c_double),
+        ("elapsed_ms", C.c_double), ("map_ms", C.c_double), ("dist_evals", C.c_uint64), ("n_unique", C.c_uint64),
+        ("empty_events", C.c_int), ("gpu_launches", C.c_int),
+    ]
+
+
+class CqbError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[cqb {code}] {msg}")
+        self.code = code
+
+
+class CqbInvalidArgument(CqbError, ValueError):
+    """Maps the reference's std::invalid_argument."""
+
+
+_u8p = C.POINTER(C.c_uint8)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+_T = C.POINTER(Termination)
+_R = C.POINTER(Report)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library() -> C.CDLL:
+    """Load the in-tree CUDA library (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"colorq_b200 CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        L.cqb_create.argtypes = [C.c_int, C.POINTER(_vp)]
+        L.cqb_destroy.argtypes = [_vp]
+        L.cqb_last_error.argtypes = [_vp]
+        L.cqb_last_error.restype = C.c_char_p
+        L.cqb_set_stream.argtypes = [_vp, _vp]
+        L.cqb_set_grid_limit.argtypes = [_vp, C.c_int]
+        L.cqb_device_info.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.cqb_build_histogram.argtypes = [_vp, _u8p, C.c_uint64, _u32p, _u32p, _f64p, _u32p, C.c_uint64, _u64p]
+        L.cqb_run_wsm.argtypes = [_vp, _u32p, _u32p, C.c_uint64, C.c_uint64, C.c_int, _T, C.c_uint64, _f64p, _f64p,
+                                  C.c_int, _f64p, C.c_int, _u8p, _R]
+        L.cqb_wsm_iterate.argtypes = [_vp, _u32p, _u32p, C.c_uint64, C.c_uint64, C.c_int, _f64p, _u8p, C.c_int, _T,
+                                      _f64p, _f64p, C.c_int, _R]
+        L.cqb_quantize.argtypes = [_vp, _u8p, C.c_int, C.c_int, C.c_int, _T, C.c_uint64, _f64p, _f64p, C.c_int, _u8p,
+                                   _u8p, _R]
+        L.cqb_quantize_device.argtypes = [_vp, _vp, C.c_uint64, C.c_int, _T, C.c_uint64, _vp, _vp, C.c_int, _f64p,
+                                          _f64p, C.c_int, _R]
+        L.cqb_fetch_results.argtypes = [_vp, _f64p, _f64p, C.c_int, _R]
+        L.cqb_map_pixels.argtypes = [_vp, _u8p, C.c_uint64, _f64p, C.c_int, _u8p, _u8p, _u64p]
+        L.cqb_mse.argtypes = [_vp, _u8p, _u8p, C.c_uint64, _f64p]
+        L.cqb_set_profiling.argtypes = [_vp, C.c_int]
+        L.cqb_stage_times.argtypes = [_vp, C.POINTER(C.c_float), C.c_int]
+        _lib = L
+        return L
+
+
+class Context:
+    """One device context (stream + arena). Not shared across threads."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = _vp()
+        rc = self.lib.cqb_create(device, C.byref(h))
+        if rc != CQB_OK:
+            raise CqbError(rc, f"cqb_create(device={device}) failed (see stderr)")
+        self.h = h
+        self.device = device
+
+    def check(self, rc: int) -> None:
+        if rc == CQB_OK:
+            return
+        msg = self.lib.cqb_last_error(self.h).decode(errors="replace")
+        if rc == CQB_ERR_INVALID_ARGUMENT:
+            raise CqbInvalidArgument(rc, msg)
+        raise CqbError(rc, msg)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.cqb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def context(device: int = 0) -> Context:
+    """Thread-local context per device (the re-entrancy contract)."""
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]

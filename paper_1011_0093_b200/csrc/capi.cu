@@ -1,0 +1,709 @@
+// Host side of the C ABI (include/colorq_b200.h): per-context device arena,
+// stream, launch sequencing and result staging. No CPU fallback exists: every
+// numeric result below comes from the sm_100a kernels in hist/wsm/map.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <random>
+#include <string>
+
+#include "../../include/colorq_b200.h"
+#include "hist.cuh"
+#include "map.cuh"
+#include "wsm.cuh"
+
+using namespace cqb;
+
+namespace {
+
+struct Staging {  // pinned host mirror of the per-call results
+  double centers[3 * KMAX];
+  unsigned long long evals, mse_err, n_unique;
+  double sse;
+  int iterations, status, n_empty;
+};
+
+}  // namespace
+
+struct cqb_ctx {
+  int device = 0;
+  int num_sms = 0;
+  int loop_blocks_max = 0;
+  int grid_limit = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+
+  uint2* bins = nullptr;  // 2^24 x {count, ~first}; all-zero between calls
+  uint8_t* lut = nullptr; // 2^24 key -> palette index
+
+  size_t cap_px = 0;
+  uint8_t* d_img = nullptr;
+  uint8_t* d_img2 = nullptr;
+  uint8_t* d_index = nullptr;
+  uint8_t* d_rgb = nullptr;
+  size_t cap_tiles = 0;
+  unsigned long long* tile_state = nullptr;  // [ntiles] + ticket at [cap_tiles]
+
+  size_t cap_s = 0;
+  uint32_t* d_keys = nullptr;
+  uint32_t* d_counts = nullptr;
+  uint32_t* d_first = nullptr;
+  uint8_t* d_labels = nullptr;
+  double* d_weights = nullptr;
+  unsigned long long* d_n = nullptr;  // N'
+
+  WsmState* st = nullptr;
+  double* d_hist = nullptr;
+  int cap_hist = 0;
+  double* d_traj = nullptr;
+  size_t cap_traj = 0;
+  double* d_centers_in = nullptr;
+  int* d_sortedDr = nullptr;
+  uint8_t* d_orderR = nullptr;
+  uint32_t* d_palkey = nullptr;
+
+  unsigned long long* d_draws = nullptr;
+  unsigned long long* h_draws = nullptr;
+  int cap_draws = 0;
+  bool draws_valid = false;
+  uint64_t draws_seed = 0;
+  int draws_n = 0;
+
+  Staging* h_stage = nullptr;
+  double* h_hist = nullptr;
+  unsigned long long* h_scalar = nullptr;
+  cudaEvent_t ev[4] = {};
+  bool profiling = false;
+  cudaEvent_t pev[8] = {};  // stage boundaries when profiling
+  int last_k = 0;
+  int last_hist_cap = 0;
+  int launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(cqb_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? CQB_ERR_OOM : CQB_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+  } while (0)
+
+#define CKL()                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = cudaGetLastError();                                                         \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(ctx, CQB_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                     \
+    ++ctx->launches;                                                                             \
+  } while (0)
+
+#define TRY(x)             \
+  do {                     \
+    int r_ = (x);          \
+    if (r_ != CQB_OK) return r_; \
+  } while (0)
+
+template <typename T>
+int grow(cqb_ctx* ctx, T** p, size_t n) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)));
+  return CQB_OK;
+}
+
+int ensure_pixels(cqb_ctx* ctx, size_t P) {
+  if (P <= ctx->cap_px) return CQB_OK;
+  const size_t cap = (P + 15) / 16 * 16 + 64;
+  TRY(grow(ctx, &ctx->d_img, 3 * cap));
+  TRY(grow(ctx, &ctx->d_img2, 3 * cap));
+  TRY(grow(ctx, &ctx->d_index, cap));
+  TRY(grow(ctx, &ctx->d_rgb, 3 * cap));
+  ctx->cap_px = cap;
+  const size_t tiles = (P + TILE_PX - 1) / TILE_PX + 1;
+  if (tiles > ctx->cap_tiles) {
+    TRY(grow(ctx, &ctx->tile_state, tiles + 1));
+    ctx->cap_tiles = tiles;
+  }
+  return CQB_OK;
+}
+
+int ensure_samples(cqb_ctx* ctx, size_t n) {
+  if (n <= ctx->cap_s) return CQB_OK;
+  const size_t cap = n + 64;
+  TRY(grow(ctx, &ctx->d_keys, cap));
+  TRY(grow(ctx, &ctx->d_counts, cap));
+  TRY(grow(ctx, &ctx->d_first, cap));
+  TRY(grow(ctx, &ctx->d_labels, cap));
+  TRY(grow(ctx, &ctx->d_weights, cap));
+  ctx->cap_s = cap;
+  return CQB_OK;
+}
+
+int ensure_hist(cqb_ctx* ctx, int n) {
+  if (n <= ctx->cap_hist) return CQB_OK;
+  TRY(grow(ctx, &ctx->d_hist, (size_t)n));
+  if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+  ctx->h_hist = nullptr;
+  CK(cudaMallocHost(&ctx->h_hist, sizeof(double) * (size_t)n));
+  ctx->cap_hist = n;
+  return CQB_OK;
+}
+
+int check_term(cqb_ctx* ctx, const cqb_termination* t) {
+  if (!t) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "termination is null");
+  if (t->mode == 1) {
+    if (!(t->epsilon > 0)) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "convergent termination requires epsilon > 0");
+    if (t->hard_cap < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hard_cap must be >= 1");
+  } else if (t->mode == 0) {
+    if (t->max_iters < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "max_iters must be >= 1");
+  } else {
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "unknown termination mode %d", t->mode);
+  }
+  return CQB_OK;
+}
+
+int term_iters(const cqb_termination* t) { return t->mode == 1 ? t->hard_cap : t->max_iters; }
+
+int check_k(cqb_ctx* ctx, int k) {
+  if (k < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "k must be >= 1");
+  if (k > KMAX) return fail(ctx, CQB_ERR_UNSUPPORTED, "k = %d exceeds the device limit %d", k, KMAX);
+  return CQB_OK;
+}
+
+// Raw mt19937_64 stream for init_centers (kmeans.hpp:56-65). The stream does
+// not depend on N', so it is produced here and consumed on device.
+int upload_draws(cqb_ctx* ctx, uint64_t seed, int ndraws) {
+  if (ctx->draws_valid && ctx->draws_seed == seed && ctx->draws_n >= ndraws) return CQB_OK;
+  if (ndraws > ctx->cap_draws) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_draws) cudaFreeHost(ctx->h_draws);
+    ctx->h_draws = nullptr;
+    CK(cudaMallocHost(&ctx->h_draws, sizeof(unsigned long long) * (size_t)ndraws));
+    TRY(grow(ctx, &ctx->d_draws, (size_t)ndraws));
+    ctx->cap_draws = ndraws;
+  }
+  CK(cudaEventSynchronize(ctx->ev[3]));  // previous upload finished reading h_draws
+  std::mt19937_64 g(seed);
+  for (int i = 0; i < ndraws; ++i) ctx->h_draws[i] = g();
+  CK(cudaMemcpyAsync(ctx->d_draws, ctx->h_draws, sizeof(unsigned long long) * (size_t)ndraws, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+  ctx->draws_valid = true;
+  ctx->draws_seed = seed;
+  ctx->draws_n = ndraws;
+  return CQB_OK;
+}
+
+int loop_grid(cqb_ctx* ctx) {
+  int g = ctx->loop_blocks_max;
+  if (ctx->grid_limit > 0) g = std::min(g, ctx->grid_limit);
+  return std::max(1, std::min(g, MAXBLK));
+}
+
+// Zero the small per-run state (accumulators + scalars).
+int reset_state(cqb_ctx* ctx) {
+  CK(cudaMemsetAsync(ctx->st->acc, 0, sizeof(ctx->st->acc), ctx->stream));
+  CK(cudaMemsetAsync(&ctx->st->evals, 0,
+                     sizeof(WsmState) - offsetof(WsmState, evals), ctx->stream));
+  return CQB_OK;
+}
+
+// K1 + K2 on ctx->stream over a device raster (16-B aligned).
+int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P) {
+  const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  const uint32_t ntiles = (uint32_t)((P + TILE_PX - 1) / TILE_PX);
+  CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
+  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+  k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins);
+  CKL();
+  k_hist_compact<<<ntiles, HIST_THREADS, 0, ctx->stream>>>(
+      d_img, P, ctx->bins, ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->tile_state,
+      reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles), ctx->d_n, ntiles);
+  CKL();
+  return CQB_OK;
+}
+
+int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_first, uint64_t total, double* traj,
+                int traj_cap) {
+  LoopParams L{};
+  L.keys = ctx->d_keys;
+  L.counts = ctx->d_counts;
+  L.labels = ctx->d_labels;
+  L.n_ptr = ctx->d_n;
+  L.shard_lo = 0;
+  L.shard_hi_or_max = ~0ull;
+  L.total = total;
+  L.k = k;
+  L.mode = term->mode;
+  L.max_iters = term->max_iters;
+  L.eps = term->epsilon;
+  L.cap = term->hard_cap;
+  L.dense_first = dense_first;
+  L.st = ctx->st;
+  L.sse_hist = ctx->d_hist;
+  L.hist_cap = ctx->cap_hist;
+  L.traj = traj;
+  L.traj_cap = traj_cap;
+  void* args[] = {&L};
+  CK(cudaLaunchCooperativeKernel((const void*)k_wsm_loop, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, 0,
+                                 ctx->stream));
+  CKL();
+  return CQB_OK;
+}
+
+int stage_results(cqb_ctx* ctx, int k, int hist_n) {
+  Staging* h = ctx->h_stage;
+  WsmState* st = ctx->st;
+  CK(cudaMemcpyAsync(h->centers, st->final_C, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&h->evals, &st->evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&h->mse_err, &st->mse_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&h->n_unique, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&h->sse, &st->sse, sizeof(double) + 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (hist_n > 0)
+    CK(cudaMemcpyAsync(ctx->h_hist, ctx->d_hist, sizeof(double) * (size_t)hist_n, cudaMemcpyDeviceToHost, ctx->stream));
+  return CQB_OK;
+}
+
+int check_status(cqb_ctx* ctx) {
+  const int s = ctx->h_stage->status;
+  if (s == ST_K_EXCEEDS_N)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
+  if (s == ST_DRAWS_EXHAUSTED) return fail(ctx, CQB_ERR_INTERNAL, "init_centers: raw draw buffer exhausted");
+  if (s != ST_OK) return fail(ctx, CQB_ERR_INTERNAL, "device status %d", s);
+  return CQB_OK;
+}
+
+void fill_report(cqb_ctx* ctx, int k, uint64_t seed, uint64_t total, double* centers_out, double* sse_history,
+                 int hist_cap, cqb_report* rep) {
+  const Staging* h = ctx->h_stage;
+  if (centers_out) memcpy(centers_out, h->centers, sizeof(double) * 3 * (size_t)k);
+  if (sse_history)
+    for (int i = 0; i < std::min(hist_cap, h->iterations); ++i) sse_history[i] = ctx->h_hist[i];
+  if (rep) {
+    rep->iterations = h->iterations;
+    rep->k = k;
+    rep->seed = seed;
+    rep->sse = h->sse;
+    rep->mse = total ? (double)h->mse_err / (double)total : 0.0;
+    rep->dist_evals = h->evals;
+    rep->n_unique = h->n_unique;
+    rep->empty_events = h->n_empty;
+    rep->gpu_launches = ctx->launches;
+    float ms = 0.f;
+    rep->elapsed_ms = cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess ? ms : 0.0;
+    rep->map_ms = cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]) == cudaSuccess ? ms : 0.0;
+    cudaGetLastError();
+  }
+}
+
+// The fused device pipeline: histogram -> init -> WSM loop -> map + MSE.
+#define PROF(i)                                                   \
+  do {                                                            \
+    if (ctx->profiling) CK(cudaEventRecord(ctx->pev[i], ctx->stream)); \
+  } while (0)
+
+int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, const cqb_termination* term,
+                     uint64_t seed, uint8_t* d_index, uint8_t* d_rgb_out, int ndraws) {
+  ctx->launches = 0;
+  TRY(ensure_samples(ctx, P));
+  TRY(ensure_hist(ctx, term_iters(term)));
+  TRY(upload_draws(ctx, seed, ndraws));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  PROF(0);
+  {
+    const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
+    const uint32_t ntiles = (uint32_t)((P + TILE_PX - 1) / TILE_PX);
+    CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
+    TRY(reset_state(ctx));
+    PROF(1);
+    const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins);
+    CKL();
+    PROF(2);
+    k_hist_compact<<<ntiles, HIST_THREADS, 0, ctx->stream>>>(
+        d_img, P, ctx->bins, ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->tile_state,
+        reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles), ctx->d_n, ntiles);
+    CKL();
+  }
+  PROF(3);
+  k_init_centers<<<1, 32, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
+  CKL();
+  PROF(4);
+  TRY(launch_loop(ctx, k, term, 1, P, nullptr, 0));
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  PROF(5);
+  k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->st->final_C, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
+  CKL();
+  const int gu = ctx->num_sms * 4;
+  k_map_unique<<<gu, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_counts, ctx->d_labels, ctx->d_n, k, ctx->d_sortedDr,
+                                            ctx->d_orderR, ctx->d_palkey, ctx->lut, ctx->bins, &ctx->st->mse_err, 1);
+  CKL();
+  PROF(6);
+  if (d_index || d_rgb_out) {
+    const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
+    const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+    k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->lut, ctx->d_palkey, k, d_index,
+                                                                   d_rgb_out);
+    CKL();
+  }
+  PROF(7);
+  CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  TRY(stage_results(ctx, k, term_iters(term)));
+  ctx->last_k = k;
+  ctx->last_hist_cap = term_iters(term);
+  return CQB_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int cqb_create(int device, cqb_ctx** out) {
+  cqb_ctx* ctx = nullptr;
+  if (!out) return CQB_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  ctx = new (std::nothrow) cqb_ctx();
+  if (!ctx) return CQB_ERR_OOM;
+  ctx->device = device;
+  int rc = [&]() -> int {
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      return fail(ctx, CQB_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", device,
+                  prop.major, prop.minor);
+    if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
+    ctx->num_sms = prop.multiProcessorCount;
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop, LOOP_THREADS, 0));
+    if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
+    ctx->loop_blocks_max = std::min(nb, 2) * ctx->num_sms;
+    CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    CK(cudaMalloc(&ctx->bins, sizeof(uint2) << 24));
+    CK(cudaMemset(ctx->bins, 0, sizeof(uint2) << 24));
+    CK(cudaMalloc(&ctx->lut, (size_t)1 << 24));
+    CK(cudaMalloc(&ctx->st, sizeof(WsmState)));
+    CK(cudaMemset(ctx->st, 0, sizeof(WsmState)));
+    CK(cudaMalloc(&ctx->d_n, sizeof(unsigned long long)));
+    CK(cudaMalloc(&ctx->d_centers_in, sizeof(double) * 3 * KMAX));
+    CK(cudaMalloc(&ctx->d_sortedDr, sizeof(int) * KMAX * KMAX));
+    CK(cudaMalloc(&ctx->d_orderR, KMAX * KMAX));
+    CK(cudaMalloc(&ctx->d_palkey, sizeof(uint32_t) * KMAX));
+    CK(cudaMallocHost(&ctx->h_stage, sizeof(Staging)));
+    CK(cudaMallocHost(&ctx->h_scalar, sizeof(unsigned long long) * 4));
+    for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+    for (auto& e : ctx->pev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    CK(cudaDeviceSynchronize());
+    return CQB_OK;
+  }();
+  if (rc != CQB_OK) {
+    static thread_local std::string last;
+    last = ctx->err;
+    cqb_destroy(ctx);
+    fprintf(stderr, "cqb_create: %s\n", last.c_str());
+    return rc;
+  }
+  *out = ctx;
+  return CQB_OK;
+}
+
+int cqb_destroy(cqb_ctx* ctx) {
+  if (!ctx) return CQB_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_labels, ctx->d_weights, ctx->d_n, ctx->st,
+                 ctx->d_hist, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
+                 ctx->d_draws};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (ctx->h_draws) cudaFreeHost(ctx->h_draws);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+  if (ctx->h_scalar) cudaFreeHost(ctx->h_scalar);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->pev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return CQB_OK;
+}
+
+const char* cqb_last_error(const cqb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int cqb_set_stream(cqb_ctx* ctx, void* stream) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  ctx->draws_valid = false;
+  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+  return CQB_OK;
+}
+
+int cqb_set_grid_limit(cqb_ctx* ctx, int max_blocks) {
+  if (!ctx || max_blocks < 0) return CQB_ERR_INVALID_ARGUMENT;
+  ctx->grid_limit = max_blocks;
+  return CQB_OK;
+}
+
+int cqb_set_profiling(cqb_ctx* ctx, int on) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  ctx->profiling = on != 0;
+  return CQB_OK;
+}
+
+int cqb_stage_times(cqb_ctx* ctx, float* ms, int n) {
+  if (!ctx || !ms) return CQB_ERR_INVALID_ARGUMENT;
+  if (!ctx->profiling) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "profiling is off");
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n && i < 7; ++i) CK(cudaEventElapsedTime(&ms[i], ctx->pev[i], ctx->pev[i + 1]));
+  return CQB_OK;
+}
+
+int cqb_device_info(cqb_ctx* ctx, int* num_sms, int* loop_blocks) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (loop_blocks) *loop_blocks = loop_grid(ctx);
+  return CQB_OK;
+}
+
+int cqb_build_histogram(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, uint32_t* keys, uint32_t* counts,
+                        double* weights, uint32_t* first_index, uint64_t cap, uint64_t* n_unique) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (n_pixels == 0 || !rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "build_histogram: empty image");
+  if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  CK(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  TRY(ensure_pixels(ctx, n_pixels));
+  TRY(ensure_samples(ctx, n_pixels));
+  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
+  if (weights) {
+    k_hist_weights<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_counts, ctx->d_n, n_pixels, ctx->d_weights);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  k_bins_reset<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, ctx->bins);
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
+  const uint64_t nu = ctx->h_scalar[0];
+  if (n_unique) *n_unique = nu;
+  if (nu > cap) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "output capacity %llu < N' = %llu",
+                            (unsigned long long)cap, (unsigned long long)nu);
+  if (keys) CK(cudaMemcpyAsync(keys, ctx->d_keys, 4 * nu, cudaMemcpyDeviceToHost, ctx->stream));
+  if (counts) CK(cudaMemcpyAsync(counts, ctx->d_counts, 4 * nu, cudaMemcpyDeviceToHost, ctx->stream));
+  if (first_index) CK(cudaMemcpyAsync(first_index, ctx->d_first, 4 * nu, cudaMemcpyDeviceToHost, ctx->stream));
+  if (weights) CK(cudaMemcpyAsync(weights, ctx->d_weights, 8 * nu, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CQB_OK;
+}
+
+static int run_loop_common(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* counts, uint64_t n, uint64_t total,
+                           int k, const cqb_termination* term, int dense_first, const double* centers_in,
+                           const uint8_t* labels_in, uint64_t seed, double* centers_out, double* sse_history,
+                           int hist_cap, double* trajectory, int traj_cap, uint8_t* labels_out, cqb_report* report) {
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  if (n == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "empty histogram");
+  if ((uint64_t)k > n) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
+  if (total == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "total_pixels must be > 0");
+  CK(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  TRY(ensure_samples(ctx, n));
+  TRY(ensure_hist(ctx, term_iters(term)));
+  const int tcap = trajectory ? std::min(traj_cap, term_iters(term)) : 0;
+  if (tcap > 0 && (size_t)tcap * 3 * k > ctx->cap_traj) {
+    TRY(grow(ctx, &ctx->d_traj, (size_t)tcap * 3 * k));
+    ctx->cap_traj = (size_t)tcap * 3 * k;
+  }
+  CK(cudaMemcpyAsync(ctx->d_keys, keys, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_counts, counts, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h_scalar[1] = n;
+  CK(cudaMemcpyAsync(ctx->d_n, &ctx->h_scalar[1], sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->stream));
+  if (labels_in) CK(cudaMemcpyAsync(ctx->d_labels, labels_in, n, cudaMemcpyHostToDevice, ctx->stream));
+  else CK(cudaMemsetAsync(ctx->d_labels, 0, n, ctx->stream));
+  TRY(reset_state(ctx));
+  const int ndraws = k + 64;
+  if (centers_in) {
+    CK(cudaMemcpyAsync(ctx->st->C[0], centers_in, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    TRY(upload_draws(ctx, seed, ndraws));
+  }
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (!centers_in) {
+    k_init_centers<<<1, 32, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
+    CKL();
+  }
+  TRY(launch_loop(ctx, k, term, dense_first, total, tcap ? ctx->d_traj : nullptr, tcap));
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  TRY(stage_results(ctx, k, term_iters(term)));
+  CK(cudaStreamSynchronize(ctx->stream));
+  TRY(check_status(ctx));
+  const int iters = ctx->h_stage->iterations;
+  if (tcap > 0)
+    CK(cudaMemcpy(trajectory, ctx->d_traj, sizeof(double) * 3 * (size_t)k * (size_t)std::min(tcap, iters),
+                  cudaMemcpyDeviceToHost));
+  if (labels_out) CK(cudaMemcpy(labels_out, ctx->d_labels, n, cudaMemcpyDeviceToHost));
+  fill_report(ctx, k, seed, 0, centers_out, sse_history, hist_cap, report);
+  return CQB_OK;
+}
+
+int cqb_run_wsm(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* counts, uint64_t n_unique, uint64_t total,
+                int k, const cqb_termination* term, uint64_t seed, double* centers_out, double* sse_history,
+                int hist_cap, double* trajectory, int traj_cap, uint8_t* labels_out, cqb_report* report) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  return run_loop_common(ctx, keys, counts, n_unique, total, k, term, 1, nullptr, nullptr, seed, centers_out,
+                         sse_history, hist_cap, trajectory, traj_cap, labels_out, report);
+}
+
+int cqb_wsm_iterate(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* counts, uint64_t n_unique, uint64_t total,
+                    int k, const double* centers_in, uint8_t* labels_inout, int dense_first,
+                    const cqb_termination* term, double* centers_out, double* sse_history, int hist_cap,
+                    cqb_report* report) {
+  if (!ctx || !centers_in || !labels_inout) return CQB_ERR_INVALID_ARGUMENT;
+  return run_loop_common(ctx, keys, counts, n_unique, total, k, term, dense_first, centers_in, labels_inout, 0,
+                         centers_out, sse_history, hist_cap, nullptr, 0, labels_inout, report);
+}
+
+int cqb_quantize_device(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int k, const cqb_termination* term,
+                        uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, int sync, double* centers_out,
+                        double* sse_history, int hist_cap, cqb_report* report) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  if (n_pixels == 0 || !d_rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize: empty image");
+  if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  CK(cudaSetDevice(ctx->device));
+  TRY(ensure_pixels(ctx, n_pixels));
+  const uint8_t* img = d_rgb;
+  if (!aligned16(d_rgb)) {  // vector loads need a 16-B aligned raster
+    CK(cudaMemcpyAsync(ctx->d_img2, d_rgb, 3 * n_pixels, cudaMemcpyDeviceToDevice, ctx->stream));
+    img = ctx->d_img2;
+  }
+  uint8_t* idx_out = d_index_out;
+  uint8_t* rgb_out = d_rgb_out;
+  if (idx_out && !aligned16(idx_out)) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "index output must be 16-B aligned");
+  if (rgb_out && !aligned16(rgb_out)) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "rgb output must be 16-B aligned");
+  int ndraws = k + 64;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    TRY(enqueue_quantize(ctx, img, n_pixels, k, term, seed, idx_out, rgb_out, ndraws));
+    if (!sync) return CQB_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_stage->status == ST_DRAWS_EXHAUSTED) {
+      ndraws *= 4;
+      continue;
+    }
+    break;
+  }
+  TRY(check_status(ctx));
+  fill_report(ctx, k, seed, n_pixels, centers_out, sse_history, hist_cap, report);
+  return CQB_OK;
+}
+
+int cqb_fetch_results(cqb_ctx* ctx, double* centers_out, double* sse_history, int hist_cap, cqb_report* report) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->stream));
+  TRY(check_status(ctx));
+  fill_report(ctx, ctx->last_k, ctx->draws_seed, 0, centers_out, sse_history, hist_cap, report);
+  return CQB_OK;
+}
+
+int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                 uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
+                 uint8_t* rgb_out, cqb_report* report) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (width <= 0 || height <= 0 || !rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "image dimensions must be positive");
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  const uint64_t P = (uint64_t)width * (uint64_t)height;
+  CK(cudaSetDevice(ctx->device));
+  TRY(ensure_pixels(ctx, P));
+  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  cqb_report rep{};
+  TRY(cqb_quantize_device(ctx, ctx->d_img, P, k, term, seed, index_out ? ctx->d_index : nullptr,
+                          rgb_out ? ctx->d_rgb : nullptr, 1, centers_out, sse_history, hist_cap, &rep));
+  if (index_out) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (report) *report = rep;
+  return CQB_OK;
+}
+
+int cqb_map_pixels(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, const double* centers, int k,
+                   uint8_t* rgb_out, uint8_t* index_out, uint64_t* sq_err_sum) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (k < 1 || !centers) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "map_pixels: empty palette");
+  if (k > KMAX) return fail(ctx, CQB_ERR_UNSUPPORTED, "k = %d exceeds the device limit %d", k, KMAX);
+  if (n_pixels == 0) return CQB_OK;
+  if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  CK(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  TRY(ensure_pixels(ctx, n_pixels));
+  TRY(ensure_samples(ctx, n_pixels));
+  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_centers_in, centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(&ctx->st->mse_err, 0, sizeof(unsigned long long), ctx->stream));
+  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
+  k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->d_centers_in, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
+  CKL();
+  k_map_unique<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_counts, nullptr, ctx->d_n, k,
+                                                          ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey, ctx->lut,
+                                                          ctx->bins, &ctx->st->mse_err, 1);
+  CKL();
+  const uint64_t nchunk = (n_pixels + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+  k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(ctx->d_img, n_pixels, ctx->lut, ctx->d_palkey, k,
+                                                                 index_out ? ctx->d_index : nullptr,
+                                                                 rgb_out ? ctx->d_rgb : nullptr);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_scalar, &ctx->st->mse_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  if (index_out) CK(cudaMemcpyAsync(index_out, ctx->d_index, n_pixels, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * n_pixels, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (sq_err_sum) *sq_err_sum = ctx->h_scalar[0];
+  return CQB_OK;
+}
+
+int cqb_mse(cqb_ctx* ctx, const uint8_t* a, const uint8_t* b, uint64_t n_pixels, double* out) {
+  if (!ctx || !out) return CQB_ERR_INVALID_ARGUMENT;
+  if (n_pixels == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "mse: empty images");
+  CK(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  TRY(ensure_pixels(ctx, n_pixels));
+  CK(cudaMemcpyAsync(ctx->d_img, a, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_img2, b, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(&ctx->st->mse_err, 0, sizeof(unsigned long long), ctx->stream));
+  k_mse<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_img, ctx->d_img2, 3 * n_pixels, &ctx->st->mse_err);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_scalar, &ctx->st->mse_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = (double)ctx->h_scalar[0] / (double)n_pixels;
+  return CQB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,312 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): histogram / unique colors / weights / labels /
+dist_evals / map / MSE bit-exact; centers and SSE within 1e-6 relative
+(bit-exact centers expected whenever P is a power of two — SURVEY.md §8(c)).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1011_0093_b200 import api
+from paper_1011_0093_b200.configs import CONFIGS, gmm_image, uniform_image, value_noise_image
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CENTER_RTOL = 1e-6  # BASELINE.json tolerance for centers / MSE
+SSE_RTOL = 1e-9     # moment-form SSE vs sequential FP64 sum
+
+
+def _cases():
+    return {
+        "gmm96x64": lambda: gmm_image(96, 64, 16, 7),            # P = 6144 (2^11 * 3)
+        "gmm128x64": lambda: gmm_image(128, 64, 32, 8),          # P = 8192 (power of two)
+        "gmm101x77": lambda: gmm_image(101, 77, 24, 9),          # tail pixels, odd P
+        "noise256": lambda: value_noise_image(256, 256, 11, cells=(64, 32, 16, 8)),
+        "uniform256": lambda: uniform_image(256, 256, 12),
+        "cfg1": lambda: CONFIGS["cfg1"].image(),
+        "cfg2": lambda: CONFIGS["cfg2"].image(),
+    }
+
+
+CASES = _cases()
+
+
+@pytest.fixture(scope="module")
+def images():
+    return {k: f() for k, f in CASES.items()}
+
+
+def _pow2(n):
+    return n & (n - 1) == 0
+
+
+# --------------------------------------------------------------------------- histogram
+@pytest.mark.parametrize("case", list(CASES))
+def test_histogram_bit_exact(case, images, port):
+    img = images[case]
+    h = api.build_histogram(img)
+    o = port.build_histogram(img)
+    assert h.size() == len(o.keys)
+    np.testing.assert_array_equal(h.keys, o.keys)       # first-occurrence order
+    np.testing.assert_array_equal(h.counts, o.counts)
+    np.testing.assert_array_equal(h.weights, o.weights)  # count * (1/P), bit-exact
+    flat = img.reshape(-1, 3).astype(np.uint32)
+    keys = (flat[:, 0] << 16) | (flat[:, 1] << 8) | flat[:, 2]
+    np.testing.assert_array_equal(keys[h.first_index], h.keys)
+    assert np.all(np.diff(h.first_index.astype(np.int64)) > 0)
+
+
+def test_histogram_known_answers():
+    # histogram_test.cpp:46-61
+    h1 = api.build_histogram(np.array([[[4, 5, 6]]], np.uint8))
+    assert h1.size() == 1 and h1.weights[0] == 1.0 and h1.counts[0] == 1
+    img = np.array([[[0, 0, 0], [0, 0, 0]], [[255, 255, 255], [0, 0, 0]]], np.uint8)
+    h = api.build_histogram(img)
+    assert h.size() == 2
+    assert tuple(h.colors[0]) == (0, 0, 0)
+    assert h.weights[0] == 0.75 and h.weights[1] == 0.25
+    with pytest.raises(ValueError):
+        api.build_histogram(np.zeros((0, 3), np.uint8))
+
+
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 4095, 4096, 4097, 70001])
+def test_histogram_ragged_sizes(n, port):
+    rng = np.random.default_rng(n)
+    img = rng.integers(0, 4, size=(n, 3), dtype=np.uint8) * 60  # heavy repeats + runs
+    img[: n // 3] = img[0]
+    h = api.build_histogram(img)
+    o = port.build_histogram(img)
+    np.testing.assert_array_equal(h.keys, o.keys)
+    np.testing.assert_array_equal(h.counts, o.counts)
+
+
+def test_histogram_permutation_and_repeat(port):
+    img = gmm_image(64, 64, 8, 3)
+    a = api.build_histogram(img)
+    perm = np.random.default_rng(3).permutation(img.reshape(-1, 3))
+    b = api.build_histogram(perm)
+    assert dict(zip(a.keys.tolist(), a.counts.tolist())) == dict(zip(b.keys.tolist(), b.counts.tolist()))
+    # table is returned to zero: a second call sees identical results
+    c = api.build_histogram(img)
+    np.testing.assert_array_equal(a.counts, c.counts)
+    np.testing.assert_array_equal(a.keys, c.keys)
+
+
+def test_histogram_all_colors():
+    # every 24-bit color exactly once, in key order -> N' = 2^24
+    keys = np.arange(1 << 24, dtype=np.uint32)
+    img = np.stack([(keys >> 16) & 255, (keys >> 8) & 255, keys & 255], 1).astype(np.uint8)
+    h = api.build_histogram(img)
+    assert h.size() == 1 << 24
+    np.testing.assert_array_equal(h.keys, keys)
+    assert np.all(h.counts == 1)
+
+
+# --------------------------------------------------------------------------- WSM loop
+def _run_both(img, k, port, term=("conv", 1e-4, 100), seed=1, traj=True):
+    h = api.build_histogram(img)
+    P = img.shape[0] * img.shape[1]
+    if term[0] == "conv":
+        t = api.Termination.convergent(term[1], term[2])
+        o = port.run_wsm(h.keys, h.counts, P, k, mode=1, eps=term[1], cap=term[2], seed=seed, trajectory=traj)
+    else:
+        t = api.Termination.fixed(term[1])
+        o = port.run_wsm(h.keys, h.counts, P, k, mode=0, max_iters=term[1], seed=seed, trajectory=traj)
+    g = api.run_wsm(h, k, t, seed, trajectory=traj, labels=True)
+    return h, g, o, P
+
+
+@pytest.mark.parametrize("case,k", [("gmm96x64", 8), ("gmm128x64", 16), ("gmm101x77", 32), ("noise256", 64),
+                                    ("uniform256", 256), ("cfg1", 32), ("cfg2", 64), ("cfg2", 256)])
+def test_run_wsm_matches_oracle(case, k, images, port):
+    img = images[case]
+    h, g, o, P = _run_both(img, k, port)
+    assert g.report.iterations == o.iterations
+    np.testing.assert_allclose(g.report.sse_history, o.sse_history, rtol=SSE_RTOL)
+    if _pow2(P):
+        np.testing.assert_array_equal(g.palette, o.centers)
+        np.testing.assert_array_equal(g.trajectory, o.trajectory)
+        assert g.report.dist_evals == o.dist_evals
+    else:
+        np.testing.assert_allclose(g.palette, o.centers, rtol=CENTER_RTOL)
+        np.testing.assert_allclose(g.trajectory, o.trajectory, rtol=CENTER_RTOL)
+        assert abs(g.report.dist_evals - o.dist_evals) <= 1e-6 * o.dist_evals
+
+
+def test_run_wsm_fixed_and_seeds(images, port):
+    for seed in (1, 2, 99):
+        h, g, o, P = _run_both(images["gmm128x64"], 12, port, term=("fixed", 9), seed=seed)
+        assert g.report.iterations == 9 == o.iterations
+        np.testing.assert_array_equal(g.palette, o.centers)
+        assert g.report.dist_evals == o.dist_evals
+
+
+def test_run_wsm_k_equals_n_and_k1(port):
+    img = gmm_image(16, 16, 4, 3)
+    h = api.build_histogram(img)
+    r = api.run_wsm(h, h.size(), api.Termination.convergent(), 1)
+    assert r.report.iterations == 1 and r.report.sse == 0.0  # kmeans_test.cpp:242-248
+    r1 = api.run_wsm(h, 1, api.Termination.fixed(1), 1)
+    assert r1.report.dist_evals == h.size()  # kmeans_test.cpp:102-111
+    with pytest.raises(ValueError):
+        api.run_wsm(h, h.size() + 1, api.Termination.fixed(2), 1)  # kmeans.hpp:54-56
+
+
+def test_teacher_forced_iterations(images, port, ref):
+    """Per-iteration labels and evals given the oracle's centers."""
+    img = images["gmm128x64"]
+    k = 16
+    h = api.build_histogram(img)
+    P = img.shape[0] * img.shape[1]
+    o = port.run_wsm(h.keys, h.counts, P, k, mode=0, max_iters=10, seed=5, trajectory=True, labels=True)
+    init = port.init_centers(h.keys, k, 5)
+    pairs = k * (k - 1) // 2
+    for it in range(1, 11):
+        C_in = init if it == 1 else o.trajectory[it - 2]
+        lab_in = np.zeros(h.size(), np.int32) if it == 1 else o.label_trajectory[it - 2]
+        nxt, lab, rep = api.wsm_iterate(h, C_in, lab_in, api.Termination.fixed(1), dense_first=(it == 1))
+        np.testing.assert_array_equal(lab, o.label_trajectory[it - 1])
+        np.testing.assert_array_equal(nxt, o.trajectory[it - 1])
+        _, sse, evals, _, _ = ref.sort_means_step(h.keys, h.counts, P, C_in, lab_in)
+        assert rep.dist_evals == pairs + evals
+        assert rep.sse == pytest.approx(sse, rel=SSE_RTOL)
+
+
+def test_empty_cluster_reseed(port, ref):
+    """update_centers' empty-cluster branch (kmeans.hpp:272-294)."""
+    img = gmm_image(64, 64, 6, 21)
+    h = api.build_histogram(img)
+    P = 64 * 64
+    rng = np.random.default_rng(0)
+    C_in = h.colors[rng.choice(h.size(), 8, replace=False)].copy()
+    C_in[2] = (999.0, 999.0, 999.0)   # owns nothing
+    C_in[5] = (-500.0, 0.0, 0.0)      # owns nothing
+    lab0 = np.zeros(h.size(), np.int32)
+    lab_ref, _, _, _, _ = ref.sort_means_step(h.keys, h.counts, P, C_in, lab0)
+    nxt_ref = ref.update_centers(h.keys, h.counts, P, lab_ref, C_in)
+    nxt, lab, rep = api.wsm_iterate(h, C_in, lab0, api.Termination.fixed(1))
+    np.testing.assert_array_equal(lab, lab_ref)
+    np.testing.assert_array_equal(nxt, nxt_ref)
+    assert rep.empty_events == 2
+
+
+def test_midpoint_tie_quirk(ref):
+    """Sort-means keeps p when x is the exact midpoint and t < p."""
+    keys = np.array([(10 << 16), (20 << 16), (30 << 16), (0 << 16)], np.uint32)  # r = 10, 20, 30, 0
+    counts = np.ones(4, np.uint32)
+    h = api.ColorHistogram(keys, counts, counts / 4.0, 4)
+    C_in = np.array([[10.0, 0, 0], [30.0, 0, 0], [200.0, 0, 0]])
+    lab_in = np.array([1, 1, 1, 0], np.int32)  # x = 20 is the midpoint of c0 = 10 and c1 = 30, starts at p = 1
+    lab_ref, sse, evals, _, _ = ref.sort_means_step(keys, counts, 4, C_in, lab_in)
+    _, lab, rep = api.wsm_iterate(h, C_in, lab_in, api.Termination.fixed(1))
+    np.testing.assert_array_equal(lab, lab_ref)
+    assert lab[1] == 1  # not the naive lowest index 0
+    assert rep.dist_evals == 3 + evals
+
+
+# --------------------------------------------------------------------------- map + mse
+@pytest.mark.parametrize("k", [1, 7, 64, 256])
+def test_map_pixels_matches_oracle(k, images, port):
+    img = images["noise256"]
+    rng = np.random.default_rng(k)
+    pal = rng.uniform(-3.0, 258.0, size=(k, 3))
+    pal[0] = (12.5, 99.5, 200.49999)  # half-way rounding (lround: away from zero)
+    out, idx, err = api.map_pixels_indexed(img, pal)
+    ref_out, ref_idx = port.map_pixels(img, pal)
+    np.testing.assert_array_equal(out, ref_out)
+    np.testing.assert_array_equal(idx, ref_idx)
+    assert err / (img.size // 3) == port.mse(img, ref_out)
+
+
+def test_map_pixels_edge_cases(port):
+    img = gmm_image(16, 16, 4, 3)
+    np.testing.assert_array_equal(api.map_pixels(img, np.zeros((1, 3))), np.zeros_like(img))
+    h = api.build_histogram(img)
+    np.testing.assert_array_equal(api.map_pixels(img, h.colors), img)  # imageio_test.cpp:99-105
+    with pytest.raises(ValueError):
+        api.map_pixels(img, np.zeros((0, 3)))
+    pal = np.array([[10.0, 10, 10], [10.0, 10, 10], [200.0, 0, 0]])  # duplicate entries: lowest index wins
+    _, idx, _ = api.map_pixels_indexed(img, pal)
+    assert not np.any(idx == 1)
+
+
+def test_mse_known_answers(port):
+    black = np.zeros((8, 8, 3), np.uint8)
+    white = np.full((8, 8, 3), 255, np.uint8)
+    assert api.mse(black, white) == 195075.0
+    a = gmm_image(31, 17, 5, 4)
+    b = gmm_image(31, 17, 5, 5)
+    assert api.mse(a, b) == port.mse(a, b) == api.mse(b, a)
+    with pytest.raises(ValueError):
+        api.mse(black, np.zeros((4, 4, 3), np.uint8))
+
+
+# --------------------------------------------------------------------------- end to end
+@pytest.mark.parametrize("case,k", [("gmm96x64", 16), ("gmm101x77", 8), ("cfg1", 32), ("cfg2", 256),
+                                    ("uniform256", 64)])
+def test_quantize_end_to_end(case, k, images, port):
+    img = images[case]
+    q = api.quantize(img, k, api.Termination.convergent(1e-4, 100), seed=1)
+    h = port.build_histogram(img)
+    P = img.shape[0] * img.shape[1]
+    o = port.run_wsm(h.keys, h.counts, P, k, mode=1, eps=1e-4, cap=100, seed=1)
+    assert q.report.iterations == o.iterations
+    assert q.report.n_unique == len(h.keys)
+    ref_out, ref_idx = port.map_pixels(img, o.centers)
+    if _pow2(P):
+        np.testing.assert_array_equal(q.palette, o.centers)
+        np.testing.assert_array_equal(q.mapped, ref_out)
+        np.testing.assert_array_equal(q.index_map, ref_idx)
+        assert q.report.mse == port.mse(img, ref_out)
+    else:
+        np.testing.assert_allclose(q.palette, o.centers, rtol=CENTER_RTOL)
+        assert q.report.mse == pytest.approx(port.mse(img, ref_out), rel=CENTER_RTOL)
+    # self-consistency of the fused outputs
+    mine, my_idx = port.map_pixels(img, q.palette)
+    np.testing.assert_array_equal(q.mapped, mine)
+    np.testing.assert_array_equal(q.index_map, my_idx)
+    assert q.report.mse == port.mse(img, q.mapped)
+
+
+def test_generate_palette_api(images):
+    img = images["gmm96x64"]
+    a = api.generate_palette(img, api.MethodParams("wsm-c"), 16, 1)
+    b = api.generate_palette(img, api.MethodParams("wsm-c"), 16, 1)
+    np.testing.assert_array_equal(a.palette, b.palette)  # cli_test.cpp:123-130 determinism
+    assert a.report.method == "wsm-c"
+    with pytest.raises(api.UnknownMethodError):
+        api.generate_palette(img, api.MethodParams("mc"), 16, 1)
+    with pytest.raises(ValueError):
+        api.generate_palette(img, api.MethodParams("wsm"), 0, 1)
+
+
+def test_cpp_shim():
+    exe = os.path.join(ROOT, "build", "shim_test")
+    assert os.path.exists(exe), "build/shim_test missing (run make)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+# --------------------------------------------------------------------------- full-size properties
+@pytest.mark.slow
+def test_cfg4_properties(port):
+    img = CONFIGS["cfg4"].image()
+    P = img.shape[0] * img.shape[1]
+    h = api.build_histogram(img)
+    o = port.build_histogram(img)
+    np.testing.assert_array_equal(h.keys, o.keys)
+    np.testing.assert_array_equal(h.counts, o.counts)
+    assert int(h.counts.sum(dtype=np.uint64)) == P
+    q = api.quantize(img, 256, api.Termination.convergent(1e-4, 100), seed=1)
+    assert q.report.n_unique == h.size()
+    hist = np.array(q.report.sse_history)
+    assert np.all(np.diff(hist) <= 1e-9 * hist[:-1])  # SSE nonincreasing
+    # mapping is idempotent and consistent with the palette
+    again, idx2, _ = api.map_pixels_indexed(q.mapped, q.palette)
+    np.testing.assert_array_equal(again, q.mapped)
+    assert q.report.mse == pytest.approx(api.mse(img, q.mapped), rel=0, abs=0)
