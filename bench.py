@@ -218,7 +218,9 @@ def measure_device(lib, ctx, torch, d_img, P, k, steps, warmup, stream, flush, p
             if profile:
                 ms = (C.c_float * 7)()
                 ctx.check(lib.cqb_stage_times(ctx.h, ms, 7))
-                stage.append(list(ms))
+                tl = np.zeros(5 * HARD_CAP, np.uint64)
+                ctx.check(lib.cqb_loop_timeline(ctx.h, tl.ctypes.data_as(C.POINTER(C.c_uint64)), HARD_CAP))
+                stage.append((list(ms), tl.reshape(HARD_CAP, 5).astype(np.int64)))
     torch.cuda.synchronize()
     for a, b in evs:
         times.append(a.elapsed_time(b))
@@ -276,11 +278,12 @@ def run_ours(a, cfg, world, rank, local):
     _, stage, rep_p, _, _ = measure_device(lib, ctx, torch, d_img, P, k, max(3, min(a.steps, 5)), 1, stream, flush,
                                            profile=True)
     ctx.check(lib.cqb_set_profiling(ctx.h, 0))
-    st = np.median(np.array(stage), axis=0)
+    st = np.median(np.array([x[0] for x in stage]), axis=0)
     names = N.STAGES
     stage_ms = {n: float(v) for n, v in zip(names, st)}
     n_unique = int(rep.n_unique)
     iters = int(rep.iterations)
+    phases = _loop_phases(stage[-1][1], iters)
     peaks = _peaks()
     dom = max(stage_ms, key=stage_ms.get)
     roof = _roofline(dom, stage_ms[dom], P, n_unique, iters, k, peaks, int(rep.dist_evals))
@@ -330,6 +333,7 @@ def run_ours(a, cfg, world, rank, local):
             "gpu_launches": launches,
             "roofline": roof,
             "stages_ms": {kk: round(v, 5) for kk, v in stage_ms.items()},
+            "loop_phases_us": phases,
             "dist_evals": int(rep.dist_evals),
             "clocks": clk,
         }
@@ -355,15 +359,38 @@ def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
     ctx.check(lib.cqb_set_profiling(ctx.h, 1))
     _, stage, _, _, _ = measure_device(lib, ctx, torch, d, cfg.pixels, 256, 2, 0, stream, flush, profile=True)
     ctx.check(lib.cqb_set_profiling(ctx.h, 0))
-    st = np.median(np.array(stage), axis=0)
+    st = np.median(np.array([x[0] for x in stage]), axis=0)
     stage_ms = {n: float(v) for n, v in zip(N.STAGES, st)}
+    phases = _loop_phases(stage[-1][1], int(rep.iterations))
     ms = sum(times) / len(times)
     dom = max(stage_ms, key=stage_ms.get)
     return {"workload": _workload(cfg, 256), "value": cfg.pixels / (ms * 1e-3) / 1e6, "unit": "Mpixel/s",
             "ms_per_step": ms, "n_unique": int(rep.n_unique), "iterations": int(rep.iterations),
             "dist_evals": int(rep.dist_evals), "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "loop_phases_us": phases,
             "roofline": _roofline(dom, stage_ms[dom], cfg.pixels, int(rep.n_unique), int(rep.iterations), 256, peaks,
                                   int(rep.dist_evals))}
+
+
+def _loop_phases(tl, iters):
+    """Mean per-iteration phase durations (us) from the loop's globaltimer stamps:
+    assign+flush, grid barrier 1, finalize, tables, grid barrier 2."""
+    tl = tl[:iters]
+    if iters < 2 or not tl[:, 0].all():
+        return None
+    first = {"assign_us": float(tl[0, 1] - tl[0, 0]) / 1e3}
+    a = tl[1:]
+    nxt0 = tl[1:, 0]
+    prev = tl[:-1]
+    return {
+        "iter1_assign_us": first["assign_us"],
+        "assign_us": float(np.mean(a[:, 1] - a[:, 0])) / 1e3,
+        "barrier1_us": float(np.mean(a[:, 2] - a[:, 1])) / 1e3,
+        "finalize_us": float(np.mean(prev[:, 3] - prev[:, 2])) / 1e3,
+        "tables_us": float(np.mean(prev[:, 4] - prev[:, 3])) / 1e3,
+        "barrier2_us": float(np.mean(nxt0 - prev[:, 4])) / 1e3,
+        "iteration_us": float(np.mean(np.diff(tl[:, 0]))) / 1e3,
+    }
 
 
 def _peaks():

@@ -79,6 +79,10 @@ int cqb_device_info(cqb_ctx* ctx, int* num_sms, int* loop_blocks);
  * unique-color map + MSE, [6] per-pixel map. */
 int cqb_set_profiling(cqb_ctx* ctx, int on);
 int cqb_stage_times(cqb_ctx* ctx, float* ms, int n);
+/* With profiling on: %globaltimer stamps (ns) of block 0 per WSM iteration,
+ * 5 per iteration: assign start, deltas flushed, barrier passed, finalize
+ * done, tables done. */
+int cqb_loop_timeline(cqb_ctx* ctx, unsigned long long* stamps, int n_iters);
 
 /* ---- histogram ---------------------------------------------------------
  * Replaces build_histogram(const RgbImage&) (histogram.hpp:65-99,105-108).

@@ -59,6 +59,7 @@ struct cqb_ctx {
   WsmState* st = nullptr;
   double* d_hist = nullptr;
   int cap_hist = 0;
+  unsigned long long* d_timeline = nullptr;  // 5 stamps per iteration (profiling)
   double* d_traj = nullptr;
   size_t cap_traj = 0;
   double* d_centers_in = nullptr;
@@ -159,6 +160,7 @@ int ensure_samples(cqb_ctx* ctx, size_t n) {
 int ensure_hist(cqb_ctx* ctx, int n) {
   if (n <= ctx->cap_hist) return CQB_OK;
   TRY(grow(ctx, &ctx->d_hist, (size_t)n));
+  TRY(grow(ctx, &ctx->d_timeline, (size_t)n * 5));
   if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
   ctx->h_hist = nullptr;
   CK(cudaMallocHost(&ctx->h_hist, sizeof(double) * (size_t)n));
@@ -261,6 +263,7 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.hist_cap = ctx->cap_hist;
   L.traj = traj;
   L.traj_cap = traj_cap;
+  L.timeline = ctx->profiling ? ctx->d_timeline : nullptr;
   void* args[] = {&L};
   CK(cudaLaunchCooperativeKernel((const void*)k_wsm_loop, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, 0,
                                  ctx->stream));
@@ -343,7 +346,7 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
     CKL();
   }
   PROF(3);
-  k_init_centers<<<1, 32, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
+  k_init_centers<<<1, KMAX, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
   CKL();
   PROF(4);
   TRY(launch_loop(ctx, k, term, 1, P, nullptr, 0));
@@ -434,7 +437,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
                  ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_labels, ctx->d_weights, ctx->d_n, ctx->st,
-                 ctx->d_hist, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
+                 ctx->d_hist, ctx->d_timeline, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
                  ctx->d_draws};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -482,6 +485,15 @@ int cqb_stage_times(cqb_ctx* ctx, float* ms, int n) {
   return CQB_OK;
 }
 
+int cqb_loop_timeline(cqb_ctx* ctx, unsigned long long* stamps, int n_iters) {
+  if (!ctx || !stamps) return CQB_ERR_INVALID_ARGUMENT;
+  if (!ctx->profiling) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "profiling is off");
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int n = std::min(n_iters, ctx->cap_hist);
+  CK(cudaMemcpy(stamps, ctx->d_timeline, sizeof(unsigned long long) * 5 * (size_t)n, cudaMemcpyDeviceToHost));
+  return CQB_OK;
+}
+
 int cqb_device_info(cqb_ctx* ctx, int* num_sms, int* loop_blocks) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
   if (num_sms) *num_sms = ctx->num_sms;
@@ -524,10 +536,11 @@ static int run_loop_common(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* c
                            int k, const cqb_termination* term, int dense_first, const double* centers_in,
                            const uint8_t* labels_in, uint64_t seed, double* centers_out, double* sse_history,
                            int hist_cap, double* trajectory, int traj_cap, uint8_t* labels_out, cqb_report* report) {
-  TRY(check_k(ctx, k));
-  TRY(check_term(ctx, term));
+  if (k < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k must be >= 1");
   if (n == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "empty histogram");
   if ((uint64_t)k > n) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
   if (total == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "total_pixels must be > 0");
   CK(cudaSetDevice(ctx->device));
   ctx->launches = 0;
@@ -553,7 +566,7 @@ static int run_loop_common(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* c
   }
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (!centers_in) {
-    k_init_centers<<<1, 32, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
+    k_init_centers<<<1, KMAX, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
     CKL();
   }
   TRY(launch_loop(ctx, k, term, dense_first, total, tcap ? ctx->d_traj : nullptr, tcap));

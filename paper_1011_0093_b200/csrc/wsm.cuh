@@ -5,7 +5,7 @@
 // One cooperative persistent kernel runs the whole iteration loop:
 //
 //   prologue : tables(C_1)                                   | grid.sync
-//   iter it  : assign(it)  -> per-block u64 moments -> acc[it&1] | grid.sync
+//   iter it  : assign(it)  -> per-block exact moment deltas -> acc | grid.sync
 //              finalize(it) redundantly in EVERY block (new centers, empty
 //              reseed, moment-form SSE, termination) + tables(C_{it+1})
 //                                                            | grid.sync
@@ -36,7 +36,7 @@ namespace cg = cooperative_groups;
 
 struct WsmState {
   double C[2][3 * KMAX];                  // center buffers [k*3 + ch]
-  unsigned long long acc[2][5 * KMAX];    // [field*KMAX + k]: Sr, Sg, Sb, N, Q
+  unsigned long long acc[5 * KMAX];       // exact sums [field*KMAX + k]: Sr, Sg, Sb, N, Q
   double sortedD[KMAX * KMAX];            // row p: d(c_p, c_order[p][j]) ascending
   uint8_t order[KMAX * KMAX];             // row p: [p, others by (d, index)]
   double final_C[3 * KMAX];
@@ -70,75 +70,85 @@ struct LoopParams {
   int hist_cap;
   double* traj;
   int traj_cap;
+  unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (5 per iteration)
 };
 
 // ---------------------------------------------------------------------------
 // init_centers on device (kmeans.hpp:53-70): partial Fisher–Yates over
 // iota(N') using the raw mt19937_64 stream computed on the host (the stream is
-// independent of N'); bounded_rand's rejection + modulo (:43-49) run here, so
-// nothing waits for N' on the host. Positions >= k live in a small swap map.
-__global__ void k_init_centers(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ n_ptr,
-                               int k, const unsigned long long* __restrict__ draws, int ndraws, WsmState* st) {
+// independent of N'). bounded_rand's rejection + modulo (:43-49) are evaluated
+// for all k draws in parallel (a rejection, probability < N'/2^64 per draw,
+// diverts to the exact sequential path); the k swaps then run in one thread
+// with positions >= k held in a small open-addressing map.
+__global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restrict__ keys,
+                                                      const unsigned long long* __restrict__ n_ptr, int k,
+                                                      const unsigned long long* __restrict__ draws, int ndraws,
+                                                      WsmState* st) {
+  constexpr int HS = 2 * KMAX;  // hash slots for positions >= k
+  __shared__ unsigned long long jv[KMAX];
   __shared__ uint32_t lowv[KMAX];
-  __shared__ unsigned long long mpos[KMAX];
-  __shared__ uint32_t mval[KMAX];
-  __shared__ int msize;
-  const int lane = threadIdx.x;
+  __shared__ unsigned long long hpos[HS];
+  __shared__ uint32_t hval[HS];
+  __shared__ int s_rejected;
+  const int tid = threadIdx.x;
   const unsigned long long n = *n_ptr;
   if ((unsigned long long)k > n) {
-    if (lane == 0) st->status = ST_K_EXCEEDS_N;
+    if (tid == 0) st->status = ST_K_EXCEEDS_N;
     return;
   }
-  for (int i = lane; i < k; i += 32) lowv[i] = (uint32_t)i;
-  if (lane == 0) msize = 0;
-  __syncwarp();
-  int di = 0;
-  for (int i = 0; i < k; ++i) {
+  if (tid == 0) s_rejected = 0;
+  for (int h = tid; h < HS; h += blockDim.x) hpos[h] = ~0ull;
+  __syncthreads();
+  for (int i = tid; i < k; i += blockDim.x) {
+    lowv[i] = (uint32_t)i;
     const unsigned long long bound = n - (unsigned long long)i;
     const unsigned long long limit = ~0ull - (~0ull % bound);
-    unsigned long long r;
-    do {
-      if (di >= ndraws) {
-        if (lane == 0) st->status = ST_DRAWS_EXHAUSTED;
-        return;
-      }
-      r = draws[di++];
-    } while (r >= limit);
-    const unsigned long long j = (unsigned long long)i + r % bound;
-    const uint32_t vi = lowv[i];
-    uint32_t vj;
-    if (j < (unsigned long long)k) {
-      vj = lowv[j];
-      __syncwarp();
-      if (lane == 0) lowv[j] = vi;
-    } else {
-      const int ms = msize;
-      int found = -1;
-      for (int b = 0; b < ms; b += 32) {
-        const int e = b + lane;
-        const unsigned hit = __ballot_sync(0xffffffffu, e < ms && mpos[e] == j);
-        if (hit) {
-          found = b + __ffs(hit) - 1;
-          break;
-        }
-      }
-      vj = found >= 0 ? mval[found] : (uint32_t)j;
-      __syncwarp();
-      if (lane == 0) {
-        if (found >= 0) {
-          mval[found] = vi;
-        } else {
-          mpos[ms] = j;
-          mval[ms] = vi;
-          msize = ms + 1;
-        }
+    const unsigned long long r = i < ndraws ? draws[i] : ~0ull;
+    if (r >= limit) s_rejected = 1;
+    jv[i] = (unsigned long long)i + r % bound;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (s_rejected) {  // exact sequential draw consumption
+      int di = 0;
+      for (int i = 0; i < k; ++i) {
+        const unsigned long long bound = n - (unsigned long long)i;
+        const unsigned long long limit = ~0ull - (~0ull % bound);
+        unsigned long long r;
+        do {
+          if (di >= ndraws) {
+            st->status = ST_DRAWS_EXHAUSTED;
+            s_rejected = 2;
+            break;
+          }
+          r = draws[di++];
+        } while (r >= limit);
+        if (s_rejected == 2) break;
+        jv[i] = (unsigned long long)i + r % bound;
       }
     }
-    __syncwarp();
-    if (lane == 0) lowv[i] = vj;
-    __syncwarp();
+    if (s_rejected != 2) {
+      for (int i = 0; i < k; ++i) {
+        const unsigned long long j = jv[i];
+        const uint32_t vi = lowv[i];
+        uint32_t vj;
+        if (j < (unsigned long long)k) {
+          vj = lowv[j];
+          lowv[j] = vi;
+        } else {
+          int h = (int)((j * 0x9E3779B97F4A7C15ull) >> 55);  // 9 bits -> [0, 512)
+          while (hpos[h] != ~0ull && hpos[h] != j) h = (h + 1) & (HS - 1);
+          vj = hpos[h] == j ? hval[h] : (uint32_t)j;
+          hpos[h] = j;
+          hval[h] = vi;
+        }
+        lowv[i] = vj;
+      }
+    }
   }
-  for (int i = lane; i < k; i += 32) {
+  __syncthreads();
+  if (s_rejected == 2) return;
+  for (int i = tid; i < k; i += blockDim.x) {
     const uint32_t key = keys[lowv[i]];
     st->C[0][3 * i + 0] = (double)key_r(key);
     st->C[0][3 * i + 1] = (double)key_g(key);
@@ -149,23 +159,35 @@ __global__ void k_init_centers(const uint32_t* __restrict__ keys, const unsigned
 
 // ---------------------------------------------------------------------------
 // Shared-memory working set of one persistent block.
+//
+// Cluster moments are accumulated as exact integers in TWO per-block arrays
+// (plus / minus) of u64 values split into (lo, hi) u32 words: shared-memory
+// 64-bit atomics are CAS loops on sm_100a, 32-bit ones are native, and the
+// carry out of `lo` is propagated by the thread that produced it. From the
+// second iteration of a launch only points whose label CHANGED touch the
+// accumulators (subtract from the old cluster, add to the new one), so the
+// per-iteration atomic work falls with the label churn (a few % of N').
 struct LoopSmem {
   double cx[KMAX], cy[KMAX], cz[KMAX];   // centers of the current assignment
   double nx[KMAX], ny[KMAX], nz[KMAX];   // next centers (finalize)
-  unsigned long long acc[5 * KMAX];      // block-local exact moments
+  uint2 accp[5 * KMAX];                  // block-local moment deltas (+)
+  uint2 accm[5 * KMAX];                  // block-local moment deltas (-)
   int2 cb[KMAX];                         // dense path: {packed center, cc*256 + k}
   uint32_t row0[KMAX];                   // dense path: sorted d(c_0, .) as integers
   double rowd[KMAX];                     // tables scratch
   double red_hi[LOOP_THREADS / 32], red_lo[LOOP_THREADS / 32];
   int red_i[LOOP_THREADS / 32];
-  unsigned long long red_u[LOOP_THREADS / 32];
   int empty_list[KMAX];
   unsigned int taken[KMAX];
   int n_empty;
-  int stop;
   double sse;
-  unsigned long long evals;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Row p of the center tables (kmeans.hpp:147-168): d[p][t] = dist2(c_p, c_t)
 // and the order row [p, others sorted by (d, index)] by rank counting.
@@ -189,17 +211,26 @@ __device__ void tables_row(LoopSmem& S, WsmState* st, int p, int k) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void acc_add(LoopSmem& S, int k, uint32_t key, uint32_t cnt) {
-  const unsigned long long c = cnt;
-  const uint32_t r = key_r(key), g = key_g(key), b = key_b(key);
-  atomicAdd(&S.acc[0 * KMAX + k], c * r);
-  atomicAdd(&S.acc[1 * KMAX + k], c * g);
-  atomicAdd(&S.acc[2 * KMAX + k], c * b);
-  atomicAdd(&S.acc[3 * KMAX + k], c);
-  atomicAdd(&S.acc[4 * KMAX + k], c * (unsigned long long)(r * r + g * g + b * b));
+// u64 += v on a (lo, hi) pair of shared u32 words, native 32-bit atomics only.
+__device__ __forceinline__ void sadd64(uint2* a, unsigned long long v) {
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(&a->x, lo);
+  const uint32_t c = (uint32_t)(old + lo) < old ? 1u : 0u;
+  if (hi + c) atomicAdd(&a->y, hi + c);
 }
 
-// Iteration 1, dense + integer-exact (see header).
+// The five exact moments of one sample: Σc·r, Σc·g, Σc·b, Σc, Σc·|x|².
+__device__ __forceinline__ void acc_point(uint2* acc, int k, uint32_t key, uint32_t cnt) {
+  const unsigned long long c = cnt;
+  const uint32_t r = key_r(key), g = key_g(key), b = key_b(key);
+  sadd64(&acc[0 * KMAX + k], c * r);
+  sadd64(&acc[1 * KMAX + k], c * g);
+  sadd64(&acc[2 * KMAX + k], c * b);
+  sadd64(&acc[3 * KMAX + k], c);
+  sadd64(&acc[4 * KMAX + k], c * (unsigned long long)(r * r + g * g + b * b));
+}
+
+// Iteration 1, dense + integer-exact (see header). Full accumulation.
 __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned long long lo, unsigned long long hi,
                                    unsigned long long& evals) {
   const int k = L.k;
@@ -239,17 +270,17 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
         }
         evals += (unsigned long long)lo_j;  // 1 (prev) + (lo_j - 1) candidates
         L.labels[i] = (uint8_t)lab;
-        acc_add(S, lab, x[q], L.counts[i]);
+        acc_point(S.accp, lab, x[q], L.counts[i]);
       }
     }
   }
 }
 
-// Iterations >= 2: FP64 sort-means scan from the previous label
-// (kmeans.hpp:211-236), tables in L2 (written by this kernel, read after the
-// grid barrier with coherent loads).
+// Iterations >= 2 (or the first of a teacher-forced launch, full = true):
+// FP64 sort-means scan from the previous label (kmeans.hpp:211-236); tables
+// in L2 (written by this kernel, read after the grid barrier).
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned long long lo, unsigned long long hi,
-                                  unsigned long long& evals) {
+                                  bool full, unsigned long long& evals) {
   const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
   const double* __restrict__ sd = L.st->sortedD;
   const uint8_t* __restrict__ od = L.st->order;
@@ -277,8 +308,15 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       }
     }
     evals += ev;
-    L.labels[i] = (uint8_t)best;
-    acc_add(S, best, key, L.counts[i]);
+    if (full) {
+      if (best != p) L.labels[i] = (uint8_t)best;
+      acc_point(S.accp, best, key, L.counts[i]);
+    } else if (best != p) {
+      L.labels[i] = (uint8_t)best;
+      const uint32_t cnt = L.counts[i];
+      acc_point(S.accm, p, key, cnt);
+      acc_point(S.accp, best, key, cnt);
+    }
   }
 }
 
@@ -388,6 +426,18 @@ __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& g
   }
 }
 
+// Flush the block's moment deltas into the global exact sums (u64, modular).
+__device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
+  for (int e = threadIdx.x; e < 5 * KMAX; e += blockDim.x) {
+    if ((e & (KMAX - 1)) >= k) continue;
+    const uint2 a = S.accp[e], m = S.accm[e];
+    const unsigned long long d = ((unsigned long long)a.y << 32 | a.x) - ((unsigned long long)m.y << 32 | m.x);
+    if (d) atomicAdd(&gacc[e], d);
+    S.accp[e] = make_uint2(0u, 0u);
+    S.accm[e] = make_uint2(0u, 0u);
+  }
+}
+
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
 __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
   __shared__ LoopSmem S;
@@ -400,13 +450,19 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
   const unsigned long long lo = L.shard_lo < n ? L.shard_lo : n;
   const unsigned long long hi = L.shard_hi_or_max < n ? L.shard_hi_or_max : n;
   const double inv_P = 1.0 / (double)L.total;
+  unsigned long long* gacc = st->acc;  // exact running sums (zeroed by the host per launch)
+  unsigned long long* tl = L.timeline;
+  const bool rec = tl && blockIdx.x == 0 && tid == 0;
 
   for (int t = tid; t < k; t += blockDim.x) {
     S.cx[t] = st->C[0][3 * t];
     S.cy[t] = st->C[0][3 * t + 1];
     S.cz[t] = st->C[0][3 * t + 2];
   }
-  for (int t = tid; t < 5 * KMAX; t += blockDim.x) S.acc[t] = 0ull;
+  for (int t = tid; t < 5 * KMAX; t += blockDim.x) {
+    S.accp[t] = make_uint2(0u, 0u);
+    S.accm[t] = make_uint2(0u, 0u);
+  }
   __syncthreads();
   // prologue: tables of the initial centers (all pairs evaluated: non-incremental)
   for (int p = blockIdx.x; p < k; p += gridDim.x) tables_row(S, st, p, k);
@@ -415,6 +471,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
 
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   for (int it = 1;; ++it) {
+    const bool rec_it = rec && it <= L.hist_cap;
+    if (rec_it) tl[(it - 1) * 5 + 0] = globaltimer();
     // ---------------- assign(it) ----------------
     unsigned long long evals = 0;
     if (it == 1 && L.dense_first) {
@@ -426,22 +484,15 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
       __syncthreads();
       assign_dense_first(S, L, lo, hi, evals);
     } else {
-      assign_sort_means(S, L, lo, hi, evals);
+      assign_sort_means(S, L, lo, hi, it == 1, evals);
     }
     evals = warp_sum(evals);
     if ((tid & 31) == 0 && evals) atomicAdd(&st->evals, evals);
     __syncthreads();
-    unsigned long long* gacc = st->acc[it & 1];
-    for (int t = tid; t < k; t += blockDim.x) {
-      if (S.acc[3 * KMAX + t]) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) {
-          atomicAdd(&gacc[f * KMAX + t], S.acc[f * KMAX + t]);
-          S.acc[f * KMAX + t] = 0ull;
-        }
-      }
-    }
+    flush_moments(S, gacc, k);
+    if (rec_it) tl[(it - 1) * 5 + 1] = globaltimer();
     grid.sync();
+    if (rec_it) tl[(it - 1) * 5 + 2] = globaltimer();
 
     // ---------------- finalize(it), redundantly per block ----------------
     dd part{0.0, 0.0};
@@ -526,11 +577,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
       S.cy[t] = S.ny[t];
       S.cz[t] = S.nz[t];
     }
-    // zero the accumulator the NEXT assign will use (last read in finalize(it-1))
-    unsigned long long* nacc = st->acc[(it + 1) & 1];
-    for (int t = blockIdx.x * blockDim.x + tid; t < 5 * KMAX; t += gridDim.x * blockDim.x) nacc[t] = 0ull;
     __syncthreads();
+    if (rec_it) tl[(it - 1) * 5 + 3] = globaltimer();
     for (int p = blockIdx.x; p < k; p += gridDim.x) tables_row(S, st, p, k);
+    if (rec_it) tl[(it - 1) * 5 + 4] = globaltimer();
     grid.sync();
   }
 }
