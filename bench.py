@@ -218,9 +218,9 @@ def measure_device(lib, ctx, torch, d_img, P, k, steps, warmup, stream, flush, p
             if profile:
                 ms = (C.c_float * 7)()
                 ctx.check(lib.cqb_stage_times(ctx.h, ms, 7))
-                tl = np.zeros(5 * HARD_CAP, np.uint64)
+                tl = np.zeros(8 * HARD_CAP, np.uint64)
                 ctx.check(lib.cqb_loop_timeline(ctx.h, tl.ctypes.data_as(C.POINTER(C.c_uint64)), HARD_CAP))
-                stage.append((list(ms), tl.reshape(HARD_CAP, 5).astype(np.int64)))
+                stage.append((list(ms), tl.reshape(HARD_CAP, 8).astype(np.int64)))
     torch.cuda.synchronize()
     for a, b in evs:
         times.append(a.elapsed_time(b))
@@ -373,23 +373,28 @@ def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
 
 
 def _loop_phases(tl, iters):
-    """Mean per-iteration phase durations (us) from the loop's globaltimer stamps:
-    assign+flush, grid barrier 1, finalize, tables, grid barrier 2."""
+    """Mean per-iteration phase durations (us) of block 0 from the loop's
+    globaltimer stamps (iterations >= 2; iteration 1 reported separately)."""
     tl = tl[:iters]
-    if iters < 2 or not tl[:, 0].all():
+    if iters < 3 or not tl[:, 0].all():
         return None
-    first = {"assign_us": float(tl[0, 1] - tl[0, 0]) / 1e3}
-    a = tl[1:]
-    nxt0 = tl[1:, 0]
-    prev = tl[:-1]
+    a = tl[1:-1]
+    nxt = tl[2:, 0]
+    d = lambda x, y: float(np.mean(y - x)) / 1e3  # noqa: E731
     return {
-        "iter1_assign_us": first["assign_us"],
-        "assign_us": float(np.mean(a[:, 1] - a[:, 0])) / 1e3,
-        "barrier1_us": float(np.mean(a[:, 2] - a[:, 1])) / 1e3,
-        "finalize_us": float(np.mean(prev[:, 3] - prev[:, 2])) / 1e3,
-        "tables_us": float(np.mean(prev[:, 4] - prev[:, 3])) / 1e3,
-        "barrier2_us": float(np.mean(nxt0 - prev[:, 4])) / 1e3,
-        "iteration_us": float(np.mean(np.diff(tl[:, 0]))) / 1e3,
+        "iter1_assign_us": float(tl[0, 3] - tl[0, 0]) / 1e3,
+        "stage_rows_us": d(a[:, 0], a[:, 1]),
+        "points_us": d(a[:, 1], a[:, 2]),
+        "flush_us": d(a[:, 2], a[:, 3]),
+        "barrier1_us": d(a[:, 3], a[:, 4]),
+        "finalize_us": d(a[:, 4], a[:, 5]),
+        "tables_us": d(a[:, 5], a[:, 6]),
+        "barrier2_us": d(a[:, 6], nxt),
+        "iteration_us": float(np.mean(np.diff(tl[1:, 0]))) / 1e3,
+        "changed_per_iter": [int(v) & 0xFFFFFFFF for v in tl[1:8, 7]],
+        "deep_per_iter": [int(v) >> 32 for v in tl[1:8, 7]],
+        "changed_mean": float(np.mean(tl[1:, 7] & 0xFFFFFFFF)),
+        "deep_mean": float(np.mean(tl[1:, 7] >> 32)),
     }
 
 

@@ -80,9 +80,12 @@ int cqb_device_info(cqb_ctx* ctx, int* num_sms, int* loop_blocks);
 int cqb_set_profiling(cqb_ctx* ctx, int on);
 int cqb_stage_times(cqb_ctx* ctx, float* ms, int n);
 /* With profiling on: %globaltimer stamps (ns) of block 0 per WSM iteration,
- * 5 per iteration: assign start, deltas flushed, barrier passed, finalize
- * done, tables done. */
+ * 8 per iteration: assign start, rows staged, points done, deltas flushed,
+ * barrier passed, finalize done, tables done, (reserved). */
 int cqb_loop_timeline(cqb_ctx* ctx, unsigned long long* stamps, int n_iters);
+/* With profiling on: per-block finish stamps of the assign phase for the
+ * first 8 iterations, [iteration][block] (load-balance diagnostics). */
+int cqb_block_times(cqb_ctx* ctx, unsigned long long* out, int n);
 
 /* ---- histogram ---------------------------------------------------------
  * Replaces build_histogram(const RgbImage&) (histogram.hpp:65-99,105-108).

@@ -27,7 +27,7 @@ EXPORTS = (
     "cqb_create", "cqb_destroy", "cqb_last_error", "cqb_set_stream", "cqb_set_grid_limit", "cqb_device_info",
     "cqb_build_histogram", "cqb_run_wsm", "cqb_wsm_iterate", "cqb_quantize", "cqb_quantize_device",
     "cqb_fetch_results", "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
-    "cqb_loop_timeline",
+    "cqb_loop_timeline", "cqb_block_times",
 )
 STAGES = ("reset", "hist_count", "hist_compact", "init", "wsm_loop", "map_unique", "map_pixels")
 
@@ -97,6 +97,7 @@ def load_library() -> C.CDLL:
         L.cqb_set_profiling.argtypes = [_vp, C.c_int]
         L.cqb_stage_times.argtypes = [_vp, C.POINTER(C.c_float), C.c_int]
         L.cqb_loop_timeline.argtypes = [_vp, _u64p, C.c_int]
+        L.cqb_block_times.argtypes = [_vp, _u64p, C.c_int]
         _lib = L
         return L
 

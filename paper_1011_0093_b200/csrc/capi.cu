@@ -52,14 +52,20 @@ struct cqb_ctx {
   uint32_t* d_keys = nullptr;
   uint32_t* d_counts = nullptr;
   uint32_t* d_first = nullptr;
-  uint8_t* d_labels = nullptr;
+  uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
+  uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
+  uint32_t* d_mkeys = nullptr;    // Morton-ordered samples (K2b)
+  uint32_t* d_mcounts = nullptr;
+  uint32_t* d_mrank = nullptr;
+  unsigned long long* bin_tile_state = nullptr;  // K2b look-back [N_BIN_TILES] + ticket
   double* d_weights = nullptr;
   unsigned long long* d_n = nullptr;  // N'
 
   WsmState* st = nullptr;
   double* d_hist = nullptr;
   int cap_hist = 0;
-  unsigned long long* d_timeline = nullptr;  // 5 stamps per iteration (profiling)
+  unsigned long long* d_timeline = nullptr;  // 8 stamps per iteration (profiling)
+  unsigned long long* d_block_times = nullptr;  // [8 iterations][MAXBLK] (profiling)
   double* d_traj = nullptr;
   size_t cap_traj = 0;
   double* d_centers_in = nullptr;
@@ -79,6 +85,7 @@ struct cqb_ctx {
   unsigned long long* h_scalar = nullptr;
   cudaEvent_t ev[4] = {};
   bool profiling = false;
+  int stamp_iter = 3;
   cudaEvent_t pev[8] = {};  // stage boundaries when profiling
   int last_k = 0;
   int last_hist_cap = 0;
@@ -152,6 +159,10 @@ int ensure_samples(cqb_ctx* ctx, size_t n) {
   TRY(grow(ctx, &ctx->d_counts, cap));
   TRY(grow(ctx, &ctx->d_first, cap));
   TRY(grow(ctx, &ctx->d_labels, cap));
+  TRY(grow(ctx, &ctx->d_lab_rank, cap));
+  TRY(grow(ctx, &ctx->d_mkeys, cap));
+  TRY(grow(ctx, &ctx->d_mcounts, cap));
+  TRY(grow(ctx, &ctx->d_mrank, cap));
   TRY(grow(ctx, &ctx->d_weights, cap));
   ctx->cap_s = cap;
   return CQB_OK;
@@ -160,7 +171,7 @@ int ensure_samples(cqb_ctx* ctx, size_t n) {
 int ensure_hist(cqb_ctx* ctx, int n) {
   if (n <= ctx->cap_hist) return CQB_OK;
   TRY(grow(ctx, &ctx->d_hist, (size_t)n));
-  TRY(grow(ctx, &ctx->d_timeline, (size_t)n * 5));
+  TRY(grow(ctx, &ctx->d_timeline, (size_t)n * 8));
   if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
   ctx->h_hist = nullptr;
   CK(cudaMallocHost(&ctx->h_hist, sizeof(double) * (size_t)n));
@@ -242,11 +253,22 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P) {
   return CQB_OK;
 }
 
+// K2b: Morton-order samples from the bin table (also zeroes it).
+int enqueue_morton(cqb_ctx* ctx) {
+  CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_BIN_TILES + 1), ctx->stream));
+  k_bins_compact<<<N_BIN_TILES, BC_THREADS, 0, ctx->stream>>>(
+      ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
+      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_BIN_TILES), ctx->d_n);
+  CKL();
+  return CQB_OK;
+}
+
 int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_first, uint64_t total, double* traj,
                 int traj_cap) {
   LoopParams L{};
-  L.keys = ctx->d_keys;
-  L.counts = ctx->d_counts;
+  L.keys = ctx->d_mkeys;
+  L.counts = ctx->d_mcounts;
+  L.rank = ctx->d_mrank;
   L.labels = ctx->d_labels;
   L.n_ptr = ctx->d_n;
   L.shard_lo = 0;
@@ -264,6 +286,10 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.traj = traj;
   L.traj_cap = traj_cap;
   L.timeline = ctx->profiling ? ctx->d_timeline : nullptr;
+  L.block_times = ctx->profiling ? ctx->d_block_times : nullptr;
+  L.stamp_iter = ctx->stamp_iter;
+  if (ctx->profiling)
+    CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
   void* args[] = {&L};
   CK(cudaLaunchCooperativeKernel((const void*)k_wsm_loop, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, 0,
                                  ctx->stream));
@@ -344,6 +370,7 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
         d_img, P, ctx->bins, ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->tile_state,
         reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles), ctx->d_n, ntiles);
     CKL();
+    TRY(enqueue_morton(ctx));
   }
   PROF(3);
   k_init_centers<<<1, KMAX, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
@@ -355,8 +382,8 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->st->final_C, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
   CKL();
   const int gu = ctx->num_sms * 4;
-  k_map_unique<<<gu, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_counts, ctx->d_labels, ctx->d_n, k, ctx->d_sortedDr,
-                                            ctx->d_orderR, ctx->d_palkey, ctx->lut, ctx->bins, &ctx->st->mse_err, 1);
+  k_map_unique<<<gu, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, ctx->d_labels, ctx->d_n, k,
+                                            ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey, ctx->lut, &ctx->st->mse_err);
   CKL();
   PROF(6);
   if (d_index || d_rgb_out) {
@@ -399,16 +426,18 @@ int cqb_create(int device, cqb_ctx** out) {
     int nb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop, LOOP_THREADS, 0));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
-    ctx->loop_blocks_max = std::min(nb, 2) * ctx->num_sms;
+    ctx->loop_blocks_max = std::min(nb, 1) * ctx->num_sms;
     CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     CK(cudaMalloc(&ctx->bins, sizeof(uint2) << 24));
     CK(cudaMemset(ctx->bins, 0, sizeof(uint2) << 24));
     CK(cudaMalloc(&ctx->lut, (size_t)1 << 24));
+    CK(cudaMalloc(&ctx->bin_tile_state, sizeof(unsigned long long) * (N_BIN_TILES + 1)));
     CK(cudaMalloc(&ctx->st, sizeof(WsmState)));
     CK(cudaMemset(ctx->st, 0, sizeof(WsmState)));
     CK(cudaMalloc(&ctx->d_n, sizeof(unsigned long long)));
     CK(cudaMalloc(&ctx->d_centers_in, sizeof(double) * 3 * KMAX));
+    CK(cudaMalloc(&ctx->d_block_times, sizeof(unsigned long long) * 8 * MAXBLK));
     CK(cudaMalloc(&ctx->d_sortedDr, sizeof(int) * KMAX * KMAX));
     CK(cudaMalloc(&ctx->d_orderR, KMAX * KMAX));
     CK(cudaMalloc(&ctx->d_palkey, sizeof(uint32_t) * KMAX));
@@ -436,8 +465,9 @@ int cqb_destroy(cqb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
-                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_labels, ctx->d_weights, ctx->d_n, ctx->st,
-                 ctx->d_hist, ctx->d_timeline, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
+                 ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
+                 ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
                  ctx->d_draws};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -474,6 +504,7 @@ int cqb_set_grid_limit(cqb_ctx* ctx, int max_blocks) {
 int cqb_set_profiling(cqb_ctx* ctx, int on) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
   ctx->profiling = on != 0;
+  if (on > 1) ctx->stamp_iter = on;  // on > 1: also selects the iteration for per-block stamps
   return CQB_OK;
 }
 
@@ -490,7 +521,15 @@ int cqb_loop_timeline(cqb_ctx* ctx, unsigned long long* stamps, int n_iters) {
   if (!ctx->profiling) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "profiling is off");
   CK(cudaStreamSynchronize(ctx->stream));
   const int n = std::min(n_iters, ctx->cap_hist);
-  CK(cudaMemcpy(stamps, ctx->d_timeline, sizeof(unsigned long long) * 5 * (size_t)n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(stamps, ctx->d_timeline, sizeof(unsigned long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  return CQB_OK;
+}
+
+int cqb_block_times(cqb_ctx* ctx, unsigned long long* out, int n) {
+  if (!ctx || !out) return CQB_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(out, ctx->d_block_times, sizeof(unsigned long long) * (size_t)std::min(n, 8 * MAXBLK),
+                cudaMemcpyDeviceToHost));
   return CQB_OK;
 }
 
@@ -555,8 +594,16 @@ static int run_loop_common(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* c
   CK(cudaMemcpyAsync(ctx->d_counts, counts, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
   ctx->h_scalar[1] = n;
   CK(cudaMemcpyAsync(ctx->d_n, &ctx->h_scalar[1], sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->stream));
-  if (labels_in) CK(cudaMemcpyAsync(ctx->d_labels, labels_in, n, cudaMemcpyHostToDevice, ctx->stream));
-  else CK(cudaMemsetAsync(ctx->d_labels, 0, n, ctx->stream));
+  k_bins_scatter<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_counts, ctx->d_n, ctx->bins);
+  CKL();
+  TRY(enqueue_morton(ctx));
+  if (labels_in) {
+    CK(cudaMemcpyAsync(ctx->d_lab_rank, labels_in, n, cudaMemcpyHostToDevice, ctx->stream));
+    k_labels_gather<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_mrank, ctx->d_lab_rank, ctx->d_labels, ctx->d_n);
+    CKL();
+  } else {
+    CK(cudaMemsetAsync(ctx->d_labels, 0, n, ctx->stream));
+  }
   TRY(reset_state(ctx));
   const int ndraws = k + 64;
   if (centers_in) {
@@ -575,11 +622,19 @@ static int run_loop_common(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* c
   TRY(stage_results(ctx, k, term_iters(term)));
   CK(cudaStreamSynchronize(ctx->stream));
   TRY(check_status(ctx));
+  if (ctx->h_stage->n_unique != n)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "histogram keys must be distinct (%llu distinct of %llu)",
+                (unsigned long long)ctx->h_stage->n_unique, (unsigned long long)n);
   const int iters = ctx->h_stage->iterations;
   if (tcap > 0)
     CK(cudaMemcpy(trajectory, ctx->d_traj, sizeof(double) * 3 * (size_t)k * (size_t)std::min(tcap, iters),
                   cudaMemcpyDeviceToHost));
-  if (labels_out) CK(cudaMemcpy(labels_out, ctx->d_labels, n, cudaMemcpyDeviceToHost));
+  if (labels_out) {
+    k_labels_scatter<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_mrank, ctx->d_labels, ctx->d_lab_rank, ctx->d_n);
+    CKL();
+    CK(cudaMemcpyAsync(labels_out, ctx->d_lab_rank, n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   fill_report(ctx, k, seed, 0, centers_out, sse_history, hist_cap, report);
   return CQB_OK;
 }
@@ -680,11 +735,12 @@ int cqb_map_pixels(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, const do
   CK(cudaMemcpyAsync(ctx->d_centers_in, centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(&ctx->st->mse_err, 0, sizeof(unsigned long long), ctx->stream));
   TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
+  TRY(enqueue_morton(ctx));
   k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->d_centers_in, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
   CKL();
-  k_map_unique<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_counts, nullptr, ctx->d_n, k,
+  k_map_unique<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, nullptr, ctx->d_n, k,
                                                           ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey, ctx->lut,
-                                                          ctx->bins, &ctx->st->mse_err, 1);
+                                                          &ctx->st->mse_err);
   CKL();
   const uint64_t nchunk = (n_pixels + PX_PER_THREAD - 1) / PX_PER_THREAD;
   const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);

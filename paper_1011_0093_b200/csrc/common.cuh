@@ -6,7 +6,7 @@
 namespace cqb {
 
 constexpr int KMAX = 256;            // palette sizes handled on device (u8 labels)
-constexpr int LOOP_THREADS = 512;    // persistent WSM loop block size
+constexpr int LOOP_THREADS = 1024;   // persistent WSM loop block size (one block per SM)
 constexpr int MAXBLK = 1024;         // max persistent blocks (reseed candidate slots)
 constexpr int HIST_THREADS = 256;    // histogram / compaction block size
 constexpr int PX_PER_THREAD = 16;    // 16 pixels = 48 B = 3 x 16-B vector loads
@@ -97,6 +97,31 @@ __device__ __forceinline__ int load_chunk_keys(const uint8_t* __restrict__ img, 
     }
   }
   return n;
+}
+
+// Morton (Z-order) code of a color: bits of r, g, b interleaved (r highest).
+// The 2^24-bin histogram is indexed by this code, so a bin-order scan yields
+// the unique colors in a space-filling-curve order: consecutive samples are
+// spatial neighbours in RGB, which makes the WSM warps coherent.
+__host__ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 8 bits -> every 3rd bit
+  v &= 0xFFu;
+  v = (v | (v << 8)) & 0x0000F00Fu;
+  v = (v | (v << 4)) & 0x000C30C3u;
+  v = (v | (v << 2)) & 0x00249249u;
+  return v;
+}
+__host__ __device__ __forceinline__ uint32_t compact3(uint32_t v) {
+  v &= 0x00249249u;
+  v = (v | (v >> 2)) & 0x000C30C3u;
+  v = (v | (v >> 4)) & 0x0000F00Fu;
+  v = (v | (v >> 8)) & 0x000000FFu;
+  return v;
+}
+__host__ __device__ __forceinline__ uint32_t morton_of_key(uint32_t key) {
+  return (spread3(key >> 16) << 2) | (spread3(key >> 8) << 1) | spread3(key);
+}
+__host__ __device__ __forceinline__ uint32_t key_of_morton(uint32_t m) {
+  return (compact3(m >> 2) << 16) | (compact3(m >> 1) << 8) | compact3(m);
 }
 
 template <typename T>

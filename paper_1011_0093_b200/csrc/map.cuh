@@ -9,8 +9,8 @@
 //                  final WSM label with the STRICT break d(R_p,R_t) > 4*prev
 //                  (exact for lowest-index ties: a pruned t has d(x,R_t) >
 //                  prev >= min). Writes the 16 MiB key->index LUT, the exact
-//                  u64 Σ count*err (so MSE needs no per-pixel pass), and
-//                  returns the touched histogram bins to zero.
+//                  u64 Σ count*err (so MSE needs no per-pixel pass). It
+//                  walks the samples in Morton order (coherent rows).
 //   k_map_pixels : per pixel: LUT gather (L2-resident), emits the u8 index map
 //                  and the mapped RGB raster with 16-B vector stores.
 //   k_mse        : standalone mse(a, b) with __vabsdiffu4 + dp4a.
@@ -63,8 +63,7 @@ __global__ void __launch_bounds__(256) k_map_unique(const uint32_t* __restrict__
                                                     const unsigned long long* __restrict__ n_ptr, int k,
                                                     const int* __restrict__ sortedDr, const uint8_t* __restrict__ orderR,
                                                     const uint32_t* __restrict__ pal_key, uint8_t* __restrict__ lut,
-                                                    uint2* __restrict__ bins, unsigned long long* __restrict__ err_sum,
-                                                    int do_map) {
+                                                    unsigned long long* __restrict__ err_sum) {
   __shared__ uint32_t s_key[KMAX];
   __shared__ int s_cc[KMAX];
   __shared__ unsigned long long s_red[8];
@@ -79,7 +78,7 @@ __global__ void __launch_bounds__(256) k_map_unique(const uint32_t* __restrict__
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t x = keys[i];
-    if (do_map) {
+    {
       const int xx = key_dot(x, x);
       const int p = start_labels ? start_labels[i] : 0;
       const int prev = xx + s_cc[p] - 2 * key_dot(x, s_key[p]);
@@ -99,9 +98,8 @@ __global__ void __launch_bounds__(256) k_map_unique(const uint32_t* __restrict__
       lut[x] = (uint8_t)best;
       err += (unsigned long long)counts[i] * (unsigned long long)mind;
     }
-    bins[x] = make_uint2(0u, 0u);
   }
-  if (do_map) {
+  {
     err = warp_sum(err);
     if ((tid & 31) == 0) s_red[tid >> 5] = err;
     __syncthreads();
@@ -172,6 +170,21 @@ __global__ void __launch_bounds__(HIST_THREADS) k_map_pixels(const uint8_t* __re
       }
     }
   }
+}
+
+// Label layout helpers: Morton-ordered samples <-> first-occurrence order.
+// lab_m[j] = lab_rank[rank[j]]  /  lab_rank[rank[j]] = lab_m[j]
+__global__ void k_labels_gather(const uint32_t* __restrict__ rank, const uint8_t* __restrict__ lab_rank,
+                                uint8_t* __restrict__ lab_m, const unsigned long long* __restrict__ n_ptr) {
+  const uint64_t n = *n_ptr;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    lab_m[i] = lab_rank[rank[i]];
+}
+__global__ void k_labels_scatter(const uint32_t* __restrict__ rank, const uint8_t* __restrict__ lab_m,
+                                 uint8_t* __restrict__ lab_rank, const unsigned long long* __restrict__ n_ptr) {
+  const uint64_t n = *n_ptr;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    lab_rank[rank[i]] = lab_m[i];
 }
 
 // mse(a, b) numerator: exact u64 Σ squared channel differences (metrics.hpp:21-27).

@@ -41,19 +41,25 @@ struct WsmState {
   uint8_t order[KMAX * KMAX];             // row p: [p, others by (d, index)]
   double final_C[3 * KMAX];
   uint32_t chosen[KMAX];                  // init: chosen sample indices
-  unsigned long long cand_d[2][MAXBLK];   // reseed candidates (d bits, index)
+  unsigned long long cand_d[2][MAXBLK];   // reseed candidates (d bits, rank, key)
   unsigned int cand_i[2][MAXBLK];
+  unsigned int cand_k[2][MAXBLK];
   unsigned long long evals;               // point + pair distance evaluations
   unsigned long long mse_err;             // Σ count * int distance (map pass)
   double sse;
   int iterations;
   int status;
   int n_empty_events;
+  int stop_it;                            // iteration at which block 0 decided to stop
 };
 
+// Sample arrays are in MORTON order (k_bins_compact); rank[i] is sample i's
+// first-occurrence rank, used wherever the reference breaks ties by sample
+// index (empty-cluster reseed, kmeans.hpp:277-289).
 struct LoopParams {
   const uint32_t* keys;
   const uint32_t* counts;
+  const uint32_t* rank;
   uint8_t* labels;
   const unsigned long long* n_ptr;  // N' on device
   unsigned long long shard_lo;      // this rank's sample range (single GPU: 0..N')
@@ -70,7 +76,9 @@ struct LoopParams {
   int hist_cap;
   double* traj;
   int traj_cap;
-  unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (5 per iteration)
+  unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (8 per iteration)
+  unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
+  int stamp_iter;
 };
 
 // ---------------------------------------------------------------------------
@@ -174,14 +182,24 @@ struct LoopSmem {
   uint2 accm[5 * KMAX];                  // block-local moment deltas (-)
   int2 cb[KMAX];                         // dense path: {packed center, cc*256 + k}
   uint32_t row0[KMAX];                   // dense path: sorted d(c_0, .) as integers
-  double rowd[KMAX];                     // tables scratch
+  double rowd[2][KMAX];                  // tables scratch (two rows per pass)
+  int rank_part[2][2][KMAX];             // tables: [row][half of u-range][t]
+  int row_sorted[2];                     // tables: previous permutation still sorted
+  unsigned long long red_u64[LOOP_THREADS / 32];
   double red_hi[LOOP_THREADS / 32], red_lo[LOOP_THREADS / 32];
   int red_i[LOOP_THREADS / 32];
+  int red_j[LOOP_THREADS / 32];
   int empty_list[KMAX];
   unsigned int taken[KMAX];
   int n_empty;
-  double sse;
 };
+
+// Per-block phase stamps for one iteration (profiling): bt[phase * G + block].
+#define BLOCK_STAMP(phase)                                                                   \
+  do {                                                                                       \
+    if (L.block_times && it == L.stamp_iter && threadIdx.x == 0)                                        \
+      L.block_times[(phase) * gridDim.x + blockIdx.x] = globaltimer();                     \
+  } while (0)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -189,26 +207,81 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Row p of the center tables (kmeans.hpp:147-168): d[p][t] = dist2(c_p, c_t)
-// and the order row [p, others sorted by (d, index)] by rank counting.
-__device__ void tables_row(LoopSmem& S, WsmState* st, int p, int k) {
+// Sorted center rows staged in shared memory, truncated at R entries
+// (R = K for K <= 64); deeper scans continue in the global rows (L2).
+struct RowStage {
+  const double* d;   // row p starts at d + p * stride
+  const uint8_t* o;
+  int R;             // entries available per row (R == k: full rows)
+  int stride;
+};
+
+// Rows pa (and pb, or -1) of the center tables (kmeans.hpp:147-168):
+// d[p][t] = dist2(c_p, c_t) and the order row [p, others sorted by
+// (d, index)]. The block's 1024 threads take two rows per pass.
+//
+// Incremental path (like the reference's insertion repair, :169-180): the
+// previous permutation is re-checked under the new distances; if it is
+// still strictly increasing in (d, index) it IS the unique sorted order and
+// only the distances are rewritten. Otherwise (early iterations) the row is
+// re-sorted by rank counting, half of the block per row, u-range split in 2.
+__device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental) {
+  static_assert(LOOP_THREADS == 4 * KMAX, "tables layout assumes 1024 threads");
   const int tid = threadIdx.x;
-  if (tid < k) S.rowd[tid] = tid == p ? 0.0 : dist2_rn(S.cx[p], S.cy[p], S.cz[p], S.cx[tid], S.cy[tid], S.cz[tid]);
+  const int r = tid >> 9;                     // which row of the pair
+  const int t = tid & (KMAX - 1);             // element / position
+  const int h = (tid >> 8) & 1;               // half of the u-range
+  const int p = r ? pb : pa;
+  if (tid < 2) S.row_sorted[tid] = incremental ? 1 : 0;
+  if (p >= 0 && h == 0 && t < k)
+    S.rowd[r][t] = t == p ? 0.0 : dist2_rn(S.cx[p], S.cy[p], S.cz[p], S.cx[t], S.cy[t], S.cz[t]);
   __syncthreads();
-  if (tid < k) {
-    int rank = 0;
-    if (tid != p) {
-      const double dt = S.rowd[tid];
-      rank = 1;
-      for (int u = 0; u < k; ++u) {
-        const double du = S.rowd[u];
-        rank += (u != p) & ((du < dt) | ((du == dt) & (u < tid)));
-      }
+  uint8_t e_t = 0;
+  if (incremental && p >= 0 && h == 0 && t < k) {
+    e_t = st->order[p * KMAX + t];
+    if (t >= 1 && t + 1 < k) {
+      const int e_n = st->order[p * KMAX + t + 1];
+      const double da = S.rowd[r][e_t], db = S.rowd[r][e_n];
+      const bool ok = (da < db) || (da == db && (int)e_t < e_n);
+      if (!ok) S.row_sorted[r] = 0;
     }
-    st->sortedD[p * KMAX + rank] = S.rowd[tid];
-    st->order[p * KMAX + rank] = (uint8_t)tid;
   }
   __syncthreads();
+  const bool sorted_r = S.row_sorted[r] != 0;
+  if (sorted_r) {
+    if (p >= 0 && h == 0 && t < k) st->sortedD[p * KMAX + t] = S.rowd[r][e_t];
+  } else if (p >= 0 && t < k) {
+    int cnt = 0;
+    if (t != p) {
+      const double dt = S.rowd[r][t];
+      const int u0 = h * (KMAX / 2), u1 = min(k, u0 + KMAX / 2);
+      for (int u = u0; u < u1; ++u) {
+        const double du = S.rowd[r][u];
+        cnt += (u != p) & ((du < dt) | ((du == dt) & (u < t)));
+      }
+    }
+    S.rank_part[r][h][t] = cnt;
+  }
+  __syncthreads();
+  if (!sorted_r && p >= 0 && h == 0 && t < k) {
+    const int rank = t == p ? 0 : 1 + S.rank_part[r][0][t] + S.rank_part[r][1][t];
+    st->sortedD[p * KMAX + rank] = S.rowd[r][t];
+    st->order[p * KMAX + rank] = (uint8_t)t;
+  }
+  __syncthreads();
+}
+
+// Rows are owned by blocks 1..G-1 (block 0 runs the SSE / termination
+// finalize meanwhile); a single-block grid does everything itself.
+__device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, bool incremental) {
+  const int G = (int)gridDim.x;
+  const int first = G == 1 ? 0 : (int)blockIdx.x - 1;
+  const int stride = G == 1 ? 1 : G - 1;
+  if (first < 0) return;
+  for (int p = first; p < k; p += 2 * stride) {
+    const int q = p + stride;
+    tables_rows2(S, st, p, q < k ? q : -1, k, incremental);
+  }
 }
 
 // u64 += v on a (lo, hi) pair of shared u32 words, native 32-bit atomics only.
@@ -230,22 +303,63 @@ __device__ __forceinline__ void acc_point(uint2* acc, int k, uint32_t key, uint3
   sadd64(&acc[4 * KMAX + k], c * (unsigned long long)(r * r + g * g + b * b));
 }
 
+// Work distribution: the Morton-ordered samples are dealt out in 32-sample
+// warp segments round-robin over all warps of the grid (grid-stride at warp
+// granularity). A segment is a compact patch of color space, so the warp's
+// lanes share their previous center, row and most candidates (broadcast
+// shared-memory reads, little divergence), while the round-robin spreads the
+// expensive regions (Voronoi boundaries) evenly over the blocks.
+__device__ __forceinline__ unsigned long long grid_threads() { return (unsigned long long)gridDim.x * blockDim.x; }
+
+// Full accumulation of one point per lane; when every valid lane of the warp
+// carries the same label (the common case in Morton order) the five moments
+// are warp-reduced and one lane does the five atomics.
+__device__ __forceinline__ void acc_point_warp(uint2* acc, bool valid, int lab, uint32_t key, uint32_t cnt) {
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!act) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(act) - 1;
+  const int l0 = __shfl_sync(0xffffffffu, lab, leader);
+  if (__all_sync(0xffffffffu, !valid || lab == l0)) {
+    const unsigned long long c = valid ? cnt : 0u;
+    const uint32_t r = key_r(key), g = key_g(key), b = key_b(key);
+    unsigned long long f0 = c * r, f1 = c * g, f2 = c * b, f3 = c,
+                       f4 = c * (unsigned long long)(r * r + g * g + b * b);
+    f0 = warp_sum(f0);
+    f1 = warp_sum(f1);
+    f2 = warp_sum(f2);
+    f3 = warp_sum(f3);
+    f4 = warp_sum(f4);
+    if (lane == leader) {
+      sadd64(&acc[0 * KMAX + l0], f0);
+      sadd64(&acc[1 * KMAX + l0], f1);
+      sadd64(&acc[2 * KMAX + l0], f2);
+      sadd64(&acc[3 * KMAX + l0], f3);
+      sadd64(&acc[4 * KMAX + l0], f4);
+    }
+  } else if (valid) {
+    acc_point(acc, lab, key, cnt);
+  }
+}
+
 // Iteration 1, dense + integer-exact (see header). Full accumulation.
 __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned long long lo, unsigned long long hi,
                                    unsigned long long& evals) {
   const int k = L.k;
-  const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
-  const unsigned long long g0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long bhi = hi;
+  const unsigned long long T = grid_threads();
+  const int lane = threadIdx.x & 31;
   const int cc0 = S.cb[0].y >> 8;  // |c_0|^2
   const uint32_t c0 = (uint32_t)S.cb[0].x;
   constexpr int PPT = 4;
-  for (unsigned long long base = lo + g0; base < hi; base += PPT * T) {
+  for (unsigned long long base = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; base - lane < bhi;
+       base += PPT * T) {
     uint32_t x[PPT];
     int best[PPT];
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       const unsigned long long i = base + q * T;
-      x[q] = i < hi ? L.keys[i] : 0u;
+      x[q] = i < bhi ? L.keys[i] : 0u;
       best[q] = 0x7fffffff;
     }
     for (int t = 0; t < k; ++t) {
@@ -256,8 +370,10 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       const unsigned long long i = base + q * T;
-      if (i < hi) {
-        const int lab = best[q] & 255;
+      const bool valid = i < bhi;
+      const int lab = best[q] & 255;
+      uint32_t cnt = 0;
+      if (valid) {
         const int xx = key_dot(x[q], x[q]);
         const uint32_t prev0 = (uint32_t)(xx + cc0 - 2 * key_dot(x[q], c0));
         const uint32_t bound = 4u * prev0;
@@ -270,52 +386,158 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
         }
         evals += (unsigned long long)lo_j;  // 1 (prev) + (lo_j - 1) candidates
         L.labels[i] = (uint8_t)lab;
-        acc_point(S.accp, lab, x[q], L.counts[i]);
+        cnt = L.counts[i];
       }
+      acc_point_warp(S.accp, valid, lab, x[q], cnt);
     }
   }
 }
 
 // Iterations >= 2 (or the first of a teacher-forced launch, full = true):
-// FP64 sort-means scan from the previous label (kmeans.hpp:211-236); tables
-// in L2 (written by this kernel, read after the grid barrier).
-__device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned long long lo, unsigned long long hi,
-                                  bool full, unsigned long long& evals) {
-  const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
-  const double* __restrict__ sd = L.st->sortedD;
-  const uint8_t* __restrict__ od = L.st->order;
-  const int k = L.k;
-  for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += T) {
-    const uint32_t key = L.keys[i];
-    const int p = L.labels[i];
-    const double x0 = (double)key_r(key), x1 = (double)key_g(key), x2 = (double)key_b(key);
-    const double prev = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);
-    const double bound = 4.0 * prev;
-    double mind = prev;
-    int best = p;
-    unsigned long long ev = 1;
-    const double* rowd = sd + p * KMAX;
-    const uint8_t* rowo = od + p * KMAX;
-    for (int j = 1; j < k; ++j) {
-      const double dj = rowd[j];
-      if (dj >= bound) break;
-      const int t = rowo[j];
-      const double d = dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]);
-      ++ev;
-      if (d < mind || (d == mind && t < best)) {
-        mind = d;
-        best = t;
-      }
+// FP64 sort-means scan from the previous label (kmeans.hpp:211-236).
+//
+// The reference scan evaluates exactly the row entries before the first j
+// with d[p][t_j] >= 4*prev (:220-226); rows are sorted, so the break index J
+// is found by binary search over the staged prefix and the J-1 candidates are
+// evaluated independently (the lexicographic (dist, index) minimum does not
+// depend on evaluation order). A scan that runs past the staged prefix
+// ("deep" point, < 1% of points) is finished by the whole warp: 32 row
+// entries per coalesced L2 read, break located by ballot, candidates
+// evaluated one per lane, lexicographic minimum by shuffle reduction.
+__device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
+  if (d < md || (d == md && t < mb)) {
+    md = d;
+    mb = t;
+  }
+}
+
+__device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo,
+                                  unsigned long long hi, bool full, unsigned long long& evals,
+                                  unsigned int& n_changed, unsigned int& n_deep) {
+  constexpr int PPT = 2;
+  const unsigned long long T = grid_threads();
+  const int lane = threadIdx.x & 31;
+  const double* __restrict__ gd = L.st->sortedD;
+  const uint8_t* __restrict__ go = L.st->order;
+  const int k = L.k, R = RS.R;
+  // warp-uniform trip count (every lane of a warp runs the same batches)
+  for (unsigned long long base = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; base - lane < hi;
+       base += PPT * T) {
+    uint32_t key[PPT];
+    int lab[PPT], nlab[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const unsigned long long i = base + q * T;
+      key[q] = i < hi ? L.keys[i] : 0u;
+      lab[q] = i < hi ? (int)L.labels[i] : 0;
     }
-    evals += ev;
-    if (full) {
-      if (best != p) L.labels[i] = (uint8_t)best;
-      acc_point(S.accp, best, key, L.counts[i]);
-    } else if (best != p) {
-      L.labels[i] = (uint8_t)best;
-      const uint32_t cnt = L.counts[i];
-      acc_point(S.accm, p, key, cnt);
-      acc_point(S.accp, best, key, cnt);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const bool valid = base + q * T < hi;
+      const int p = lab[q];
+      const double x0 = (double)key_r(key[q]), x1 = (double)key_g(key[q]), x2 = (double)key_b(key[q]);
+      double mind = 0.0, bound = 0.0;
+      int best = p;
+      bool deep = false;
+      if (valid) {
+        const double prev = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);
+        bound = 4.0 * prev;
+        mind = prev;
+        const double* rd = RS.d + p * RS.stride;
+        const uint8_t* ro = RS.o + p * RS.stride;
+        // exponential then binary search: most points stop at J = 1
+        int J = 1;
+        if (R > 1 && rd[1] < bound) {
+          int lo_j = 1, hi_j = R;
+          for (int st2 = 2; st2 < R; st2 <<= 1) {
+            if (rd[st2] >= bound) {
+              hi_j = st2;
+              break;
+            }
+            lo_j = st2;
+          }
+          int a = lo_j + 1, b = hi_j;
+          while (a < b) {
+            const int m = (a + b) >> 1;
+            if (rd[m] >= bound) b = m;
+            else a = m + 1;
+          }
+          J = a;
+        }
+        evals += (unsigned long long)J;  // prev + (J - 1) candidates
+        int j = 1;
+        for (; j + 1 < J; j += 2) {
+          const int t0 = ro[j], t1 = ro[j + 1];
+          const double d0 = dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]);
+          const double d1 = dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]);
+          lex_min(mind, best, d0, t0);
+          lex_min(mind, best, d1, t1);
+        }
+        if (j < J) {
+          const int t0 = ro[j];
+          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]), t0);
+        }
+        deep = (J == R) && (R < k);
+      }
+      unsigned dm = __ballot_sync(0xffffffffu, deep);
+      n_deep += deep;
+      while (dm) {  // warp-cooperative continuation of each deep lane's scan
+        const int src = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const int pp = __shfl_sync(0xffffffffu, p, src);
+        const double bb = __shfl_sync(0xffffffffu, bound, src);
+        const double y0 = __shfl_sync(0xffffffffu, x0, src), y1 = __shfl_sync(0xffffffffu, x1, src);
+        const double y2 = __shfl_sync(0xffffffffu, x2, src);
+        double wm = __shfl_sync(0xffffffffu, mind, src);
+        int wb = __shfl_sync(0xffffffffu, best, src);
+        for (int j0 = R; j0 < k; j0 += 32) {
+          const int j = j0 + lane;
+          const bool in = j < k && gd[pp * KMAX + (j < k ? j : 0)] < bb;
+          const unsigned okm = __ballot_sync(0xffffffffu, in);
+          const int nev = __ffs(~okm) ? __ffs(~okm) - 1 : 32;  // leading lanes before the break
+          double d = __longlong_as_double(0x7ff0000000000000LL);
+          int t = 0x7fffffff;
+          if (lane < nev) {
+            t = go[pp * KMAX + j];
+            d = dist2_rn(y0, y1, y2, S.cx[t], S.cy[t], S.cz[t]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, d, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, t, o);
+            lex_min(d, t, od, ot);
+          }
+          lex_min(wm, wb, d, t);
+          if (lane == 0) evals += (unsigned long long)nev;
+          if (nev < 32) break;
+        }
+        if (lane == src) {
+          mind = wm;
+          best = wb;
+        }
+      }
+      nlab[q] = valid ? best : lab[q];
+    }
+    uint32_t cnt[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const unsigned long long i = base + q * T;
+      cnt[q] = (i < hi && (full || nlab[q] != lab[q])) ? L.counts[i] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const unsigned long long i = base + q * T;
+      const bool valid = i < hi;
+      if (valid && nlab[q] != lab[q]) {
+        L.labels[i] = (uint8_t)nlab[q];
+        ++n_changed;
+      }
+      if (full) {
+        acc_point_warp(S.accp, valid, nlab[q], key[q], cnt[q]);
+      } else if (valid && nlab[q] != lab[q]) {
+        acc_point(S.accm, lab[q], key[q], cnt[q]);
+        acc_point(S.accp, nlab[q], key[q], cnt[q]);
+      }
     }
   }
 }
@@ -339,6 +561,48 @@ __device__ dd block_sum_dd(LoopSmem& S, dd v) {
   return tot;
 }
 
+// One fixed-tree block reduction of (double-double, int, int).
+__device__ void block_sum3(LoopSmem& S, dd& v, int& a, int& b) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd w{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+    v = dd_add(v, w);
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    S.red_hi[wid] = v.hi;
+    S.red_lo[wid] = v.lo;
+    S.red_i[wid] = a;
+    S.red_j[wid] = b;
+  }
+  __syncthreads();
+  if (wid == 0) {  // fixed shuffle tree over the (<= 32) warp partials
+    const int nw = (int)(blockDim.x >> 5);
+    dd x = lane < nw ? dd{S.red_hi[lane], S.red_lo[lane]} : dd{0.0, 0.0};
+    int xa = lane < nw ? S.red_i[lane] : 0, xb = lane < nw ? S.red_j[lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dd w{__shfl_xor_sync(0xffffffffu, x.hi, o), __shfl_xor_sync(0xffffffffu, x.lo, o)};
+      x = dd_add(x, w);
+      xa += __shfl_xor_sync(0xffffffffu, xa, o);
+      xb += __shfl_xor_sync(0xffffffffu, xb, o);
+    }
+    if (lane == 0) {
+      S.red_hi[0] = x.hi;
+      S.red_lo[0] = x.lo;
+      S.red_i[0] = xa;
+      S.red_j[0] = xb;
+    }
+  }
+  __syncthreads();
+  v = dd{S.red_hi[0], S.red_lo[0]};
+  a = S.red_i[0];
+  b = S.red_j[0];
+}
+
 __device__ int block_sum_int(LoopSmem& S, int v) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_sum(v);
@@ -357,6 +621,9 @@ __device__ __forceinline__ bool cand_better(double d, unsigned int i, double bd,
 }
 
 // Empty-cluster reseed (kmeans.hpp:268-290), grid-wide, all blocks agree.
+// Candidates are ordered by (distance desc, first-occurrence rank asc): the
+// reference's strict '>' scan in sample order. Unique colors are distinct, so
+// "color already taken" is "rank already taken".
 __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long lo,
                              unsigned long long hi) {
   WsmState* st = L.st;
@@ -364,63 +631,70 @@ __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& g
   const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
   for (int e = 0; e < S.n_empty; ++e) {
     double bd = -1.0;
-    unsigned int bi = 0xffffffffu;
+    unsigned int bi = 0xffffffffu, bk = 0u;
     for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += T) {
+      const unsigned int rk = L.rank[i];
       bool used = false;
-      for (int t = 0; t < e; ++t) used |= (S.taken[t] == (unsigned int)i);
+      for (int t = 0; t < e; ++t) used |= (S.taken[t] == rk);
       if (used) continue;
       const uint32_t key = L.keys[i];
       const int m = L.labels[i];
       const double d = dist2_rn((double)key_r(key), (double)key_g(key), (double)key_b(key), S.cx[m], S.cy[m], S.cz[m]);
-      if (cand_better(d, (unsigned int)i, bd, bi)) {
+      if (cand_better(d, rk, bd, bi)) {
         bd = d;
-        bi = (unsigned int)i;
+        bi = rk;
+        bk = key;
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double od = __shfl_xor_sync(0xffffffffu, bd, o);
       const unsigned int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const unsigned int ok = __shfl_xor_sync(0xffffffffu, bk, o);
       if (cand_better(od, oi, bd, bi)) {
         bd = od;
         bi = oi;
+        bk = ok;
       }
     }
     __syncthreads();
     if (lane == 0) {
       S.red_hi[wid] = bd;
       S.red_i[wid] = (int)bi;
+      S.red_j[wid] = (int)bk;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       double xd = -1.0;
-      unsigned int xi = 0xffffffffu;
+      unsigned int xi = 0xffffffffu, xk = 0u;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
         if (cand_better(S.red_hi[w], (unsigned int)S.red_i[w], xd, xi)) {
           xd = S.red_hi[w];
           xi = (unsigned int)S.red_i[w];
+          xk = (unsigned int)S.red_j[w];
         }
       st->cand_d[e & 1][blockIdx.x] = __double_as_longlong(xd);
       st->cand_i[e & 1][blockIdx.x] = xi;
+      st->cand_k[e & 1][blockIdx.x] = xk;
     }
     grid.sync();
     if (threadIdx.x == 0) {
       double xd = -1.0;
-      unsigned int xi = 0xffffffffu;
+      unsigned int xi = 0xffffffffu, xk = 0u;
       for (unsigned int b = 0; b < gridDim.x; ++b) {
         const double d = __longlong_as_double((long long)st->cand_d[e & 1][b]);
         const unsigned int i = st->cand_i[e & 1][b];
         if (cand_better(d, i, xd, xi)) {
           xd = d;
           xi = i;
+          xk = st->cand_k[e & 1][b];
         }
       }
       S.taken[e] = xi;
       const int ke = S.empty_list[e];
-      const uint32_t key = L.keys[xi];
-      S.nx[ke] = (double)key_r(key);
-      S.ny[ke] = (double)key_g(key);
-      S.nz[ke] = (double)key_b(key);
+      S.nx[ke] = (double)key_r(xk);
+      S.ny[ke] = (double)key_g(xk);
+      S.nz[ke] = (double)key_b(xk);
     }
     __syncthreads();
   }
@@ -439,8 +713,9 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 }
 
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
-__global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
+__global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   __shared__ LoopSmem S;
+  extern __shared__ __align__(16) unsigned char dyn[];
   cg::grid_group grid = cg::this_grid();
   WsmState* st = L.st;
   const int tid = threadIdx.x;
@@ -453,6 +728,15 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
   unsigned long long* gacc = st->acc;  // exact running sums (zeroed by the host per launch)
   unsigned long long* tl = L.timeline;
   const bool rec = tl && blockIdx.x == 0 && tid == 0;
+  // Sorted rows are read straight from the global tables: the warps are
+  // Morton-coherent, so a row access is one L1 transaction shared by the warp
+  // (the grid barrier's gpu-scope fence invalidates L1 between iterations).
+  RowStage RS;
+  RS.R = k;
+  RS.stride = KMAX;
+  RS.d = st->sortedD;
+  RS.o = st->order;
+  (void)dyn;
 
   for (int t = tid; t < k; t += blockDim.x) {
     S.cx[t] = st->C[0][3 * t];
@@ -465,16 +749,17 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
   }
   __syncthreads();
   // prologue: tables of the initial centers (all pairs evaluated: non-incremental)
-  for (int p = blockIdx.x; p < k; p += gridDim.x) tables_row(S, st, p, k);
-  if (blockIdx.x == 0 && tid == 0) st->evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+  tables_all(S, st, k, false);
+  unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
+  unsigned long long pair_evals = (unsigned long long)k * (unsigned long long)(k - 1) / 2;  // block 0 only
   grid.sync();
 
-  double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
   for (int it = 1;; ++it) {
     const bool rec_it = rec && it <= L.hist_cap;
-    if (rec_it) tl[(it - 1) * 5 + 0] = globaltimer();
+    if (rec_it) tl[(it - 1) * 8 + 0] = globaltimer();
+    BLOCK_STAMP(0);
     // ---------------- assign(it) ----------------
-    unsigned long long evals = 0;
     if (it == 1 && L.dense_first) {
       for (int t = tid; t < k; t += blockDim.x) {
         const uint32_t key = ((uint32_t)S.cx[t] << 16) | ((uint32_t)S.cy[t] << 8) | (uint32_t)S.cz[t];
@@ -482,69 +767,93 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
         S.row0[t] = (uint32_t)st->sortedD[t];  // row 0 (p = 0), integer-valued
       }
       __syncthreads();
+      if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       assign_dense_first(S, L, lo, hi, evals);
     } else {
-      assign_sort_means(S, L, lo, hi, it == 1, evals);
-    }
-    evals = warp_sum(evals);
-    if ((tid & 31) == 0 && evals) atomicAdd(&st->evals, evals);
-    __syncthreads();
-    flush_moments(S, gacc, k);
-    if (rec_it) tl[(it - 1) * 5 + 1] = globaltimer();
-    grid.sync();
-    if (rec_it) tl[(it - 1) * 5 + 2] = globaltimer();
-
-    // ---------------- finalize(it), redundantly per block ----------------
-    dd part{0.0, 0.0};
-    int empt = 0;
-    for (int t = tid; t < k; t += blockDim.x) {
-      const unsigned long long N = gacc[3 * KMAX + t];
-      const double Sr = (double)gacc[0 * KMAX + t], Sg = (double)gacc[1 * KMAX + t], Sb = (double)gacc[2 * KMAX + t];
-      if (N) {
-        const double dn = (double)N;
-        S.nx[t] = Sr / dn;
-        S.ny[t] = Sg / dn;
-        S.nz[t] = Sb / dn;
-        // Q - 2 c.S + |c|^2 N with the centers of THIS assignment
-        const double cr = S.cx[t], cgc = S.cy[t], cbc = S.cz[t];
-        dd cs = dd_add(dd_add(two_prod(cr, Sr), two_prod(cgc, Sg)), two_prod(cbc, Sb));
-        dd c2 = dd_add(dd_add(two_prod(cr, cr), two_prod(cgc, cgc)), two_prod(cbc, cbc));
-        dd term = dd_add(dd{(double)gacc[4 * KMAX + t], 0.0}, dd_scale(cs, -2.0));
-        term = dd_add(term, dd_scale(c2, dn));
-        part = dd_add(part, term);
-      } else {
-        empt = 1;
+      __syncthreads();
+      if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
+      unsigned int n_changed = 0, n_deep = 0;
+      assign_sort_means(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      if (rec_it || (tl && it <= L.hist_cap)) {  // diagnostics: label churn and deep scans
+        const unsigned long long v = ((unsigned long long)warp_sum(n_deep) << 32) | warp_sum(n_changed);
+        if ((tid & 31) == 0 && v) atomicAdd(&tl[(it - 1) * 8 + 7], v);
       }
     }
-    const dd tot = block_sum_dd(S, part);
-    const int n_empty = block_sum_int(S, empt);
-    if (tid == 0) {
-      const double sse = __dadd_rn(tot.hi, tot.lo) * inv_P;
-      S.sse = sse < 0.0 ? 0.0 : sse;
-      S.n_empty = n_empty;
-      if (n_empty) {
+    __syncthreads();
+    if (rec_it) tl[(it - 1) * 8 + 2] = globaltimer();
+    BLOCK_STAMP(1);
+    flush_moments(S, gacc, k);
+    if (rec_it) tl[(it - 1) * 8 + 3] = globaltimer();
+    BLOCK_STAMP(2);
+    grid.sync();
+    if (rec_it) tl[(it - 1) * 8 + 4] = globaltimer();
+    BLOCK_STAMP(3);
+
+    // ---------------- finalize(it) ----------------
+    // Every block: new centers S/N (FP64, exact integer inputs) + empty count.
+    int empt_local = 0;
+    for (int t = tid; t < k; t += blockDim.x) {
+      const unsigned long long N = gacc[3 * KMAX + t];
+      if (N) {
+        const double dn = (double)N;
+        S.nx[t] = (double)gacc[0 * KMAX + t] / dn;
+        S.ny[t] = (double)gacc[1 * KMAX + t] / dn;
+        S.nz[t] = (double)gacc[2 * KMAX + t] / dn;
+      } else {
+        empt_local = 1;
+      }
+    }
+    const int empt = __syncthreads_count(empt_local);  // k <= blockDim: one cluster per thread
+    if (empt) {  // rare: empty clusters (uniform across the grid)
+      if (tid == 0) {
+        S.n_empty = empt;
         int m = 0;
         for (int t = 0; t < k; ++t)
           if (gacc[3 * KMAX + t] == 0ull) S.empty_list[m++] = t;
       }
+      __syncthreads();
+      reseed_empty(S, L, grid, lo, hi);
     }
-    __syncthreads();
-    if (S.n_empty) reseed_empty(S, L, grid, lo, hi);
-    const double sse = S.sse;
-    // termination (kmeans.hpp:359-369)
-    bool stop;
-    if (L.mode == 0) {
-      stop = it >= L.max_iters;
-    } else {
-      stop = (sse == 0.0) || ((prev_sse - sse) / sse <= L.eps) || (it >= L.cap);
-    }
-    prev_sse = sse;
+    // Block 0: moment-form SSE, termination (kmeans.hpp:359-369), reporting.
     if (blockIdx.x == 0) {
+      dd part{0.0, 0.0};
+      int moved = 0, unused = 0;
+      for (int t = tid; t < k; t += blockDim.x) {
+        moved += (S.nx[t] != S.cx[t]) | (S.ny[t] != S.cy[t]) | (S.nz[t] != S.cz[t]);
+        const unsigned long long N = gacc[3 * KMAX + t];
+        if (N) {
+          const double dn = (double)N;
+          const double Sr = (double)gacc[0 * KMAX + t], Sg = (double)gacc[1 * KMAX + t];
+          const double Sb = (double)gacc[2 * KMAX + t], Q = (double)gacc[4 * KMAX + t];
+          const double cr = S.cx[t], cgc = S.cy[t], cbc = S.cz[t];
+          // Q - 2 c.S + |c|^2 N with the centers of THIS assignment
+          dd cs = dd_add(dd_add(two_prod(cr, Sr), two_prod(cgc, Sg)), two_prod(cbc, Sb));
+          dd c2 = dd_add(dd_add(two_prod(cr, cr), two_prod(cgc, cgc)), two_prod(cbc, cbc));
+          dd term = dd_add(dd{Q, 0.0}, dd_scale(cs, -2.0));
+          term = dd_add(term, dd_scale(c2, dn));
+          part = dd_add(part, term);
+        }
+      }
+      block_sum3(S, part, moved, unused);
+      const double sse = fmax(__dadd_rn(part.hi, part.lo) * inv_P, 0.0);
+      bool stop;
+      if (L.mode == 0) {
+        stop = it >= L.max_iters;
+      } else {
+        stop = (sse == 0.0) || ((prev_sse - sse) / sse <= L.eps) || (it >= L.cap);
+      }
+      prev_sse = sse;
       if (tid == 0) {
         if (it <= L.hist_cap) L.sse_hist[it - 1] = sse;
         st->iterations = it;
         st->sse = sse;
-        st->n_empty_events += S.n_empty;
+        st->n_empty_events += empt;
+        if (stop) st->stop_it = it;
+        // pair evaluations of the incremental table update (kmeans.hpp:137-155)
+        if (!stop) {
+          const unsigned long long still = (unsigned long long)(k - moved);
+          pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
+        }
       }
       if (L.traj && it <= L.traj_cap)
         for (int t = tid; t < k; t += blockDim.x) {
@@ -560,17 +869,6 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
           st->final_C[3 * t + 2] = S.nz[t];
         }
     }
-    if (stop) break;
-    // pair evaluations of the incremental table update (kmeans.hpp:137-155)
-    int moved = 0;
-    for (int t = tid; t < k; t += blockDim.x)
-      moved += (S.nx[t] != S.cx[t]) | (S.ny[t] != S.cy[t]) | (S.nz[t] != S.cz[t]);
-    const int n_moved = block_sum_int(S, moved);
-    if (blockIdx.x == 0 && tid == 0) {
-      const unsigned long long still = (unsigned long long)(k - n_moved);
-      const unsigned long long all = (unsigned long long)k * (unsigned long long)(k - 1) / 2;
-      st->evals += all - (still ? still * (still - 1) / 2 : 0ull);
-    }
     __syncthreads();
     for (int t = tid; t < k; t += blockDim.x) {
       S.cx[t] = S.nx[t];
@@ -578,10 +876,24 @@ __global__ void __launch_bounds__(LOOP_THREADS, 2) k_wsm_loop(LoopParams L) {
       S.cz[t] = S.nz[t];
     }
     __syncthreads();
-    if (rec_it) tl[(it - 1) * 5 + 3] = globaltimer();
-    for (int p = blockIdx.x; p < k; p += gridDim.x) tables_row(S, st, p, k);
-    if (rec_it) tl[(it - 1) * 5 + 4] = globaltimer();
+    if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
+    BLOCK_STAMP(4);
+    tables_all(S, st, k, true);  // wasted work on the final iteration only
+    if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
+    BLOCK_STAMP(5);
     grid.sync();
+    if (*reinterpret_cast<volatile int*>(&st->stop_it) == it) break;
+  }
+  // one evals flush per block (a per-warp atomic every iteration would
+  // serialize thousands of same-address atomics in L2)
+  evals = warp_sum(evals);
+  __syncthreads();
+  if ((tid & 31) == 0) S.red_u64[tid >> 5] = evals;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long tot = blockIdx.x == 0 ? pair_evals : 0ull;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += S.red_u64[w];
+    atomicAdd(&st->evals, tot);
   }
 }
 
