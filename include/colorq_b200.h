@@ -151,6 +151,24 @@ int cqb_map_pixels(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, const do
 /* Replaces mse(a, b) (metrics.hpp:18-29): exact u64 sum / P. */
 int cqb_mse(cqb_ctx* ctx, const uint8_t* a, const uint8_t* b, uint64_t n_pixels, double* out);
 
+/* ---- sharded WSM (multi-GPU, one process per GPU) ----------------------
+ * The unique samples (Morton order) are split into contiguous ranges, one
+ * per rank. Each WSM iteration: cqb_shard_step on the rank's range returns
+ * the EXACT integer cluster moments (K x {Σc·r, Σc·g, Σc·b, Σc, Σc·|x|²},
+ * row-major [5][k]); the host allreduces them (sum) and every rank runs
+ * cqb_finalize_moments on the identical totals, so all ranks follow the
+ * bit-identical trajectory of the single-GPU run. Driver:
+ * paper_1011_0093_b200/distributed.py. */
+int cqb_shard_prepare(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k, uint64_t seed, uint64_t* n_unique,
+                      double* init_centers);
+int cqb_shard_step(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const double* centers, int dense_first,
+                   uint64_t* moments, uint64_t* point_evals);
+int cqb_finalize_moments(cqb_ctx* ctx, const uint64_t* moments, const double* centers_used, int k, uint64_t total,
+                         double* new_centers, double* sse, int* n_empty, int* empty_list);
+int cqb_shard_reseed_candidate(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const double* centers_used,
+                               const uint32_t* taken_ranks, int n_taken, double* d_out, uint32_t* rank_out,
+                               uint32_t* key_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@
 #include <new>
 #include <random>
 #include <string>
+#include <vector>
 
 #include "../../include/colorq_b200.h"
 #include "hist.cuh"
@@ -66,6 +67,18 @@ struct cqb_ctx {
   int cap_hist = 0;
   unsigned long long* d_timeline = nullptr;  // 8 stamps per iteration (profiling)
   unsigned long long* d_block_times = nullptr;  // [8 iterations][MAXBLK] (profiling)
+  // sharded-run scratch
+  int shard_k = 0;
+  uint64_t shard_total = 0;
+  unsigned long long* d_mom = nullptr;  // 5*KMAX
+  unsigned long long* h_mom = nullptr;  // pinned 5*KMAX + 1 (evals)
+  double* d_Cnew = nullptr;
+  double* d_scal = nullptr;             // sse + reseed outputs
+  int* d_ints = nullptr;                // n_empty + empty list
+  uint32_t* d_taken = nullptr;
+  double* d_cand_d = nullptr;
+  unsigned int* d_cand_r = nullptr;
+  unsigned int* d_cand_k = nullptr;
   double* d_traj = nullptr;
   size_t cap_traj = 0;
   double* d_centers_in = nullptr;
@@ -264,15 +277,16 @@ int enqueue_morton(cqb_ctx* ctx) {
 }
 
 int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_first, uint64_t total, double* traj,
-                int traj_cap) {
+                int traj_cap, uint64_t shard_lo = 0, uint64_t shard_hi = ~0ull, int moments_only = 0) {
   LoopParams L{};
   L.keys = ctx->d_mkeys;
   L.counts = ctx->d_mcounts;
   L.rank = ctx->d_mrank;
   L.labels = ctx->d_labels;
   L.n_ptr = ctx->d_n;
-  L.shard_lo = 0;
-  L.shard_hi_or_max = ~0ull;
+  L.shard_lo = shard_lo;
+  L.shard_hi_or_max = shard_hi;
+  L.moments_only = moments_only;
   L.total = total;
   L.k = k;
   L.mode = term->mode;
@@ -438,6 +452,15 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMalloc(&ctx->d_n, sizeof(unsigned long long)));
     CK(cudaMalloc(&ctx->d_centers_in, sizeof(double) * 3 * KMAX));
     CK(cudaMalloc(&ctx->d_block_times, sizeof(unsigned long long) * 8 * MAXBLK));
+    CK(cudaMalloc(&ctx->d_mom, sizeof(unsigned long long) * 5 * KMAX));
+    CK(cudaMallocHost(&ctx->h_mom, sizeof(unsigned long long) * (5 * KMAX + 1)));
+    CK(cudaMalloc(&ctx->d_Cnew, sizeof(double) * 3 * KMAX));
+    CK(cudaMalloc(&ctx->d_scal, sizeof(double) * 8));
+    CK(cudaMalloc(&ctx->d_ints, sizeof(int) * (KMAX + 8)));
+    CK(cudaMalloc(&ctx->d_taken, sizeof(uint32_t) * KMAX));
+    CK(cudaMalloc(&ctx->d_cand_d, sizeof(double) * MAXBLK));
+    CK(cudaMalloc(&ctx->d_cand_r, sizeof(unsigned int) * MAXBLK));
+    CK(cudaMalloc(&ctx->d_cand_k, sizeof(unsigned int) * MAXBLK));
     CK(cudaMalloc(&ctx->d_sortedDr, sizeof(int) * KMAX * KMAX));
     CK(cudaMalloc(&ctx->d_orderR, KMAX * KMAX));
     CK(cudaMalloc(&ctx->d_palkey, sizeof(uint32_t) * KMAX));
@@ -467,7 +490,8 @@ int cqb_destroy(cqb_ctx* ctx) {
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
                  ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
-                 ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
+                 ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
+                 ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
                  ctx->d_draws};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -475,6 +499,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
   if (ctx->h_scalar) cudaFreeHost(ctx->h_scalar);
+  if (ctx->h_mom) cudaFreeHost(ctx->h_mom);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pev)
@@ -772,6 +797,126 @@ int cqb_mse(cqb_ctx* ctx, const uint8_t* a, const uint8_t* b, uint64_t n_pixels,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   *out = (double)ctx->h_scalar[0] / (double)n_pixels;
+  return CQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sharded WSM (multi-GPU): one step of the same persistent loop over a sample
+// range, exact moments out; reduction and termination live in the host driver.
+
+int cqb_shard_prepare(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k, uint64_t seed, uint64_t* n_unique,
+                      double* init_centers) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (n_pixels == 0 || !rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "build_histogram: empty image");
+  TRY(check_k(ctx, k));
+  CK(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  TRY(ensure_pixels(ctx, n_pixels));
+  TRY(ensure_samples(ctx, n_pixels));
+  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  const int ndraws = k + 64;
+  TRY(upload_draws(ctx, seed, ndraws));
+  TRY(reset_state(ctx));
+  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
+  TRY(enqueue_morton(ctx));
+  k_init_centers<<<1, KMAX, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
+  CKL();
+  CK(cudaMemsetAsync(ctx->d_labels, 0, n_pixels, ctx->stream));
+  CK(cudaMemcpyAsync(&ctx->h_stage->status, &ctx->st->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_stage->centers, ctx->st->C[0], sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  TRY(check_status(ctx));
+  if (n_unique) *n_unique = ctx->h_scalar[0];
+  if (init_centers) memcpy(init_centers, ctx->h_stage->centers, sizeof(double) * 3 * (size_t)k);
+  ctx->shard_k = k;
+  ctx->shard_total = n_pixels;
+  return CQB_OK;
+}
+
+int cqb_shard_step(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const double* centers, int dense_first,
+                   uint64_t* moments, uint64_t* point_evals) {
+  if (!ctx || !centers || !moments) return CQB_ERR_INVALID_ARGUMENT;
+  if (ctx->shard_k < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_shard_prepare first");
+  const int k = ctx->shard_k;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->st->C[0], centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  TRY(reset_state(ctx));
+  TRY(ensure_hist(ctx, 1));
+  const cqb_termination one{0, 1, 1e-4, 1};
+  TRY(launch_loop(ctx, k, &one, dense_first, ctx->shard_total, nullptr, 0, lo, hi, 1));
+  CK(cudaMemcpyAsync(ctx->h_mom, ctx->st->acc, sizeof(unsigned long long) * 5 * KMAX, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_mom + 5 * KMAX, &ctx->st->evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(&ctx->h_stage->status, &ctx->st->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  TRY(check_status(ctx));
+  for (int f = 0; f < 5; ++f)
+    for (int c = 0; c < k; ++c) moments[f * k + c] = ctx->h_mom[f * KMAX + c];
+  // the kernel's prologue counted a full table build; pair evaluations are the driver's
+  if (point_evals) *point_evals = ctx->h_mom[5 * KMAX] - (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+  return CQB_OK;
+}
+
+int cqb_finalize_moments(cqb_ctx* ctx, const uint64_t* moments, const double* centers_used, int k, uint64_t total,
+                         double* new_centers, double* sse, int* n_empty, int* empty_list) {
+  if (!ctx || !moments || !centers_used) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(check_k(ctx, k));
+  CK(cudaSetDevice(ctx->device));
+  std::vector<unsigned long long> tmp(5 * KMAX, 0ull);
+  for (int f = 0; f < 5; ++f)
+    for (int c = 0; c < k; ++c) tmp[f * KMAX + c] = moments[f * k + c];
+  CK(cudaMemcpyAsync(ctx->d_mom, tmp.data(), sizeof(unsigned long long) * 5 * KMAX, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_centers_in, centers_used, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  k_finalize<<<1, KMAX, 0, ctx->stream>>>(ctx->d_mom, ctx->d_centers_in, k, total, ctx->d_Cnew, ctx->d_scal,
+                                          ctx->d_ints, ctx->d_ints + 1);
+  CKL();
+  std::vector<int> ints(KMAX + 1);
+  double s = 0;
+  CK(cudaMemcpyAsync(new_centers, ctx->d_Cnew, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&s, ctx->d_scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ints.data(), ctx->d_ints, sizeof(int) * (KMAX + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (sse) *sse = s;
+  if (n_empty) *n_empty = ints[0];
+  if (empty_list)
+    for (int i = 0; i < ints[0]; ++i) empty_list[i] = ints[1 + i];
+  return CQB_OK;
+}
+
+int cqb_shard_reseed_candidate(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const double* centers_used,
+                               const uint32_t* taken_ranks, int n_taken, double* d_out, uint32_t* rank_out,
+                               uint32_t* key_out) {
+  if (!ctx || !centers_used) return CQB_ERR_INVALID_ARGUMENT;
+  const int k = ctx->shard_k;
+  if (k < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_shard_prepare first");
+  if (n_taken < 0 || n_taken > KMAX) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "bad taken list");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->d_centers_in, centers_used, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (n_taken)
+    CK(cudaMemcpyAsync(ctx->d_taken, taken_ranks, sizeof(uint32_t) * (size_t)n_taken, cudaMemcpyHostToDevice,
+                       ctx->stream));
+  const int nb = ctx->num_sms * 2;
+  k_reseed_scan<<<nb, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mrank, ctx->d_labels, lo, hi, ctx->d_centers_in,
+                                             ctx->d_taken, n_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k);
+  CKL();
+  k_reseed_pick<<<1, 32, 0, ctx->stream>>>(ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, nb, ctx->d_scal + 1,
+                                           reinterpret_cast<unsigned int*>(ctx->d_ints + KMAX + 2),
+                                           reinterpret_cast<unsigned int*>(ctx->d_ints + KMAX + 3));
+  CKL();
+  double d = 0;
+  unsigned int rk[2] = {0, 0};
+  CK(cudaMemcpyAsync(&d, ctx->d_scal + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(rk, ctx->d_ints + KMAX + 2, sizeof(unsigned int) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (d_out) *d_out = d;
+  if (rank_out) *rank_out = rk[0];
+  if (key_out) *key_out = rk[1];
   return CQB_OK;
 }
 

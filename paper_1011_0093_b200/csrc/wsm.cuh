@@ -77,6 +77,7 @@ struct LoopParams {
   double* traj;
   int traj_cap;
   unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (8 per iteration)
+  int moments_only;  // sharded step: stop after assign + flush (global sums = this shard's moments)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
   int stamp_iter;
 };
@@ -184,7 +185,7 @@ struct LoopSmem {
   uint32_t row0[KMAX];                   // dense path: sorted d(c_0, .) as integers
   double rowd[2][KMAX];                  // tables scratch (two rows per pass)
   int rank_part[2][2][KMAX];             // tables: [row][half of u-range][t]
-  int row_sorted[2];                     // tables: previous permutation still sorted
+  uint8_t rowo[2][KMAX];                 // tables: permutation being repaired
   unsigned long long red_u64[LOOP_THREADS / 32];
   double red_hi[LOOP_THREADS / 32], red_lo[LOOP_THREADS / 32];
   int red_i[LOOP_THREADS / 32];
@@ -232,41 +233,65 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
   const int t = tid & (KMAX - 1);             // element / position
   const int h = (tid >> 8) & 1;               // half of the u-range
   const int p = r ? pb : pa;
-  if (tid < 2) S.row_sorted[tid] = incremental ? 1 : 0;
-  if (p >= 0 && h == 0 && t < k)
+  const bool lead = p >= 0 && h == 0;         // one thread per (row, element)
+  if (lead && t < k) {
     S.rowd[r][t] = t == p ? 0.0 : dist2_rn(S.cx[p], S.cy[p], S.cz[p], S.cx[t], S.cy[t], S.cz[t]);
-  __syncthreads();
-  uint8_t e_t = 0;
-  if (incremental && p >= 0 && h == 0 && t < k) {
-    e_t = st->order[p * KMAX + t];
-    if (t >= 1 && t + 1 < k) {
-      const int e_n = st->order[p * KMAX + t + 1];
-      const double da = S.rowd[r][e_t], db = S.rowd[r][e_n];
-      const bool ok = (da < db) || (da == db && (int)e_t < e_n);
-      if (!ok) S.row_sorted[r] = 0;
-    }
+    if (incremental) S.rowo[r][t] = st->order[p * KMAX + t];
   }
   __syncthreads();
-  const bool sorted_r = S.row_sorted[r] != 0;
-  if (sorted_r) {
-    if (p >= 0 && h == 0 && t < k) st->sortedD[p * KMAX + t] = S.rowd[r][e_t];
-  } else if (p >= 0 && t < k) {
-    int cnt = 0;
-    if (t != p) {
-      const double dt = S.rowd[r][t];
-      const int u0 = h * (KMAX / 2), u1 = min(k, u0 + KMAX / 2);
-      for (int u = u0; u < u1; ++u) {
-        const double du = S.rowd[r][u];
-        cnt += (u != p) & ((du < dt) | ((du == dt) & (u < t)));
+  bool resort = !incremental;
+  if (incremental) {
+    // Odd-even transposition sort of positions 1..k-1 starting from the
+    // previous permutation, by (d, index). A row that is still in order
+    // converges in one round; repair is capped, then falls back to a full
+    // rank-count sort.
+    int rounds = 0;
+    bool again = true;
+    while (again && rounds < 16) {
+      int swapped = 0;
+#pragma unroll
+      for (int ph = 0; ph < 2; ++ph) {
+        const int pos = 1 + ph + 2 * t;
+        if (lead && pos + 1 < k) {
+          const int ea = S.rowo[r][pos], eb = S.rowo[r][pos + 1];
+          const double da = S.rowd[r][ea], db = S.rowd[r][eb];
+          if (db < da || (db == da && eb < ea)) {
+            S.rowo[r][pos] = (uint8_t)eb;
+            S.rowo[r][pos + 1] = (uint8_t)ea;
+            swapped = 1;
+          }
+        }
+        __syncthreads();
       }
+      again = __syncthreads_or(swapped) != 0;
+      ++rounds;
     }
-    S.rank_part[r][h][t] = cnt;
+    resort = again;
+    if (!resort && lead && t < k) {
+      const int e = S.rowo[r][t];
+      st->sortedD[p * KMAX + t] = S.rowd[r][e];
+      st->order[p * KMAX + t] = (uint8_t)e;
+    }
   }
-  __syncthreads();
-  if (!sorted_r && p >= 0 && h == 0 && t < k) {
-    const int rank = t == p ? 0 : 1 + S.rank_part[r][0][t] + S.rank_part[r][1][t];
-    st->sortedD[p * KMAX + rank] = S.rowd[r][t];
-    st->order[p * KMAX + rank] = (uint8_t)t;
+  if (resort) {  // full rank-count sort (uniform across the block)
+    if (p >= 0 && t < k) {
+      int cnt = 0;
+      if (t != p) {
+        const double dt = S.rowd[r][t];
+        const int u0 = h * (KMAX / 2), u1 = min(k, u0 + KMAX / 2);
+        for (int u = u0; u < u1; ++u) {
+          const double du = S.rowd[r][u];
+          cnt += (u != p) & ((du < dt) | ((du == dt) & (u < t)));
+        }
+      }
+      S.rank_part[r][h][t] = cnt;
+    }
+    __syncthreads();
+    if (lead && t < k) {
+      const int rank = t == p ? 0 : 1 + S.rank_part[r][0][t] + S.rank_part[r][1][t];
+      st->sortedD[p * KMAX + rank] = S.rowd[r][t];
+      st->order[p * KMAX + rank] = (uint8_t)t;
+    }
   }
   __syncthreads();
 }
@@ -419,7 +444,8 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   const int lane = threadIdx.x & 31;
   const double* __restrict__ gd = L.st->sortedD;
   const uint8_t* __restrict__ go = L.st->order;
-  const int k = L.k, R = RS.R;
+  const int k = L.k;
+  (void)RS;
   // warp-uniform trip count (every lane of a warp runs the same batches)
   for (unsigned long long base = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; base - lane < hi;
        base += PPT * T) {
@@ -438,33 +464,62 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       const double x0 = (double)key_r(key[q]), x1 = (double)key_g(key[q]), x2 = (double)key_b(key[q]);
       double mind = 0.0, bound = 0.0;
       int best = p;
-      bool deep = false;
       if (valid) {
-        const double prev = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);
-        bound = 4.0 * prev;
-        mind = prev;
-        const double* rd = RS.d + p * RS.stride;
-        const uint8_t* ro = RS.o + p * RS.stride;
-        // exponential then binary search: most points stop at J = 1
-        int J = 1;
-        if (R > 1 && rd[1] < bound) {
-          int lo_j = 1, hi_j = R;
-          for (int st2 = 2; st2 < R; st2 <<= 1) {
+        mind = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);  // prev
+        bound = 4.0 * mind;
+      }
+      const unsigned act = __ballot_sync(0xffffffffu, valid);
+      const int p0 = __shfl_sync(0xffffffffu, p, act ? __ffs(act) - 1 : 0);
+      int J = 1;  // prev + (J - 1) candidates: the reference's evaluation count
+      if (act && __all_sync(0xffffffffu, !valid || p == p0)) {
+        // Coherent warp (one shared previous center): lane l holds entry l of
+        // row p; each point finds its break index by a 5-step shuffle binary
+        // search and the candidates come by shuffle (broadcast center reads).
+        const int kk = k < 32 ? k : 32;
+        const double rdl = lane < kk ? gd[p0 * KMAX + lane] : 0.0;
+        const int tl = lane < kk ? (int)go[p0 * KMAX + lane] : 0;
+        int pos = 0;  // largest index with d[p][t] < bound (entry 0 is p itself, d = 0)
+#pragma unroll
+        for (int s2 = 16; s2 > 0; s2 >>= 1) {
+          const double v = __shfl_sync(0xffffffffu, rdl, (pos + s2) & 31);
+          if (pos + s2 < kk && v < bound) pos += s2;
+        }
+        J = valid ? pos + 1 : 1;
+        const int jmax = __reduce_max_sync(0xffffffffu, (unsigned)J);
+        for (int j = 1; j < jmax; ++j) {
+          const int t = __shfl_sync(0xffffffffu, tl, j);
+          if (j < J) lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+        }
+        if (valid && J == kk && kk < k) {  // rare: scan continues past entry 31
+          for (; J < k; ++J) {
+            if (gd[p * KMAX + J] >= bound) break;
+            const int t = go[p * KMAX + J];
+            lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+          }
+          n_deep += 1;
+        }
+      } else if (valid) {
+        // Generic lane-local scan: exponential + binary search for the break
+        // index in row p, then the J - 1 candidates.
+        const double* rd = gd + p * KMAX;
+        const uint8_t* ro = go + p * KMAX;
+        if (k > 1 && rd[1] < bound) {
+          int lo_j = 1, hi_j = k;
+          for (int st2 = 2; st2 < k; st2 <<= 1) {
             if (rd[st2] >= bound) {
               hi_j = st2;
               break;
             }
             lo_j = st2;
           }
-          int a = lo_j + 1, b = hi_j;
-          while (a < b) {
-            const int m = (a + b) >> 1;
-            if (rd[m] >= bound) b = m;
-            else a = m + 1;
+          int a2 = lo_j + 1, b2 = hi_j;
+          while (a2 < b2) {
+            const int m = (a2 + b2) >> 1;
+            if (rd[m] >= bound) b2 = m;
+            else a2 = m + 1;
           }
-          J = a;
+          J = a2;
         }
-        evals += (unsigned long long)J;  // prev + (J - 1) candidates
         int j = 1;
         for (; j + 1 < J; j += 2) {
           const int t0 = ro[j], t1 = ro[j + 1];
@@ -477,45 +532,8 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
           const int t0 = ro[j];
           lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]), t0);
         }
-        deep = (J == R) && (R < k);
       }
-      unsigned dm = __ballot_sync(0xffffffffu, deep);
-      n_deep += deep;
-      while (dm) {  // warp-cooperative continuation of each deep lane's scan
-        const int src = __ffs(dm) - 1;
-        dm &= dm - 1;
-        const int pp = __shfl_sync(0xffffffffu, p, src);
-        const double bb = __shfl_sync(0xffffffffu, bound, src);
-        const double y0 = __shfl_sync(0xffffffffu, x0, src), y1 = __shfl_sync(0xffffffffu, x1, src);
-        const double y2 = __shfl_sync(0xffffffffu, x2, src);
-        double wm = __shfl_sync(0xffffffffu, mind, src);
-        int wb = __shfl_sync(0xffffffffu, best, src);
-        for (int j0 = R; j0 < k; j0 += 32) {
-          const int j = j0 + lane;
-          const bool in = j < k && gd[pp * KMAX + (j < k ? j : 0)] < bb;
-          const unsigned okm = __ballot_sync(0xffffffffu, in);
-          const int nev = __ffs(~okm) ? __ffs(~okm) - 1 : 32;  // leading lanes before the break
-          double d = __longlong_as_double(0x7ff0000000000000LL);
-          int t = 0x7fffffff;
-          if (lane < nev) {
-            t = go[pp * KMAX + j];
-            d = dist2_rn(y0, y1, y2, S.cx[t], S.cy[t], S.cz[t]);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(0xffffffffu, d, o);
-            const int ot = __shfl_xor_sync(0xffffffffu, t, o);
-            lex_min(d, t, od, ot);
-          }
-          lex_min(wm, wb, d, t);
-          if (lane == 0) evals += (unsigned long long)nev;
-          if (nev < 32) break;
-        }
-        if (lane == src) {
-          mind = wm;
-          best = wb;
-        }
-      }
+      if (valid) evals += (unsigned long long)J;
       nlab[q] = valid ? best : lab[q];
     }
     uint32_t cnt[PPT];
@@ -788,6 +806,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     grid.sync();
     if (rec_it) tl[(it - 1) * 8 + 4] = globaltimer();
     BLOCK_STAMP(3);
+    if (L.moments_only) break;
 
     // ---------------- finalize(it) ----------------
     // Every block: new centers S/N (FP64, exact integer inputs) + empty count.
@@ -895,6 +914,140 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += S.red_u64[w];
     atomicAdd(&st->evals, tot);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Sharded-run helpers (multi-GPU host driver, paper_1011_0093_b200/distributed.py).
+
+// Device finalize of reduced moments (same math as the loop's finalize):
+// new centers S/N, moment-form double-double SSE, ascending empty list.
+// One block of KMAX threads.
+__global__ void __launch_bounds__(KMAX) k_finalize(const unsigned long long* __restrict__ mom, const double* __restrict__ Cused,
+                                                   int k, unsigned long long total, double* __restrict__ Cnew,
+                                                   double* __restrict__ sse_out, int* __restrict__ n_empty_out,
+                                                   int* __restrict__ empty_list) {
+  __shared__ double s_hi[KMAX / 32], s_lo[KMAX / 32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  dd part{0.0, 0.0};
+  int empty = 0;
+  if (t < k) {
+    const unsigned long long N = mom[3 * KMAX + t];
+    if (N) {
+      const double dn = (double)N;
+      const double Sr = (double)mom[t], Sg = (double)mom[KMAX + t], Sb = (double)mom[2 * KMAX + t];
+      const double Q = (double)mom[4 * KMAX + t];
+      Cnew[3 * t] = Sr / dn;
+      Cnew[3 * t + 1] = Sg / dn;
+      Cnew[3 * t + 2] = Sb / dn;
+      const double cr = Cused[3 * t], cgc = Cused[3 * t + 1], cbc = Cused[3 * t + 2];
+      dd cs = dd_add(dd_add(two_prod(cr, Sr), two_prod(cgc, Sg)), two_prod(cbc, Sb));
+      dd c2 = dd_add(dd_add(two_prod(cr, cr), two_prod(cgc, cgc)), two_prod(cbc, cbc));
+      dd term = dd_add(dd{Q, 0.0}, dd_scale(cs, -2.0));
+      part = dd_add(term, dd_scale(c2, dn));
+    } else {
+      empty = 1;
+      Cnew[3 * t] = Cused[3 * t];
+      Cnew[3 * t + 1] = Cused[3 * t + 1];
+      Cnew[3 * t + 2] = Cused[3 * t + 2];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd w{__shfl_xor_sync(0xffffffffu, part.hi, o), __shfl_xor_sync(0xffffffffu, part.lo, o)};
+    part = dd_add(part, w);
+  }
+  const int ne = __syncthreads_count(empty);
+  if (lane == 0) {
+    s_hi[wid] = part.hi;
+    s_lo[wid] = part.lo;
+  }
+  __syncthreads();
+  if (t == 0) {
+    dd tot{0.0, 0.0};
+    for (int w = 0; w < KMAX / 32; ++w) tot = dd_add(tot, dd{s_hi[w], s_lo[w]});
+    *sse_out = fmax(__dadd_rn(tot.hi, tot.lo) * (1.0 / (double)total), 0.0);
+    *n_empty_out = ne;
+    int m = 0;
+    for (int c = 0; c < k; ++c)
+      if (mom[3 * KMAX + c] == 0ull) empty_list[m++] = c;
+  }
+}
+
+// Reseed candidate of a shard: lexicographic max of (dist to own center,
+// -first-occurrence rank) over samples [lo, hi) whose rank is not taken.
+__global__ void k_reseed_scan(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank,
+                              const uint8_t* __restrict__ labels, unsigned long long lo, unsigned long long hi,
+                              const double* __restrict__ C, const uint32_t* __restrict__ taken, int n_taken,
+                              double* __restrict__ cand_d, unsigned int* __restrict__ cand_r,
+                              unsigned int* __restrict__ cand_k) {
+  __shared__ double sd[32];
+  __shared__ unsigned int sr[32], sk[32];
+  double bd = -1.0;
+  unsigned int br = 0xffffffffu, bk = 0u;
+  for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned int rk = rank[i];
+    bool used = false;
+    for (int e = 0; e < n_taken; ++e) used |= taken[e] == rk;
+    if (used) continue;
+    const uint32_t key = keys[i];
+    const int m = labels[i];
+    const double d = dist2_rn((double)key_r(key), (double)key_g(key), (double)key_b(key), C[3 * m], C[3 * m + 1],
+                              C[3 * m + 2]);
+    if (cand_better(d, rk, bd, br)) {
+      bd = d;
+      br = rk;
+      bk = key;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const unsigned int orr = __shfl_xor_sync(0xffffffffu, br, o);
+    const unsigned int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+    if (cand_better(od, orr, bd, br)) {
+      bd = od;
+      br = orr;
+      bk = ok;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sd[threadIdx.x >> 5] = bd;
+    sr[threadIdx.x >> 5] = br;
+    sk[threadIdx.x >> 5] = bk;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bd = sd[0];
+    br = sr[0];
+    bk = sk[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (cand_better(sd[w], sr[w], bd, br)) {
+        bd = sd[w];
+        br = sr[w];
+        bk = sk[w];
+      }
+    cand_d[blockIdx.x] = bd;
+    cand_r[blockIdx.x] = br;
+    cand_k[blockIdx.x] = bk;
+  }
+}
+
+__global__ void k_reseed_pick(const double* __restrict__ cand_d, const unsigned int* __restrict__ cand_r,
+                              const unsigned int* __restrict__ cand_k, int nb, double* out_d,
+                              unsigned int* out_r, unsigned int* out_k) {
+  if (threadIdx.x != 0) return;
+  double bd = -1.0;
+  unsigned int br = 0xffffffffu, bk = 0u;
+  for (int b = 0; b < nb; ++b)
+    if (cand_better(cand_d[b], cand_r[b], bd, br)) {
+      bd = cand_d[b];
+      br = cand_r[b];
+      bk = cand_k[b];
+    }
+  *out_d = bd;
+  *out_r = br;
+  *out_k = bk;
 }
 
 }  // namespace cqb

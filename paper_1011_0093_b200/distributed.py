@@ -1,0 +1,220 @@
+"""Sharded WSM across GPUs (one process per GPU, torch.distributed plumbing).
+
+Config 4 of BASELINE.json: the unique samples are split into contiguous
+ranges of the Morton-ordered sample array, one per rank. Every iteration of
+run_weighted_kmeans (kmeans.hpp:336-376) becomes:
+
+  1. ``backend.step(lo, hi, C, first)`` -> this shard's EXACT integer cluster
+     moments [5][K] (Σc·r, Σc·g, Σc·b, Σc, Σc·|x|²) + its point evaluations
+     (the sharded launch of the same persistent CUDA loop, moments only);
+  2. ``allreduce(sum)`` of the moments and evaluation counts (int64, exact);
+  3. ``backend.finalize(moments, C)`` on every rank -> identical new centers,
+     moment-form SSE and empty-cluster list (device kernel);
+  4. empty clusters (rare): per-rank reseed candidate (distance desc, rank
+     asc), ``allgather``, pick the global best — update_centers'
+     kmeans.hpp:272-294 rule;
+  5. termination (kmeans.hpp:359-369) evaluated identically on every rank.
+
+Integer sums make the trajectory independent of the number of ranks and of
+the summation order, so N ranks reproduce the single-GPU run bit for bit.
+
+The backend is pluggable: ``DeviceShardBackend`` drives the CUDA library
+through the C ABI; the CPU tests plug in a numpy stand-in. The collective is
+pluggable too: ``TorchCollective`` (gloo on CPU, NCCL on GPUs) or
+``LocalCollective`` (several shards in one process: the single-GPU check).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_u8p = C.POINTER(C.c_uint8)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+_f64p = C.POINTER(C.c_double)
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced range of n samples for `rank` of `world`."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def pair_evals(prev: np.ndarray | None, cur: np.ndarray) -> int:
+    """Center-pair distance evaluations of update_center_tables
+    (kmeans.hpp:137-155): all K(K-1)/2 on the first build, then only pairs
+    with at least one center that changed bitwise."""
+    k = cur.shape[0]
+    total = k * (k - 1) // 2
+    if prev is None:
+        return total
+    still = int(np.sum(np.all(prev == cur, axis=1)))
+    return total - still * (still - 1) // 2
+
+
+# --------------------------------------------------------------------------- collectives
+class LocalCollective:
+    """Single process; all shards are local (allreduce = identity)."""
+
+    world = 1
+    rank = 0
+
+    def allreduce_sum(self, a: np.ndarray) -> np.ndarray:
+        return a
+
+    def allgather(self, obj):
+        return [obj]
+
+
+class TorchCollective:
+    """torch.distributed collectives on host int64/float64 arrays. With the
+    NCCL backend the tensors go through the current CUDA device."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+    def allreduce_sum(self, a: np.ndarray) -> np.ndarray:
+        t = self.torch.from_numpy(np.ascontiguousarray(a).view(np.int64).copy()).to(self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t.cpu().numpy().view(a.dtype).reshape(a.shape)
+
+    def allgather(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+# --------------------------------------------------------------------------- device backend
+class DeviceShardBackend:
+    """The CUDA library through the sharded C-ABI entry points."""
+
+    def __init__(self, device: int = 0):
+        from . import _native
+
+        self.ctx = _native.context(device)
+        self.lib = self.ctx.lib
+        self.k = 0
+
+    def prepare(self, img: np.ndarray, k: int, seed: int):
+        a = np.ascontiguousarray(img, np.uint8)
+        P = a.size // 3
+        n = C.c_uint64()
+        C0 = np.zeros((k, 3))
+        self.ctx.check(self.lib.cqb_shard_prepare(self.ctx.h, a.ctypes.data_as(_u8p), P, k, seed, C.byref(n),
+                                                  C0.ctypes.data_as(_f64p)))
+        self.k, self.total = k, P
+        return int(n.value), P, C0
+
+    def step(self, lo: int, hi: int, centers: np.ndarray, first: bool):
+        Cin = np.ascontiguousarray(centers, np.float64)
+        mom = np.zeros((5, self.k), np.uint64)
+        ev = C.c_uint64()
+        self.ctx.check(self.lib.cqb_shard_step(self.ctx.h, lo, hi, Cin.ctypes.data_as(_f64p), int(first),
+                                               mom.ctypes.data_as(_u64p), C.byref(ev)))
+        return mom, int(ev.value)
+
+    def finalize(self, moments: np.ndarray, centers: np.ndarray, total: int):
+        k = centers.shape[0]
+        mom = np.ascontiguousarray(moments, np.uint64)
+        Cin = np.ascontiguousarray(centers, np.float64)
+        out = np.zeros((k, 3))
+        sse = C.c_double()
+        ne = C.c_int()
+        el = (C.c_int * max(k, 1))()
+        self.ctx.check(self.lib.cqb_finalize_moments(self.ctx.h, mom.ctypes.data_as(_u64p), Cin.ctypes.data_as(_f64p),
+                                                     k, total, out.ctypes.data_as(_f64p), C.byref(sse), C.byref(ne),
+                                                     el))
+        return out, float(sse.value), [int(el[i]) for i in range(ne.value)]
+
+    def reseed_candidate(self, lo: int, hi: int, centers: np.ndarray, taken: list):
+        Cin = np.ascontiguousarray(centers, np.float64)
+        tk = np.array(taken if taken else [0], np.uint32)
+        d = C.c_double()
+        r = C.c_uint32()
+        key = C.c_uint32()
+        self.ctx.check(self.lib.cqb_shard_reseed_candidate(self.ctx.h, lo, hi, Cin.ctypes.data_as(_f64p),
+                                                           tk.ctypes.data_as(_u32p), len(taken), C.byref(d),
+                                                           C.byref(r), C.byref(key)))
+        return float(d.value), int(r.value), int(key.value)
+
+
+# --------------------------------------------------------------------------- driver
+@dataclass
+class ShardedResult:
+    centers: np.ndarray
+    iterations: int
+    sse: float
+    dist_evals: int
+    sse_history: list = field(default_factory=list)
+    trajectory: list = field(default_factory=list)
+    n_unique: int = 0
+
+
+def _better(a, b) -> bool:
+    """Reseed order: distance desc, then first-occurrence rank asc."""
+    return a[0] > b[0] or (a[0] == b[0] and a[1] < b[1])
+
+
+def run_wsm_sharded(backend, img: np.ndarray, k: int, mode: int = 1, max_iters: int = 10, eps: float = 1e-4,
+                    cap: int = 100, seed: int = 1, coll=None, shards: int | None = None) -> ShardedResult:
+    """WSM (mode 0) / WSM-C (mode 1) with the samples sharded over the ranks
+    of `coll` (each rank owns one contiguous range). With LocalCollective and
+    `shards` = W, one process runs W shards sequentially — the single-GPU
+    check that sharding is exact."""
+    coll = coll or LocalCollective()
+    n, total, Cur = backend.prepare(img, k, seed)
+    if shards is None:
+        my = [shard_range(n, coll.world, coll.rank)]
+    else:
+        my = [shard_range(n, shards, r) for r in range(shards)]
+    prev_sse = math.inf
+    evals = 0
+    res = ShardedResult(Cur, 0, 0.0, 0, n_unique=n)
+    Cprev = None
+    it = 0
+    while True:
+        it += 1
+        evals += pair_evals(Cprev, Cur) if coll.rank == 0 else 0
+        mom = np.zeros((5, k), np.uint64)
+        ev = 0
+        for lo, hi in my:
+            m, e = backend.step(lo, hi, Cur, it == 1)
+            mom += m
+            ev += e
+        mom = coll.allreduce_sum(mom)
+        evals += ev
+        Cnew, sse, empties = backend.finalize(mom, Cur, total)
+        taken: list = []
+        for e_cl in empties:
+            best = (-1.0, 0xFFFFFFFF, 0)
+            for lo, hi in my:
+                cand = backend.reseed_candidate(lo, hi, Cur, taken)
+                if _better(cand, best):
+                    best = cand
+            for cand in coll.allgather(best):
+                if _better(cand, best):
+                    best = cand
+            taken.append(best[1])
+            key = best[2]
+            Cnew[e_cl] = ((key >> 16) & 255, (key >> 8) & 255, key & 255)
+        res.sse_history.append(sse)
+        res.trajectory.append(Cnew.copy())
+        Cprev, Cur = Cur, Cnew
+        if mode == 0:
+            stop = it >= max_iters
+        else:
+            stop = sse == 0.0 or (prev_sse - sse) / sse <= eps or it >= cap
+        prev_sse = sse
+        if stop:
+            break
+    total_evals = coll.allreduce_sum(np.array([evals], np.uint64))[0]
+    res.centers, res.iterations, res.sse, res.dist_evals = Cur, it, res.sse_history[-1], int(total_evals)
+    return res

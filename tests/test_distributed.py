@@ -1,0 +1,222 @@
+"""CPU-only: the multi-GPU host logic (paper_1011_0093_b200/distributed.py).
+
+World-size-2 `gloo` process groups on 127.0.0.1 run the sharded driver with a
+CPU stand-in backend (numpy + the oracle's primitive functions, test
+infrastructure only). The sharded trajectory must equal the single-process
+oracle run: iterations, centers (bit-exact for power-of-two P), dist_evals,
+SSE history — including the empty-cluster reseed exchanged via allgather.
+"""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1011_0093_b200.configs import gmm_image
+from paper_1011_0093_b200.distributed import LocalCollective, pair_evals, run_wsm_sharded, shard_range
+
+_f64p = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def _morton(keys):
+    def spread(v):
+        v = v.astype(np.uint64) & 0xFF
+        v = (v | (v << 8)) & 0x0000F00F
+        v = (v | (v << 4)) & 0x000C30C3
+        v = (v | (v << 2)) & 0x00249249
+        return v
+    k = keys.astype(np.uint64)
+    return (spread(k >> 16) << 2) | (spread(k >> 8) << 1) | spread(k)
+
+
+class FakeShardBackend:
+    """CPU stand-in for DeviceShardBackend (test infrastructure)."""
+
+    def __init__(self, init_override=None):
+        from oracle.oracle import Oracle
+
+        self.o = Oracle("port")
+        self.init_override = init_override
+
+    def prepare(self, img, k, seed):
+        h = self.o.build_histogram(img)
+        order = np.argsort(_morton(h.keys), kind="stable")
+        self.keys = h.keys[order]
+        self.counts = h.counts[order].astype(np.uint64)
+        self.rank = order.astype(np.uint32)  # first-occurrence rank of each Morton-ordered sample
+        self.X = np.stack([(self.keys >> 16) & 255, (self.keys >> 8) & 255, self.keys & 255], 1).astype(np.float64)
+        self.labels = np.zeros(len(self.keys), np.int32)
+        self.k = k
+        self.total = img.shape[0] * img.shape[1]
+        C0 = self.o.init_centers(h.keys, k, seed) if self.init_override is None else self.init_override.copy()
+        return len(self.keys), self.total, C0
+
+    def step(self, lo, hi, centers, first):
+        k = self.k
+        Cc = np.ascontiguousarray(centers, np.float64)
+        D = np.zeros(k * k)
+        order = np.zeros(k * k, np.int32)
+        f = self.o._f
+        f("center_tables")(Cc.ctypes.data_as(_f64p), k, D.ctypes.data_as(_f64p), order.ctypes.data_as(_i32p))
+        X = np.ascontiguousarray(self.X[lo:hi])
+        W = np.ones(hi - lo)
+        lab = np.ascontiguousarray(self.labels[lo:hi])
+        sse = np.zeros(1)
+        ev = np.zeros(1, np.uint64)
+        f("assign_sort_means")(X.ctypes.data_as(_f64p), W.ctypes.data_as(_f64p), hi - lo, Cc.ctypes.data_as(_f64p), k,
+                               D.ctypes.data_as(_f64p), order.ctypes.data_as(_i32p), lab.ctypes.data_as(_i32p),
+                               sse.ctypes.data_as(_f64p), ev.ctypes.data_as(_u64p))
+        self.labels[lo:hi] = lab
+        c = self.counts[lo:hi]
+        xi = self.X[lo:hi].astype(np.uint64)
+        mom = np.zeros((5, k), np.uint64)
+        for fld, v in enumerate([c * xi[:, 0], c * xi[:, 1], c * xi[:, 2], c,
+                                 c * (xi[:, 0] ** 2 + xi[:, 1] ** 2 + xi[:, 2] ** 2)]):
+            np.add.at(mom[fld], lab, v)
+        return mom, int(ev[0])
+
+    def finalize(self, mom, centers, total):
+        N = mom[3].astype(np.float64)
+        new = centers.copy()
+        nz = mom[3] > 0
+        for ch in range(3):
+            new[nz, ch] = mom[ch][nz].astype(np.float64) / N[nz]
+        Cc = centers
+        sse = 0.0
+        for t in np.nonzero(nz)[0]:
+            S = mom[:3, t].astype(np.float64)
+            sse += float(mom[4, t]) - 2 * float(np.dot(Cc[t], S)) + float(np.dot(Cc[t], Cc[t])) * N[t]
+        return new, max(sse / total, 0.0), [int(t) for t in np.nonzero(~nz)[0]]
+
+    def reseed_candidate(self, lo, hi, centers, taken):
+        X = self.X[lo:hi]
+        lab = self.labels[lo:hi]
+        d = ((X - centers[lab]) ** 2).sum(1)
+        best = (-1.0, 0xFFFFFFFF, 0)
+        for j in range(hi - lo):
+            r = int(self.rank[lo + j])
+            if r in taken:
+                continue
+            if d[j] > best[0] or (d[j] == best[0] and r < best[1]):
+                best = (float(d[j]), r, int(self.keys[lo + j]))
+        return best
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, img, k, mode, iters, init_override, out_q):
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200.distributed import TorchCollective
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = run_wsm_sharded(FakeShardBackend(init_override), img, k, mode=mode, max_iters=iters, coll=TorchCollective())
+        out_q.put((rank, res.centers, res.iterations, res.dist_evals, res.sse_history))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_gloo(world, img, k, mode=1, iters=10, init_override=None):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, img, k, mode, iters, init_override, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(outs, key=lambda o: o[0])
+
+
+def test_shard_ranges_cover_exactly():
+    for n in (1, 7, 1000, 366922):
+        for w in (1, 2, 3, 8):
+            rs = [shard_range(n, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_pair_evals_rule():
+    C0 = np.arange(12.0).reshape(4, 3)
+    assert pair_evals(None, C0) == 6
+    C1 = C0.copy()
+    assert pair_evals(C0, C1) == 0
+    C1[2, 0] += 1
+    assert pair_evals(C0, C1) == 6 - 3  # three unmoved centers keep 3 pairs
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 5])
+def test_local_shards_match_oracle(shards, port):
+    img = gmm_image(64, 32, 10, 11)  # P = 2048
+    h = port.build_histogram(img)
+    ref = port.run_wsm(h.keys, h.counts, 2048, 8, mode=1, seed=1, trajectory=True)
+    res = run_wsm_sharded(FakeShardBackend(), img, 8, shards=shards)
+    assert res.iterations == ref.iterations
+    np.testing.assert_array_equal(res.centers, ref.centers)
+    assert res.dist_evals == ref.dist_evals
+    np.testing.assert_allclose(res.sse_history, ref.sse_history, rtol=1e-9)
+
+
+def test_gloo_world2_matches_oracle(port):
+    img = gmm_image(64, 64, 12, 5)  # P = 4096
+    h = port.build_histogram(img)
+    ref = port.run_wsm(h.keys, h.counts, 4096, 12, mode=1, seed=1)
+    outs = _run_gloo(2, img, 12)
+    for rank, centers, iters, evals, hist in outs:
+        assert iters == ref.iterations
+        np.testing.assert_array_equal(centers, ref.centers)
+        assert evals == ref.dist_evals
+        np.testing.assert_allclose(hist, ref.sse_history, rtol=1e-9)
+
+
+def test_gloo_world2_empty_cluster_reseed(port):
+    """A center that owns nothing is re-seeded at the global farthest point
+    (kmeans.hpp:272-294), the candidates exchanged by allgather."""
+    img = gmm_image(32, 32, 6, 9)  # P = 1024
+    h = port.build_histogram(img)
+    init = port.init_centers(h.keys, 6, 3)
+    init[4] = (999.0, 999.0, 999.0)
+    # reference trajectory with the same init from the oracle primitives
+    X = h.colors
+    W = h.counts.astype(np.float64) / 1024.0
+    lab = np.zeros(len(X), np.int32)
+    Cc = init.copy()
+    traj = []
+    for it in range(4):
+        D = np.zeros(36)
+        order = np.zeros(36, np.int32)
+        port._f("center_tables")(Cc.ctypes.data_as(_f64p), 6, D.ctypes.data_as(_f64p), order.ctypes.data_as(_i32p))
+        sse = np.zeros(1)
+        ev = np.zeros(1, np.uint64)
+        port._f("assign_sort_means")(X.ctypes.data_as(_f64p), W.ctypes.data_as(_f64p), len(X),
+                                     Cc.ctypes.data_as(_f64p), 6, D.ctypes.data_as(_f64p),
+                                     order.ctypes.data_as(_i32p), lab.ctypes.data_as(_i32p), sse.ctypes.data_as(_f64p),
+                                     ev.ctypes.data_as(_u64p))
+        nxt = np.zeros(18)
+        port._f("update_centers")(X.ctypes.data_as(_f64p), W.ctypes.data_as(_f64p), len(X), lab.ctypes.data_as(_i32p),
+                                  Cc.ctypes.data_as(_f64p), 6, nxt.ctypes.data_as(_f64p))
+        Cc = nxt.reshape(6, 3)
+        traj.append(Cc.copy())
+    outs = _run_gloo(2, img, 6, mode=0, iters=4, init_override=init)
+    for rank, centers, iters, evals, hist in outs:
+        assert iters == 4
+        np.testing.assert_array_equal(centers, traj[-1])
+    # the far center was re-seeded onto a sample color in iteration 1
+    assert tuple(traj[0][4]) != (999.0, 999.0, 999.0)
