@@ -392,9 +392,9 @@ def _loop_phases(tl, iters):
         "barrier2_us": d(a[:, 6], nxt),
         "iteration_us": float(np.mean(np.diff(tl[1:, 0]))) / 1e3,
         "changed_per_iter": [int(v) & 0xFFFFFFFF for v in tl[1:8, 7]],
-        "deep_per_iter": [int(v) >> 32 for v in tl[1:8, 7]],
+        "active_per_iter": [int(v) >> 32 for v in tl[1:8, 7]],
         "changed_mean": float(np.mean(tl[1:, 7] & 0xFFFFFFFF)),
-        "deep_mean": float(np.mean(tl[1:, 7] >> 32)),
+        "active_mean": float(np.mean(tl[1:, 7] >> 32)),
     }
 
 

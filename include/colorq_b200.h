@@ -78,6 +78,9 @@ int cqb_device_info(cqb_ctx* ctx, int* num_sms, int* loop_blocks);
  * [4] WSM loop (tables+assign+update, all iterations), [5] map tables +
  * unique-color map + MSE, [6] per-pixel map. */
 int cqb_set_profiling(cqb_ctx* ctx, int on);
+/* Diagnostics only: disables parts of the assign phase (results become
+ * WRONG); used by tools/ablate.py to attribute time. 0 = normal. */
+int cqb_set_debug(cqb_ctx* ctx, int flags);
 int cqb_stage_times(cqb_ctx* ctx, float* ms, int n);
 /* With profiling on: %globaltimer stamps (ns) of block 0 per WSM iteration,
  * 8 per iteration: assign start, rows staged, points done, deltas flushed,

@@ -28,7 +28,7 @@ EXPORTS = (
     "cqb_build_histogram", "cqb_run_wsm", "cqb_wsm_iterate", "cqb_quantize", "cqb_quantize_device",
     "cqb_fetch_results", "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
-    "cqb_shard_reseed_candidate",
+    "cqb_shard_reseed_candidate", "cqb_set_debug",
 )
 STAGES = ("reset", "hist_count", "hist_compact", "init", "wsm_loop", "map_unique", "map_pixels")
 
@@ -99,6 +99,7 @@ def load_library() -> C.CDLL:
         L.cqb_stage_times.argtypes = [_vp, C.POINTER(C.c_float), C.c_int]
         L.cqb_loop_timeline.argtypes = [_vp, _u64p, C.c_int]
         L.cqb_block_times.argtypes = [_vp, _u64p, C.c_int]
+        L.cqb_set_debug.argtypes = [_vp, C.c_int]
         L.cqb_shard_prepare.argtypes = [_vp, _u8p, C.c_uint64, C.c_int, C.c_uint64, _u64p, _f64p]
         L.cqb_shard_step.argtypes = [_vp, C.c_uint64, C.c_uint64, _f64p, C.c_int, _u64p, _u64p]
         L.cqb_finalize_moments.argtypes = [_vp, _u64p, _f64p, C.c_int, C.c_uint64, _f64p, _f64p,

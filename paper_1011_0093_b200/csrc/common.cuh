@@ -60,6 +60,11 @@ __device__ __forceinline__ dd dd_scale(dd x, double b) {  // x * b
 }
 __device__ __forceinline__ dd dd_neg(dd x) { return {-x.hi, -x.lo}; }
 
+// Exact u8 -> double without I2F: the bits of 2^52 + v are 0x43300000:v.
+__device__ __forceinline__ double u8_to_double(uint32_t v) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);
+}
+
 __device__ __forceinline__ uint32_t key_r(uint32_t k) { return (k >> 16) & 255u; }
 __device__ __forceinline__ uint32_t key_g(uint32_t k) { return (k >> 8) & 255u; }
 __device__ __forceinline__ uint32_t key_b(uint32_t k) { return k & 255u; }

@@ -41,3 +41,8 @@ dur = lambda a, b: (ph[b] - ph[a]) / 1e3  # noqa: E731
 for a, b, n in [(0, 1, "points"), (1, 2, "flush"), (2, 3, "barrier1 wait"), (3, 4, "finalize"), (4, 5, "tables")]:
     v = dur(a, b)
     print(f"dur {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f} block0 {v[0]:6.2f}")
+
+wd = bt[6 * 1024: 6 * 1024 + 32 * 4].reshape(32, 4).astype(np.int64)
+print("block 0 per warp: phase1 cycles, drain cycles, drains")
+for w in range(32):
+    print(f"  w{w:2d} p1 {wd[w,0]:7d}  p2 {wd[w,1]:7d}  drains {wd[w,2]}")
