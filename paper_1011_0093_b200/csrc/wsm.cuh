@@ -476,38 +476,26 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       const double bound = 4.0 * mind;
       int best = p;
       const double* rd = gd + p * KMAX;
-      // break index J: first j >= 1 with d[p][t_j] >= bound (rows ascending)
+      const uint8_t* ro = go + p * KMAX;
+      // the reference's scan (kmeans.hpp:217-231), two entries per step
       int J = 1;
       if (k > 1 && rd[1] < bound && !(L.debug_flags & 1)) {
         n_active += 1;
-        int lo_j = 1, hi_j = k;
-        for (int st2 = 2; st2 < k; st2 <<= 1) {
-          if (rd[st2] >= bound) {
-            hi_j = st2;
-            break;
-          }
-          lo_j = st2;
-        }
-        int a2 = lo_j + 1, b2 = hi_j;
-        while (a2 < b2) {
-          const int m = (a2 + b2) >> 1;
-          if (rd[m] >= bound) b2 = m;
-          else a2 = m + 1;
-        }
-        J = a2;
-        const uint8_t* ro = go + p * KMAX;
         int j = 1;
-        for (; j + 1 < J; j += 2) {
-          const int t0 = ro[j], t1 = ro[j + 1];
-          const double d0 = dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]);
-          const double d1 = dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]);
-          lex_min(mind, best, d0, t0);
-          lex_min(mind, best, d1, t1);
-        }
-        if (j < J) {
+        for (;;) {
+          const double d0 = rd[j];
+          const double d1 = j + 1 < k ? rd[j + 1] : bound;
           const int t0 = ro[j];
+          const int t1 = j + 1 < k ? ro[j + 1] : 0;
+          if (d0 >= bound) break;
           lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]), t0);
+          ++j;
+          if (d1 >= bound) break;
+          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]), t1);
+          ++j;
+          if (j >= k) break;
         }
+        J = j;
       }
       ev += (uint32_t)J;  // prev + (J - 1) candidates: the reference's count
       nlab[q] = best;
