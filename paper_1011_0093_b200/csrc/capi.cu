@@ -453,7 +453,7 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMemset(ctx->st, 0, sizeof(WsmState)));
     CK(cudaMalloc(&ctx->d_n, sizeof(unsigned long long)));
     CK(cudaMalloc(&ctx->d_centers_in, sizeof(double) * 3 * KMAX));
-    CK(cudaMalloc(&ctx->d_block_times, sizeof(unsigned long long) * 8 * MAXBLK));
+    CK(cudaMalloc(&ctx->d_block_times, sizeof(unsigned long long) * 16 * MAXBLK));
     CK(cudaMalloc(&ctx->d_mom, sizeof(unsigned long long) * 5 * KMAX));
     CK(cudaMallocHost(&ctx->h_mom, sizeof(unsigned long long) * (5 * KMAX + 1)));
     CK(cudaMalloc(&ctx->d_Cnew, sizeof(double) * 3 * KMAX));
@@ -561,7 +561,7 @@ int cqb_loop_timeline(cqb_ctx* ctx, unsigned long long* stamps, int n_iters) {
 int cqb_block_times(cqb_ctx* ctx, unsigned long long* out, int n) {
   if (!ctx || !out) return CQB_ERR_INVALID_ARGUMENT;
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMemcpy(out, ctx->d_block_times, sizeof(unsigned long long) * (size_t)std::min(n, 8 * MAXBLK),
+  CK(cudaMemcpy(out, ctx->d_block_times, sizeof(unsigned long long) * (size_t)std::min(n, 16 * MAXBLK),
                 cudaMemcpyDeviceToHost));
   return CQB_OK;
 }

@@ -194,6 +194,7 @@ struct LoopSmem {
   int empty_list[KMAX];
   unsigned int taken[KMAX];
   int n_empty;
+  unsigned int wq;                       // assign: next chunk of this block's list
 };
 
 // Per-block phase stamps for one iteration (profiling): bt[phase * G + block].
@@ -445,8 +446,15 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   // J = 1 after one comparison), then the J - 1 candidates are evaluated.
   constexpr int PPT = 2;
   const uint32_t lo = (uint32_t)lo64, hi = (uint32_t)hi64;
-  const uint32_t T = gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
+  // Work split: 32-point Morton chunks dealt round-robin to the blocks
+  // (chunk c -> block c % G), so every SM gets the same number of chunks
+  // within one and samples every region of color space; inside a block the
+  // chunks are handed to the warps dynamically (shared counter), PPT at a
+  // time: a warp held up by deep scans does not hold up the block.
+  const uint32_t G = gridDim.x, W = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const uint32_t nch = (hi - lo + 31u) >> 5;
+  const uint32_t my_ch = nch > blockIdx.x ? (nch - 1u - blockIdx.x) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const uint8_t* __restrict__ go = L.st->order;
   const uint32_t* __restrict__ keys = L.keys;
@@ -455,20 +463,28 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   const int k = L.k;
   (void)RS;
   uint32_t ev = 0;
-  for (uint32_t base = lo + blockIdx.x * blockDim.x + threadIdx.x; base - lane < hi; base += PPT * T) {
-    uint32_t key[PPT];
+  (void)W;
+  (void)w;
+  for (;;) {
+    uint32_t j = 0;
+    if (lane == 0) j = atomicAdd(&S.wq, (unsigned)PPT);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    if (j >= my_ch) break;
+    uint32_t key[PPT], idx[PPT];
     int lab[PPT], nlab[PPT];
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
-      const uint32_t i = base + q * T;
-      const bool v = i < hi;
+      const uint32_t jj = j + q;
+      const uint32_t i = lo + ((blockIdx.x + G * jj) << 5) + lane;
+      const bool v = jj < my_ch && i < hi;
+      idx[q] = v ? i : hi;
       key[q] = v ? keys[i] : 0u;
       lab[q] = v ? (int)labels[i] : 0;
     }
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       nlab[q] = lab[q];
-      if (base + q * T >= hi) continue;
+      if (idx[q] >= hi) continue;
       const int p = lab[q];
       const double x0 = u8_to_double(key_r(key[q])), x1 = u8_to_double(key_g(key[q])),
                    x2 = u8_to_double(key_b(key[q]));
@@ -502,7 +518,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
     }
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
-      const uint32_t i = base + q * T;
+      const uint32_t i = idx[q];
       const bool v = i < hi;
       const bool ch = v && nlab[q] != lab[q];
       uint32_t cnt = 0;
@@ -728,6 +744,12 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     S.accm[t] = make_uint2(0u, 0u);
   }
   __syncthreads();
+  if (L.block_times && tid == 0) {  // profiling: SM of this block, evaluations in stamp_iter
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    L.block_times[6 * gridDim.x + blockIdx.x] = smid;
+    L.block_times[7 * gridDim.x + blockIdx.x] = 0ull;
+  }
   // prologue: tables of the initial centers (all pairs evaluated: non-incremental)
   tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
@@ -737,6 +759,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
   for (int it = 1;; ++it) {
     const bool rec_it = rec && it <= L.hist_cap;
+    if (tid == 0) S.wq = 0u;  // read after the __syncthreads preceding assign
     if (rec_it) tl[(it - 1) * 8 + 0] = globaltimer();
     BLOCK_STAMP(0);
     // ---------------- assign(it) ----------------
@@ -753,7 +776,12 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       __syncthreads();
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
+      const unsigned long long ev0 = evals;
       assign_sort_means(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      if (L.block_times && it == L.stamp_iter) {
+        const unsigned long long v = warp_sum(evals - ev0);
+        if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
+      }
       if (rec_it || (tl && it <= L.hist_cap)) {  // diagnostics: label churn and deep scans
         const unsigned long long v = ((unsigned long long)warp_sum(n_deep) << 32) | warp_sum(n_changed);
         if ((tid & 31) == 0 && v) atomicAdd(&tl[(it - 1) * 8 + 7], v);
@@ -772,19 +800,30 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
 
     // ---------------- finalize(it) ----------------
     // Every block: new centers S/N (FP64, exact integer inputs) + empty count.
+    // k <= KMAX <= blockDim: thread t owns cluster t. The five sums are
+    // loaded unconditionally up front (one L2 round trip, not one per
+    // division) and kept in registers for block 0's SSE below.
+    unsigned long long mS0 = 0, mS1 = 0, mS2 = 0, mN = 0, mQ = 0;
+    if (tid < k) {
+      mS0 = __ldcg(&gacc[0 * KMAX + tid]);
+      mS1 = __ldcg(&gacc[1 * KMAX + tid]);
+      mS2 = __ldcg(&gacc[2 * KMAX + tid]);
+      mN = __ldcg(&gacc[3 * KMAX + tid]);
+      if (blockIdx.x == 0) mQ = __ldcg(&gacc[4 * KMAX + tid]);
+    }
     int empt_local = 0;
-    for (int t = tid; t < k; t += blockDim.x) {
-      const unsigned long long N = gacc[3 * KMAX + t];
-      if (N) {
-        const double dn = (double)N;
-        S.nx[t] = (double)gacc[0 * KMAX + t] / dn;
-        S.ny[t] = (double)gacc[1 * KMAX + t] / dn;
-        S.nz[t] = (double)gacc[2 * KMAX + t] / dn;
+    if (tid < k) {
+      if (mN) {
+        const double dn = (double)mN;
+        S.nx[tid] = (double)mS0 / dn;
+        S.ny[tid] = (double)mS1 / dn;
+        S.nz[tid] = (double)mS2 / dn;
       } else {
         empt_local = 1;
       }
     }
     const int empt = __syncthreads_count(empt_local);  // k <= blockDim: one cluster per thread
+    BLOCK_STAMP(8);
     if (empt) {  // rare: empty clusters (uniform across the grid)
       if (tid == 0) {
         S.n_empty = empt;
@@ -799,13 +838,13 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     if (blockIdx.x == 0) {
       dd part{0.0, 0.0};
       int moved = 0, unused = 0;
-      for (int t = tid; t < k; t += blockDim.x) {
+      if (tid < k) {
+        const int t = tid;
         moved += (S.nx[t] != S.cx[t]) | (S.ny[t] != S.cy[t]) | (S.nz[t] != S.cz[t]);
-        const unsigned long long N = gacc[3 * KMAX + t];
-        if (N) {
-          const double dn = (double)N;
-          const double Sr = (double)gacc[0 * KMAX + t], Sg = (double)gacc[1 * KMAX + t];
-          const double Sb = (double)gacc[2 * KMAX + t], Q = (double)gacc[4 * KMAX + t];
+        if (mN) {
+          const double dn = (double)mN;
+          const double Sr = (double)mS0, Sg = (double)mS1;
+          const double Sb = (double)mS2, Q = (double)mQ;
           const double cr = S.cx[t], cgc = S.cy[t], cbc = S.cz[t];
           // Q - 2 c.S + |c|^2 N with the centers of THIS assignment
           dd cs = dd_add(dd_add(two_prod(cr, Sr), two_prod(cgc, Sg)), two_prod(cbc, Sb));
@@ -851,6 +890,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         }
     }
     __syncthreads();
+    BLOCK_STAMP(9);
     for (int t = tid; t < k; t += blockDim.x) {
       S.cx[t] = S.nx[t];
       S.cy[t] = S.ny[t];

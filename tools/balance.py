@@ -28,9 +28,11 @@ for _ in range(2):
     ctx.check(lib.cqb_quantize_device(ctx.h, C.c_void_p(d.data_ptr()), cfg.pixels, 256, C.byref(term), 1, None, None, 1,
                                       cent.ctypes.data_as(C.POINTER(C.c_double)),
                                       hist.ctypes.data_as(C.POINTER(C.c_double)), 100, C.byref(rep)))
-bt = np.zeros(8 * 1024, np.uint64)
-lib.cqb_block_times(ctx.h, bt.ctypes.data_as(C.POINTER(C.c_uint64)), 8 * 1024)
+bt = np.zeros(16 * 1024, np.uint64)
+lib.cqb_block_times(ctx.h, bt.ctypes.data_as(C.POINTER(C.c_uint64)), 16 * 1024)
 ph = bt[: 6 * g].reshape(6, g).astype(np.int64)
+if len(sys.argv) > 3:
+    np.save(sys.argv[3], bt)
 t0 = ph[0].min()
 names = ["iter start (after barrier2)", "points done", "flush done", "barrier1 exit", "finalize done", "tables done"]
 for i, n in enumerate(names):
