@@ -341,6 +341,7 @@ def run_ours(a, cfg, world, rank, local):
             line["cpu_baseline"] = cpu_baseline_sample(cfg, k, img)
         if world == 1 and not a.no_secondary and cfg.name == "cfg2":
             line["secondary"] = secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks)
+            line["secondary_cfg5"] = batch_cfg5(ctx, torch, dev, stream, flush, n_images=16, steps=2, warmup=1)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -370,6 +371,38 @@ def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
             "loop_phases_us": phases,
             "roofline": _roofline(dom, stage_ms[dom], cfg.pixels, int(rep.n_unique), int(rep.iterations), 256, peaks,
                                   int(rep.dist_evals))}
+
+
+def batch_cfg5(ctx, torch, dev, stream, flush, n_images=16, steps=2, warmup=1, lanes_list=(1, 4)):
+    """Config 5: independent 1024x1024 GMM-256 images (seeds 1000+i), K=256,
+    device-resident, `lanes` images in flight on this GPU (cqb_quantize_batch).
+    Aggregate Mpixel/s from CUDA events on the caller's stream (the batch call
+    joins its lane streams back into it)."""
+    from paper_1011_0093_b200 import api
+
+    cfg = CONFIGS["cfg5"]
+    imgs = [torch.from_numpy(cfg.image(i).reshape(-1)).to(dev) for i in range(n_images)]
+    term = api.Termination.convergent(EPSILON, HARD_CAP)
+    out = {"workload": f"cfg5: {n_images} x {cfg.width}x{cfg.height} GMM-256 images (seeds 1000+i), K=256, "
+                       f"convergent(eps={EPSILON}, cap={HARD_CAP})", "unit": "Mpixel/s"}
+    ctx.check(ctx.lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
+    with torch.cuda.stream(stream):
+        for lanes in lanes_list:
+            for _ in range(warmup):
+                api.quantize_batch_device(imgs, 256, term, INIT_SEED, lanes=lanes)
+            tot = 0.0
+            for _ in range(steps):
+                flush()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                _, reps = api.quantize_batch_device(imgs, 256, term, INIT_SEED, lanes=lanes)
+                e1.record(stream)
+                e1.synchronize()
+                tot += e0.elapsed_time(e1)
+            out[f"lanes{lanes}"] = {"value": cfg.pixels * n_images * steps / (tot * 1e-3) / 1e6,
+                                    "ms_per_batch": tot / steps,
+                                    "iterations": [r.iterations for r in reps[:8]]}
+    return out
 
 
 def _loop_phases(tl, iters):

@@ -143,6 +143,19 @@ int cqb_quantize_device(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, i
 /* Waits for the last enqueued quantize on this context and copies its results. */
 int cqb_fetch_results(cqb_ctx* ctx, double* centers_out, double* sse_history, int hist_cap, cqb_report* report);
 
+/* Config 5: n_images independent device-resident images,
+ * each the generate_palette + map_pixels + mse of cqb_quantize_device, with
+ * `lanes` images in flight on this GPU (0 = default 4). Each lane owns a
+ * stream, a device arena and a 1/lanes slice of the SMs for its persistent
+ * WSM kernel. Lanes wait for work already enqueued on the context's stream.
+ * The call returns when every image is done.
+ * d_rgb[i]: image i (u8x3, n_pixels[i] pixels). d_index_out / d_rgb_out:
+ * arrays of n_images device pointers, or NULL; individual entries may be NULL.
+ * centers_out: n_images x k x 3 doubles. reports: n_images entries. */
+int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, const uint64_t* n_pixels, int k,
+                       const cqb_termination* term, uint64_t seed, uint8_t* const* d_index_out,
+                       uint8_t* const* d_rgb_out, int lanes, double* centers_out, cqb_report* reports);
+
 /* ---- post-processing ---------------------------------------------------
  * Replaces map_pixels(img, palette) (image_ops.hpp:18-51): nearest ROUNDED
  * palette entry, lowest index on ties. centers: k x 3 doubles, k in [1,256];

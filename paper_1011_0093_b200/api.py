@@ -257,6 +257,39 @@ def quantize(img: np.ndarray, k: int, term: Termination | None = None, seed: int
     return QuantizeOutcome(centers.reshape(-1, 3)[:k].copy(), r, idx, out)
 
 
+def quantize_batch_device(images, k: int, term: Termination | None = None, seed: int = 1, lanes: int = 4,
+                          index_out=None, mapped_out=None, device: int = 0):
+    """Config 5: quantize independent DEVICE-resident images (CUDA tensors
+    of u8x3 pixels, or (device_pointer, n_pixels) pairs) with ``lanes``
+    images in flight on one GPU (cqb_quantize_batch). ``index_out`` /
+    ``mapped_out``: optional lists of device tensors (16-B aligned).
+    Returns (palettes [n, k, 3] float64, [RunReport])."""
+    n = len(images)
+    term = term or Termination.convergent()
+    ctx = context(device)
+
+    def ptr(x):
+        return int(x[0]) if isinstance(x, tuple) else int(x.data_ptr())
+
+    def npx(x):
+        return int(x[1]) if isinstance(x, tuple) else int(x.numel()) // 3
+
+    ptrs = (C.c_void_p * max(n, 1))(*[ptr(x) for x in images])
+    pix = np.array([npx(x) for x in images] or [0], np.uint64)
+    outs = []
+    for lst in (index_out, mapped_out):
+        outs.append(None if lst is None else (C.c_void_p * max(n, 1))(*[None if o is None else int(o.data_ptr())
+                                                                          for o in lst]))
+    centers = np.zeros(max(n, 1) * 3 * max(k, 1))
+    reps = (N.Report * max(n, 1))()
+    t = term.native()
+    ctx.check(ctx.lib.cqb_quantize_batch(ctx.h, n, ptrs, _p(pix, _u64p), k, C.byref(t), seed, outs[0], outs[1],
+                                         lanes, _p(centers, _f64p), reps))
+    name = "wsm-c" if term.mode == "convergent" else "wsm"
+    return (centers[: n * 3 * k].reshape(n, k, 3).copy(),
+            [_report_from(reps[i], name, np.zeros(0)) for i in range(n)])
+
+
 def generate_palette(img: np.ndarray, mp: MethodParams, k: int, seed: int, device: int = 0) -> QuantizeOutcome:
     """methods.hpp:107-197 — the WSM / WSM-C branch only (the comparator
     quantizers are outside this framework's scope)."""

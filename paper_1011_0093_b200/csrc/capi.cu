@@ -32,6 +32,13 @@ struct Staging {  // pinned host mirror of the per-call results
 
 struct cqb_ctx {
   int device = 0;
+  std::vector<cqb_ctx*> lanes;  // cqb_quantize_batch: images in flight (config 5)
+  cudaEvent_t join_ev = nullptr;  // cqb_quantize_batch: lanes wait for the caller's stream
+  cudaEvent_t lane_done = nullptr;  // as a lane: end of its batch work
+  cudaEvent_t join_ev_out() {
+    if (!lane_done) cudaEventCreateWithFlags(&lane_done, cudaEventDisableTiming);
+    return lane_done;
+  }
   int num_sms = 0;
   int loop_blocks_max = 0;
   int grid_limit = 0;
@@ -102,6 +109,7 @@ struct cqb_ctx {
   int debug_flags = 0;  // diagnostics only (see LoopParams::debug_flags)
   cudaEvent_t pev[8] = {};  // stage boundaries when profiling
   int last_k = 0;
+  uint64_t last_P = 0;  // pixels of the last enqueued quantize (MSE denominator)
   int last_hist_cap = 0;
   int launches = 0;
   std::string err;
@@ -413,6 +421,7 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   CK(cudaEventRecord(ctx->ev[2], ctx->stream));
   TRY(stage_results(ctx, k, term_iters(term)));
   ctx->last_k = k;
+  ctx->last_P = P;
   ctx->last_hist_cap = term_iters(term);
   return CQB_OK;
 }
@@ -507,6 +516,9 @@ int cqb_destroy(cqb_ctx* ctx) {
   for (auto& e : ctx->pev)
     if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  for (cqb_ctx* l : ctx->lanes) cqb_destroy(l);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  if (ctx->lane_done) cudaEventDestroy(ctx->lane_done);
   delete ctx;
   return CQB_OK;
 }
@@ -728,7 +740,70 @@ int cqb_fetch_results(cqb_ctx* ctx, double* centers_out, double* sse_history, in
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
   CK(cudaStreamSynchronize(ctx->stream));
   TRY(check_status(ctx));
-  fill_report(ctx, ctx->last_k, ctx->draws_seed, 0, centers_out, sse_history, hist_cap, report);
+  fill_report(ctx, ctx->last_k, ctx->draws_seed, ctx->last_P, centers_out, sse_history, hist_cap, report);
+  return CQB_OK;
+}
+
+namespace {
+int lane_fail(cqb_ctx* ctx, cqb_ctx* lane, int rc) {
+  return fail(ctx, rc, "batch lane: %s", lane->err.c_str());
+}
+}  // namespace
+
+int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, const uint64_t* n_pixels, int k,
+                       const cqb_termination* term, uint64_t seed, uint8_t* const* d_index_out,
+                       uint8_t* const* d_rgb_out, int lanes, double* centers_out, cqb_report* reports) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (n_images < 0 || (n_images > 0 && (!d_rgb || !n_pixels || !centers_out || !reports)))
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize_batch: null argument");
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  if (lanes <= 0) lanes = 4;
+  lanes = std::max(1, std::min({lanes, n_images, 16}));
+  CK(cudaSetDevice(ctx->device));
+  const int per_lane = std::max(2, loop_grid(ctx) / lanes);
+  while ((int)ctx->lanes.size() < lanes) {
+    cqb_ctx* l = nullptr;
+    const int rc = cqb_create(ctx->device, &l);
+    if (rc != CQB_OK) return fail(ctx, rc, "quantize_batch: lane creation failed");
+    ctx->lanes.push_back(l);
+  }
+  // lanes start after the work already enqueued on the caller's stream
+  if (!ctx->join_ev) CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ctx->join_ev, ctx->stream));
+  for (int l = 0; l < lanes; ++l) {
+    ctx->lanes[l]->grid_limit = per_lane;
+    CK(cudaStreamWaitEvent(ctx->lanes[l]->stream, ctx->join_ev, 0));
+  }
+  std::vector<int> pending(lanes, -1);
+  auto finish = [&](int l) -> int {
+    const int i = pending[l];
+    if (i < 0) return CQB_OK;
+    pending[l] = -1;
+    cqb_ctx* lane = ctx->lanes[l];
+    double* c = centers_out + (size_t)i * 3 * k;
+    int rc = cqb_fetch_results(lane, c, nullptr, 0, &reports[i]);
+    if (rc != CQB_OK && lane->h_stage->status == ST_DRAWS_EXHAUSTED)  // rare: rerun with the retry loop
+      rc = cqb_quantize_device(lane, d_rgb[i], n_pixels[i], k, term, seed, d_index_out ? d_index_out[i] : nullptr,
+                               d_rgb_out ? d_rgb_out[i] : nullptr, 1, c, nullptr, 0, &reports[i]);
+    return rc == CQB_OK ? CQB_OK : lane_fail(ctx, lane, rc);
+  };
+  for (int i = 0; i < n_images; ++i) {
+    const int l = i % lanes;
+    TRY(finish(l));
+    cqb_ctx* lane = ctx->lanes[l];
+    const int rc = cqb_quantize_device(lane, d_rgb[i], n_pixels[i], k, term, seed,
+                                       d_index_out ? d_index_out[i] : nullptr, d_rgb_out ? d_rgb_out[i] : nullptr, 0,
+                                       nullptr, nullptr, 0, nullptr);
+    if (rc != CQB_OK) return lane_fail(ctx, lane, rc);
+    pending[l] = i;
+  }
+  for (int l = 0; l < lanes; ++l) {
+    TRY(finish(l));
+    // order later work on the caller's stream after every lane
+    CK(cudaEventRecord(ctx->lanes[l]->join_ev_out(), ctx->lanes[l]->stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->lanes[l]->join_ev_out(), 0));
+  }
   return CQB_OK;
 }
 

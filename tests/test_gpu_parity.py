@@ -272,6 +272,33 @@ def test_quantize_end_to_end(case, k, images, port):
     assert q.report.mse == port.mse(img, q.mapped)
 
 
+def test_quantize_batch_lanes(port):
+    """Config 5 path: several images in flight (cqb_quantize_batch). Each
+    image's palette, iterations, dist_evals, MSE, index map and mapped raster
+    equal the single-image call and the oracle."""
+    import torch
+
+    imgs = [gmm_image(128, 64, 24, 300 + i) for i in range(7)]  # P = 8192: bit-exact centers
+    dev = [torch.from_numpy(im.reshape(-1)).cuda() for im in imgs]
+    idx = [torch.empty(im.shape[0] * im.shape[1], dtype=torch.uint8, device="cuda") for im in imgs]
+    out = [torch.empty(im.size, dtype=torch.uint8, device="cuda") for im in imgs]
+    term = api.Termination.convergent(1e-4, 100)
+    for lanes in (3, 4):
+        pal, reps = api.quantize_batch_device(dev, 16, term, seed=1, lanes=lanes, index_out=idx, mapped_out=out)
+        for i, im in enumerate(imgs):
+            q = api.quantize(im, 16, term, seed=1)
+            np.testing.assert_array_equal(pal[i], q.palette)
+            assert reps[i].iterations == q.report.iterations
+            assert reps[i].dist_evals == q.report.dist_evals
+            assert reps[i].mse == q.report.mse
+            np.testing.assert_array_equal(idx[i].cpu().numpy(), q.index_map.reshape(-1))
+            np.testing.assert_array_equal(out[i].cpu().numpy(), q.mapped.reshape(-1))
+    h = port.build_histogram(imgs[5])
+    o = port.run_wsm(h.keys, h.counts, 8192, 16, mode=1, eps=1e-4, cap=100, seed=1)
+    np.testing.assert_array_equal(pal[5], o.centers)
+    assert reps[5].iterations == o.iterations and reps[5].dist_evals == o.dist_evals
+
+
 def test_generate_palette_api(images):
     img = images["gmm96x64"]
     a = api.generate_palette(img, api.MethodParams("wsm-c"), 16, 1)
