@@ -214,7 +214,6 @@ def measure_device(lib, ctx, torch, d_img, P, k, steps, warmup, stream, flush, p
             evs[i][0].record(stream)
             one(0)
             evs[i][1].record(stream)
-            launches += 7
             if profile:
                 ms = (C.c_float * 7)()
                 ctx.check(lib.cqb_stage_times(ctx.h, ms, 7))
@@ -226,6 +225,7 @@ def measure_device(lib, ctx, torch, d_img, P, k, steps, warmup, stream, flush, p
         times.append(a.elapsed_time(b))
     ctx.check(lib.cqb_fetch_results(ctx.h, cent.ctypes.data_as(C.POINTER(C.c_double)),
                                     hist.ctypes.data_as(C.POINTER(C.c_double)), HARD_CAP, C.byref(rep)))
+    launches = steps * int(rep.gpu_launches)  # kernels of the library per quantize (counted by the C ABI)
     return times, stage, rep, cent.reshape(k, 3).copy(), launches
 
 

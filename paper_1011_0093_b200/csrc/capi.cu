@@ -60,6 +60,8 @@ struct cqb_ctx {
   uint32_t* d_keys = nullptr;
   uint32_t* d_counts = nullptr;
   uint32_t* d_first = nullptr;
+  uint32_t* d_bitmap = nullptr;  // P-bit first-occurrence bitmap (+ pad)
+  uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
   uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
   uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
   uint32_t* d_mkeys = nullptr;    // Morton-ordered samples (K2b)
@@ -165,6 +167,8 @@ int ensure_pixels(cqb_ctx* ctx, size_t P) {
   TRY(grow(ctx, &ctx->d_img2, 3 * cap));
   TRY(grow(ctx, &ctx->d_index, cap));
   TRY(grow(ctx, &ctx->d_rgb, 3 * cap));
+  TRY(grow(ctx, &ctx->d_bitmap, cap / 32 + 64));
+  TRY(grow(ctx, &ctx->d_bpre, cap / 32 + 64));
   ctx->cap_px = cap;
   const size_t tiles = (P + TILE_PX - 1) / TILE_PX + 1;
   if (tiles > ctx->cap_tiles) {
@@ -260,27 +264,58 @@ int reset_state(cqb_ctx* ctx) {
   return CQB_OK;
 }
 
-// K1 + K2 on ctx->stream over a device raster (16-B aligned).
-int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P) {
-  const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
-  const uint32_t ntiles = (uint32_t)((P + TILE_PX - 1) / TILE_PX);
-  CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
-  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-  k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins);
-  CKL();
-  k_hist_compact<<<ntiles, HIST_THREADS, 0, ctx->stream>>>(
-      d_img, P, ctx->bins, ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->tile_state,
-      reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles), ctx->d_n, ntiles);
+// K2b: Morton-order samples from the bin table (also zeroes it). With
+// `bitmap`, the bins hold ~first pixel index (K1) and K2b emits first indices
+// + sets the first-occurrence bitmap; without, they hold ranks
+// (k_bins_scatter).
+int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
+  CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_BIN_TILES + 1), ctx->stream));
+  k_bins_compact<<<N_BIN_TILES, BC_THREADS, 0, ctx->stream>>>(
+      ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
+      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_BIN_TILES), ctx->d_n, bitmap);
   CKL();
   return CQB_OK;
 }
 
-// K2b: Morton-order samples from the bin table (also zeroes it).
-int enqueue_morton(cqb_ctx* ctx) {
-  CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_BIN_TILES + 1), ctx->stream));
-  k_bins_compact<<<N_BIN_TILES, BC_THREADS, 0, ctx->stream>>>(
-      ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
-      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_BIN_TILES), ctx->d_n);
+// The whole unique-color reduction on ctx->stream over a device raster
+// (16-B aligned), build_histogram (histogram.hpp:65-99):
+//   K1   k_hist_count        2^24 Morton bins {count, ~first pixel}
+//   K2b  k_bins_compact      Morton-order samples {key, count, first} (bins re-zeroed)
+//                            + first-occurrence bitmap over the P pixels
+//   K2c  k_bitmap_scan       per-word set-bit prefix
+//   K2d  k_rank_from_bitmap  first-occurrence rank of every sample (and, for
+//                            the build_histogram API, the histogram in
+//                            first-occurrence order)
+// Everything after K1 is N'-proportional; no pass re-reads the pixels.
+int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamps = false,
+                      bool rank_order = false) {
+  const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  const uint32_t n_words = (uint32_t)((P + 31) / 32);
+  const uint32_t ntiles = (n_words + BS_WORDS - 1) / BS_WORDS;
+  CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
+  CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
+  if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
+  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+  k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins);
+  CKL();
+  if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
+  TRY(enqueue_morton(ctx, ctx->d_bitmap));
+  k_bitmap_scan<<<ntiles, BS_THREADS, 0, ctx->stream>>>(ctx->d_bitmap, n_words, ctx->d_bpre, ctx->tile_state,
+                                                        reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles));
+  CKL();
+  k_rank_from_bitmap<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+      ctx->d_bitmap, ctx->d_bpre, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n,
+      rank_order ? ctx->d_keys : nullptr, ctx->d_counts, ctx->d_first);
+  CKL();
+  return CQB_OK;
+}
+
+// init_centers (kmeans.hpp:53-74) when only the Morton-order samples exist:
+// the chosen ranks, then a gather by rank.
+int enqueue_init_morton(cqb_ctx* ctx, int k, int ndraws) {
+  k_init_centers<<<1, KMAX, 0, ctx->stream>>>(nullptr, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
+  CKL();
+  k_gather_chosen<<<ctx->num_sms * 4, KMAX, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mrank, ctx->d_n, k, ctx->st);
   CKL();
   return CQB_OK;
 }
@@ -380,25 +415,10 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   TRY(upload_draws(ctx, seed, ndraws));
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   PROF(0);
-  {
-    const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
-    const uint32_t ntiles = (uint32_t)((P + TILE_PX - 1) / TILE_PX);
-    CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
-    TRY(reset_state(ctx));
-    PROF(1);
-    const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins);
-    CKL();
-    PROF(2);
-    k_hist_compact<<<ntiles, HIST_THREADS, 0, ctx->stream>>>(
-        d_img, P, ctx->bins, ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->tile_state,
-        reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles), ctx->d_n, ntiles);
-    CKL();
-    TRY(enqueue_morton(ctx));
-  }
+  TRY(reset_state(ctx));
+  TRY(enqueue_histogram(ctx, d_img, P, true));
   PROF(3);
-  k_init_centers<<<1, KMAX, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
-  CKL();
+  TRY(enqueue_init_morton(ctx, k, ndraws));
   PROF(4);
   TRY(launch_loop(ctx, k, term, 1, P, nullptr, 0));
   CK(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -499,7 +519,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
-                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
@@ -595,14 +615,12 @@ int cqb_build_histogram(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, uin
   TRY(ensure_pixels(ctx, n_pixels));
   TRY(ensure_samples(ctx, n_pixels));
   CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
-  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
+  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels, false, true));
   if (weights) {
     k_hist_weights<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_counts, ctx->d_n, n_pixels, ctx->d_weights);
     CKL();
   }
   CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-  k_bins_reset<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, ctx->bins);
-  CKL();
   CK(cudaStreamSynchronize(ctx->stream));
   const uint64_t nu = ctx->h_scalar[0];
   if (n_unique) *n_unique = nu;
@@ -843,7 +861,6 @@ int cqb_map_pixels(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, const do
   CK(cudaMemcpyAsync(ctx->d_centers_in, centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(&ctx->st->mse_err, 0, sizeof(unsigned long long), ctx->stream));
   TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
-  TRY(enqueue_morton(ctx));
   k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->d_centers_in, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
   CKL();
   k_map_unique<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, nullptr, ctx->d_n, k,
@@ -901,9 +918,7 @@ int cqb_shard_prepare(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k
   TRY(upload_draws(ctx, seed, ndraws));
   TRY(reset_state(ctx));
   TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
-  TRY(enqueue_morton(ctx));
-  k_init_centers<<<1, KMAX, 0, ctx->stream>>>(ctx->d_keys, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
-  CKL();
+  TRY(enqueue_init_morton(ctx, k, ndraws));
   CK(cudaMemsetAsync(ctx->d_labels, 0, n_pixels, ctx->stream));
   CK(cudaMemcpyAsync(&ctx->h_stage->status, &ctx->st->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));

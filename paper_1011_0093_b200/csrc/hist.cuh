@@ -1,17 +1,18 @@
-// K1 + K2: unique-color data reduction (reference: build_histogram,
-// histogram.hpp:65-99) — 2^24-bin direct histogram with first-occurrence
-// tracking, then pixel-space compaction that emits the unique colors in
-// FIRST-OCCURRENCE order (histogram.hpp:77-92) with no sort.
+// Unique-color data reduction (reference: build_histogram,
+// histogram.hpp:65-99): a 2^24-bin direct histogram with first-occurrence
+// tracking, then bin-space compaction into Morton order, then the
+// first-occurrence ranks (histogram.hpp:77-92) from a bitmap of
+// first pixel indices. No sort, and only K1 reads the pixels.
 //
 // Bin table layout (HBM, 128 MiB, kept all-zero between calls), indexed by
 // the MORTON code of the color (morton_of_key):
 //   bins[m].x = pixel count          (atomicAdd, RED.ADD)
-//   bins[m].y = ~first pixel index   (atomicMax of the complement = min index);
-//               K2 then overwrites it with the first-occurrence RANK.
+//   bins[m].y = ~first pixel index   (atomicMax of the complement = min index)
 // Both words share one 8-B slot, so each pixel touches one 32-B sector.
 // K2b scans the table in bin (= Morton) order, emits the samples in that
-// spatially coherent order with their rank, and zeroes every touched bin, so
-// no 128 MiB clear is ever paid per call.
+// spatially coherent order with their first pixel, sets that pixel's bit in
+// a P-bit bitmap, and zeroes every touched bin, so no 128 MiB clear is ever
+// paid per call. K2c/K2d turn first pixels into ranks (set bits below).
 #pragma once
 #include "common.cuh"
 
@@ -59,131 +60,6 @@ __device__ __forceinline__ unsigned long long lb_load(const unsigned long long* 
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// K2: pixel-space compaction. Pixel i is the representative of its color iff
-// bins[key_i] records i as the first occurrence; the exclusive prefix count of
-// representatives in scan order IS the first-occurrence rank. Single pass,
-// decoupled look-back over tiles of TILE_PX pixels (tile ids from a ticket so
-// predecessors are always resident). Emits keys[], counts[] (and optionally
-// the first pixel index) in first-occurrence order; the last tile writes N'.
-__global__ void __launch_bounds__(HIST_THREADS) k_hist_compact(
-    const uint8_t* __restrict__ img, uint64_t P, uint2* __restrict__ bins, uint32_t* __restrict__ out_keys,
-    uint32_t* __restrict__ out_counts, uint32_t* __restrict__ out_first, unsigned long long* tile_state,
-    unsigned int* ticket, unsigned long long* n_unique, uint32_t ntiles) {
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_warp[HIST_THREADS / 32];
-  __shared__ uint32_t s_prefix;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t c = (uint64_t)tile * HIST_THREADS + tid;
-
-  uint32_t keys[PX_PER_THREAD];
-  uint32_t cnts[PX_PER_THREAD];
-  uint32_t mask = 0;
-  const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
-  const uint32_t base = (uint32_t)(c * PX_PER_THREAD);
-  if (c < nchunk) {
-    const int n = load_chunk_keys(img, P, c, keys);
-#pragma unroll
-    for (int s = 0; s < PX_PER_THREAD; ++s) {
-      cnts[s] = 0;
-      if (s < n) {
-        const uint2 b = bins[morton_of_key(keys[s])];
-        if (b.y == ~(base + s)) {
-          mask |= 1u << s;
-          cnts[s] = b.x;
-        }
-      }
-    }
-  }
-  const uint32_t cnt = __popc(mask);
-
-  // block exclusive scan of per-thread representative counts
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_warp[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t w = lane < HIST_THREADS / 32 ? s_warp[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += v;
-    }
-    if (lane < HIST_THREADS / 32) s_warp[lane] = w;  // inclusive warp totals
-  }
-  __syncthreads();
-  const uint32_t block_total = s_warp[HIST_THREADS / 32 - 1];
-  const uint32_t excl = incl - cnt + (wid ? s_warp[wid - 1] : 0);
-
-  // decoupled look-back (warp 0)
-  if (wid == 0) {
-    uint32_t prefix = 0;
-    if (tile == 0) {
-      if (lane == 0) {
-        __threadfence();
-        atomicExch(tile_state, LB_PRE | block_total);
-      }
-    } else {
-      if (lane == 0) atomicExch(tile_state + tile, LB_AGG | block_total);
-      int j = (int)tile - 1;
-      while (true) {
-        const int idx = j - lane;
-        unsigned long long st = idx >= 0 ? lb_load(tile_state + idx) : (LB_PRE | 0ull);
-        while (__any_sync(0xffffffffu, (st >> 32) == 0)) {
-          if ((st >> 32) == 0) st = lb_load(tile_state + idx);
-        }
-        const uint32_t pmask = __ballot_sync(0xffffffffu, (st >> 32) == 2);
-        const uint32_t val = (uint32_t)st;
-        if (pmask) {
-          const int first_p = __ffs(pmask) - 1;
-          prefix += warp_sum(lane <= first_p ? val : 0u);
-          break;
-        }
-        prefix += warp_sum(val);
-        j -= 32;
-      }
-      if (lane == 0) {
-        __threadfence();
-        atomicExch(tile_state + tile, LB_PRE | (prefix + block_total));
-      }
-    }
-    if (lane == 0) s_prefix = prefix;
-  }
-  __syncthreads();
-  __threadfence();
-  uint32_t rank = s_prefix + excl;
-  if (mask) {
-#pragma unroll
-    for (int s = 0; s < PX_PER_THREAD; ++s) {
-      if (mask & (1u << s)) {
-        out_keys[rank] = keys[s];
-        out_counts[rank] = cnts[s];
-        if (out_first) out_first[rank] = base + s;
-        // record the rank in the bin for the Morton-order pass (K2b). Other
-        // pixels of this color compare ~their index against it, which can
-        // never equal a rank < 2^24 while P < 2^32 - 2^24.
-        bins[morton_of_key(keys[s])].y = rank;
-        ++rank;
-      }
-    }
-  }
-  if (tile == ntiles - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
-}
-
-// Returns the touched bins to zero (used when no map pass follows).
-__global__ void k_bins_reset(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ n_unique,
-                             uint2* __restrict__ bins) {
-  const uint64_t n = *n_unique;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    bins[morton_of_key(keys[i])] = make_uint2(0u, 0u);
-}
-
 // Fill the bin table from a first-occurrence-ordered histogram (host
 // histogram APIs): bins[morton(key_r)] = {count_r, r}.
 __global__ void k_bins_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ counts,
@@ -203,11 +79,19 @@ constexpr int BC_STEPS = 8;
 constexpr int BIN_TILE = (BC_THREADS / 32) * 64 * BC_STEPS;
 constexpr int N_BIN_TILES = (1 << 24) / BIN_TILE;
 
+//
+// Two modes for the second bin word y:
+//  * bitmap == nullptr: y is the sample's rank (k_bins_scatter of a host
+//    histogram); it is emitted as m_rank.
+//  * bitmap != nullptr: y = ~first pixel index (straight from K1); the first
+//    index is emitted in m_rank (k_rank_from_bitmap turns it into the rank)
+//    and its bit is set in the P-bit first-occurrence bitmap.
 __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__ bins, uint32_t* __restrict__ m_keys,
                                                              uint32_t* __restrict__ m_counts,
                                                              uint32_t* __restrict__ m_rank,
                                                              unsigned long long* tile_state, unsigned int* ticket,
-                                                             unsigned long long* n_unique) {
+                                                             unsigned long long* n_unique,
+                                                             uint32_t* __restrict__ bitmap) {
   constexpr int NW = BC_THREADS / 32;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
@@ -284,18 +168,141 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
       if (f0) {
         m_keys[pos] = key_of_morton(bin);
         m_counts[pos] = v[q].x;
-        m_rank[pos] = v[q].y;
+        const uint32_t y = bitmap ? ~v[q].y : v[q].y;
+        m_rank[pos] = y;
+        if (bitmap) atomicOr(&bitmap[y >> 5], 1u << (y & 31));
         ++pos;
       }
       if (f1) {
         m_keys[pos] = key_of_morton(bin + 1);
         m_counts[pos] = v[q].z;
-        m_rank[pos] = v[q].w;
+        const uint32_t y = bitmap ? ~v[q].w : v[q].w;
+        m_rank[pos] = y;
+        if (bitmap) atomicOr(&bitmap[y >> 5], 1u << (y & 31));
       }
       reinterpret_cast<uint4*>(bins + wbase + q * 64)[lane] = make_uint4(0u, 0u, 0u, 0u);
     }
   }
   if (tile == N_BIN_TILES - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
+}
+
+// First-occurrence ranks from the P-bit bitmap of first pixel indices
+// (histogram.hpp:77-92 orders the unique colors by first occurrence): the
+// rank of a color whose first pixel is f is the number of set bits below f.
+// BS_WORDS words per tile; pre[w] = set bits in words < w (decoupled
+// look-back over tiles).
+constexpr int BS_THREADS = 256;
+constexpr int BS_PER_THREAD = 16;
+constexpr int BS_WORDS = BS_THREADS * BS_PER_THREAD;
+
+__global__ void __launch_bounds__(BS_THREADS) k_bitmap_scan(const uint32_t* __restrict__ bitmap, uint32_t n_words,
+                                                            uint32_t* __restrict__ pre,
+                                                            unsigned long long* tile_state, unsigned int* ticket) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[BS_THREADS / 32];
+  __shared__ uint32_t s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t w0 = tile * BS_WORDS + tid * BS_PER_THREAD;
+  uint32_t c[BS_PER_THREAD];
+  uint32_t cnt = 0;
+  if (w0 + BS_PER_THREAD <= n_words) {
+#pragma unroll
+    for (int q = 0; q < BS_PER_THREAD; q += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(bitmap + w0 + q);
+      c[q] = __popc(v.x);
+      c[q + 1] = __popc(v.y);
+      c[q + 2] = __popc(v.z);
+      c[q + 3] = __popc(v.w);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < BS_PER_THREAD; ++q) c[q] = w0 + q < n_words ? __popc(bitmap[w0 + q]) : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < BS_PER_THREAD; ++q) cnt += c[q];
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < BS_THREADS / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    if (lane < BS_THREADS / 32) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t block_total = s_warp[BS_THREADS / 32 - 1];
+  const uint32_t excl = incl - cnt + (wid ? s_warp[wid - 1] : 0);
+  if (wid == 0) {
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) atomicExch(tile_state, LB_PRE | block_total);
+    } else {
+      if (lane == 0) atomicExch(tile_state + tile, LB_AGG | block_total);
+      int j = (int)tile - 1;
+      while (true) {
+        const int idx = j - lane;
+        unsigned long long st = idx >= 0 ? lb_load(tile_state + idx) : (LB_PRE | 0ull);
+        while (__any_sync(0xffffffffu, (st >> 32) == 0)) {
+          if ((st >> 32) == 0) st = lb_load(tile_state + idx);
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+        const uint32_t val = (uint32_t)st;
+        if (pmask) {
+          const int first_p = __ffs(pmask) - 1;
+          prefix += warp_sum(lane <= first_p ? val : 0u);
+          break;
+        }
+        prefix += warp_sum(val);
+        j -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(tile_state + tile, LB_PRE | (prefix + block_total));
+      }
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + excl;
+#pragma unroll
+  for (int q = 0; q < BS_PER_THREAD; ++q) {
+    if (w0 + q < n_words) pre[w0 + q] = run;
+    run += c[q];
+  }
+}
+
+// Morton sample s (first pixel f in m_rank[s]) -> its first-occurrence rank
+// r, in place. With r_keys (the build_histogram API only), also scatters the
+// histogram into first-occurrence order (keys, counts, first index): random
+// 4-B writes, ~0.7 ms at N' = 10.6M, so the quantize path skips it.
+__global__ void k_rank_from_bitmap(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ pre,
+                                   const uint32_t* __restrict__ m_keys, const uint32_t* __restrict__ m_counts,
+                                   uint32_t* __restrict__ m_rank, const unsigned long long* __restrict__ n_unique,
+                                   uint32_t* __restrict__ r_keys, uint32_t* __restrict__ r_counts,
+                                   uint32_t* __restrict__ r_first) {
+  const uint32_t n = (uint32_t)*n_unique;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const uint32_t f = m_rank[s];
+    const uint32_t w = f >> 5;
+    const uint32_t r = pre[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
+    m_rank[s] = r;
+    if (r_keys) {
+      r_keys[r] = m_keys[s];
+      r_counts[r] = m_counts[s];
+      r_first[r] = f;
+    }
+  }
 }
 
 // weights[i] = double(count) * (1.0 / double(P))  — histogram.hpp:94-97.

@@ -94,11 +94,15 @@ __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restric
                                                       const unsigned long long* __restrict__ n_ptr, int k,
                                                       const unsigned long long* __restrict__ draws, int ndraws,
                                                       WsmState* st) {
-  constexpr int HS = 2 * KMAX;  // hash slots for positions >= k
+  // Partial Fisher-Yates (kmeans.hpp:58-68): for i < k, j_i = i + bounded_rand(N'-i),
+  // swap(idx[i], idx[j_i]), center i = colors[idx[i]]. Position i is final
+  // after step i (later steps swap positions >= i+1), so with
+  //   W(i)  = idx[i] just before step i = W(m) for the last m < i with j_m = i, else i
+  //   c_i   = idx[j_i] just before step i = W(m) for the last m < i with j_m = j_i, else j_i
+  // every chosen index follows from the j's in parallel (pointer jumping for W).
   __shared__ unsigned long long jv[KMAX];
-  __shared__ uint32_t lowv[KMAX];
-  __shared__ unsigned long long hpos[HS];
-  __shared__ uint32_t hval[HS];
+  __shared__ int ptr[2][KMAX];
+  __shared__ uint32_t wv[2][KMAX];
   __shared__ int s_rejected;
   const int tid = threadIdx.x;
   const unsigned long long n = *n_ptr;
@@ -107,10 +111,8 @@ __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restric
     return;
   }
   if (tid == 0) s_rejected = 0;
-  for (int h = tid; h < HS; h += blockDim.x) hpos[h] = ~0ull;
   __syncthreads();
   for (int i = tid; i < k; i += blockDim.x) {
-    lowv[i] = (uint32_t)i;
     const unsigned long long bound = n - (unsigned long long)i;
     const unsigned long long limit = ~0ull - (~0ull % bound);
     const unsigned long long r = i < ndraws ? draws[i] : ~0ull;
@@ -118,52 +120,99 @@ __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restric
     jv[i] = (unsigned long long)i + r % bound;
   }
   __syncthreads();
-  if (tid == 0) {
-    if (s_rejected) {  // exact sequential draw consumption
-      int di = 0;
-      for (int i = 0; i < k; ++i) {
-        const unsigned long long bound = n - (unsigned long long)i;
-        const unsigned long long limit = ~0ull - (~0ull % bound);
-        unsigned long long r;
-        do {
-          if (di >= ndraws) {
-            st->status = ST_DRAWS_EXHAUSTED;
-            s_rejected = 2;
-            break;
-          }
-          r = draws[di++];
-        } while (r >= limit);
-        if (s_rejected == 2) break;
-        jv[i] = (unsigned long long)i + r % bound;
-      }
-    }
-    if (s_rejected != 2) {
-      for (int i = 0; i < k; ++i) {
-        const unsigned long long j = jv[i];
-        const uint32_t vi = lowv[i];
-        uint32_t vj;
-        if (j < (unsigned long long)k) {
-          vj = lowv[j];
-          lowv[j] = vi;
-        } else {
-          int h = (int)((j * 0x9E3779B97F4A7C15ull) >> 55);  // 9 bits -> [0, 512)
-          while (hpos[h] != ~0ull && hpos[h] != j) h = (h + 1) & (HS - 1);
-          vj = hpos[h] == j ? hval[h] : (uint32_t)j;
-          hpos[h] = j;
-          hval[h] = vi;
+  if (tid == 0 && s_rejected) {  // exact sequential draw consumption (bounded_rand rejection, :43-49)
+    int di = 0;
+    for (int i = 0; i < k; ++i) {
+      const unsigned long long bound = n - (unsigned long long)i;
+      const unsigned long long limit = ~0ull - (~0ull % bound);
+      unsigned long long r;
+      do {
+        if (di >= ndraws) {
+          st->status = ST_DRAWS_EXHAUSTED;
+          s_rejected = 2;
+          break;
         }
-        lowv[i] = vj;
-      }
+        r = draws[di++];
+      } while (r >= limit);
+      if (s_rejected == 2) break;
+      jv[i] = (unsigned long long)i + r % bound;
     }
   }
   __syncthreads();
   if (s_rejected == 2) return;
-  for (int i = tid; i < k; i += blockDim.x) {
-    const uint32_t key = keys[lowv[i]];
-    st->C[0][3 * i + 0] = (double)key_r(key);
-    st->C[0][3 * i + 1] = (double)key_g(key);
-    st->C[0][3 * i + 2] = (double)key_b(key);
-    st->chosen[i] = lowv[i];
+  const int i = tid;
+  int pred = -1, same = -1;
+  if (i < k) {
+    const unsigned long long ji = jv[i];
+    for (int m = 0; m < i; ++m) {
+      const unsigned long long jm = jv[m];
+      if (jm == (unsigned long long)i) pred = m;
+      if (jm == ji) same = m;
+    }
+    ptr[0][i] = pred;
+    wv[0][i] = (uint32_t)i;
+  }
+  __syncthreads();
+  int cur = 0;
+  for (int round = 0; round < 9; ++round) {  // 2^9 > KMAX: every chain resolved
+    if (i < k) {
+      const int p = ptr[cur][i];
+      ptr[cur ^ 1][i] = p < 0 ? -1 : ptr[cur][p];
+      wv[cur ^ 1][i] = p < 0 ? wv[cur][i] : wv[cur][p];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  if (i < k) {
+    const uint32_t chosen = same < 0 ? (uint32_t)jv[i] : wv[cur][same];
+    if (keys) {  // first-occurrence-ordered keys available: gather here
+      const uint32_t key = keys[chosen];
+      st->C[0][3 * i + 0] = (double)key_r(key);
+      st->C[0][3 * i + 1] = (double)key_g(key);
+      st->C[0][3 * i + 2] = (double)key_b(key);
+    }
+    st->chosen[i] = chosen;
+  }
+}
+
+// Initial centers from the Morton-order samples: center i = the sample whose
+// first-occurrence rank is chosen[i] (kmeans.hpp:67-68). Each block sorts the
+// K chosen ranks in shared memory; every sample binary-searches its rank.
+__global__ void __launch_bounds__(KMAX) k_gather_chosen(const uint32_t* __restrict__ m_keys,
+                                                         const uint32_t* __restrict__ m_rank,
+                                                         const unsigned long long* __restrict__ n_ptr, int k,
+                                                         WsmState* st) {
+  __shared__ uint32_t sr[KMAX];
+  __shared__ uint32_t si[KMAX];
+  __shared__ uint32_t sc[KMAX];
+  if (st->status != ST_OK) return;
+  const int tid = threadIdx.x;
+  const uint32_t r0 = tid < k ? st->chosen[tid] : 0u;
+  if (tid < k) sc[tid] = r0;
+  __syncthreads();
+  if (tid < k) {
+    int pos = 0;
+    for (int u = 0; u < k; ++u) pos += sc[u] < r0;  // chosen ranks are distinct
+    sr[pos] = r0;
+    si[pos] = (uint32_t)tid;
+  }
+  __syncthreads();
+  const uint32_t n = (uint32_t)*n_ptr;
+  for (uint32_t s = blockIdx.x * blockDim.x + tid; s < n; s += gridDim.x * blockDim.x) {
+    const uint32_t r = m_rank[s];
+    int lo = 0, hi = k;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sr[mid] < r) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < k && sr[lo] == r) {
+      const int i = (int)si[lo];
+      const uint32_t key = m_keys[s];
+      st->C[0][3 * i + 0] = (double)key_r(key);
+      st->C[0][3 * i + 1] = (double)key_g(key);
+      st->C[0][3 * i + 2] = (double)key_b(key);
+    }
   }
 }
 
