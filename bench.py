@@ -332,6 +332,7 @@ def run_ours(a, cfg, world, rank, local):
                     "path": "cqb_quantize (C ABI) with pinned host buffers, wall clock"},
             "gpu_launches": launches,
             "roofline": roof,
+            "hbm_stages": _hbm_stages(stage_ms, P, n_unique, peaks),
             "stages_ms": {kk: round(v, 5) for kk, v in stage_ms.items()},
             "loop_phases_us": phases,
             "dist_evals": int(rep.dist_evals),
@@ -368,6 +369,7 @@ def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
     return {"workload": _workload(cfg, 256), "value": cfg.pixels / (ms * 1e-3) / 1e6, "unit": "Mpixel/s",
             "ms_per_step": ms, "n_unique": int(rep.n_unique), "iterations": int(rep.iterations),
             "dist_evals": int(rep.dist_evals), "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "hbm_stages": _hbm_stages(stage_ms, cfg.pixels, int(rep.n_unique), peaks),
             "loop_phases_us": phases,
             "roofline": _roofline(dom, stage_ms[dom], cfg.pixels, int(rep.n_unique), int(rep.iterations), 256, peaks,
                                   int(rep.dist_evals))}
@@ -451,9 +453,9 @@ def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
     elif stage in ("hist_count",):
         traffic_alg = 3.0 * P
         note = "3P bytes (u8x3 raster read); bin atomics not counted"
-    elif stage == "hist_compact":
-        traffic_alg = 3.0 * P + 8.0 * n_unique
-        note = "3P raster read + 8 B per unique color written"
+    elif stage == "bins_compact":
+        traffic_alg = 8.0 * (1 << 24) + 12.0 * n_unique
+        note = "128 MiB bin-table scan + 12 B per unique color written (Morton samples)"
     elif stage == "map_pixels":
         traffic_alg = 7.0 * P
         note = "3P read + P index + 3P RGB written"
@@ -462,8 +464,35 @@ def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
         note = "8 B per unique color"
     achieved = traffic_alg / (ms * 1e-3) / 1e9
     return {"kernel": stage, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel_ms": ms, "algorithmic_bytes": traffic_alg,
-            "peak_source": peaks["source"], "note": note}
+            "frac": achieved / peaks["hbm_gbs"], "traffic": _ncu_traffic(stage, P), "kernel_ms": ms,
+            "algorithmic_bytes": traffic_alg, "peak_source": peaks["source"], "note": note}
+
+
+def _ncu_traffic(stage, P):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    ncu --set full capture (profiles/*/traffic.json), for the same image size."""
+    for rnd in ("r02", "r01"):
+        f = os.path.join(ROOT, "profiles", rnd, "traffic.json")
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+        except Exception:
+            continue
+        e = d.get(stage, {}).get(str(P))
+        if e is not None:
+            return e
+    return None
+
+
+def _hbm_stages(stage_ms, P, n_unique, peaks):
+    """Achieved algorithmic GB/s of the HBM-bound stages."""
+    out = {}
+    for st in ("hist_count", "bins_compact", "map_pixels"):
+        if st in stage_ms and stage_ms[st] > 0:
+            r = _roofline(st, stage_ms[st], P, n_unique, 1, 0, peaks, 0)
+            out[st] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 4),
+                       "algorithmic_bytes": r["algorithmic_bytes"], "ms": round(stage_ms[st], 4)}
+    return out
 
 
 def main():

@@ -30,7 +30,8 @@ EXPORTS = (
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
     "cqb_shard_reseed_candidate", "cqb_set_debug",
 )
-STAGES = ("reset", "hist_count", "hist_compact", "init", "wsm_loop", "map_unique", "map_pixels")
+# cqb_stage_times intervals: memsets | K1 | K2b | init + bitmap scan + rank (+ gather) | loop | map tables+unique | map pixels
+STAGES = ("reset", "hist_count", "bins_compact", "init_rank", "wsm_loop", "map_unique", "map_pixels")
 
 
 class Termination(C.Structure):

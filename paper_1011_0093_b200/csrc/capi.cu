@@ -288,7 +288,7 @@ int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
 //                            first-occurrence order)
 // Everything after K1 is N'-proportional; no pass re-reads the pixels.
 int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamps = false,
-                      bool rank_order = false) {
+                      bool rank_order = false, int init_k = 0, int ndraws = 0) {
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
   const uint32_t n_words = (uint32_t)((P + 31) / 32);
   const uint32_t ntiles = (n_words + BS_WORDS - 1) / BS_WORDS;
@@ -296,26 +296,27 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
   const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-  k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins);
-  CKL();
+  const int passes = P >= (4u << 20) && !(ctx->debug_flags & 8) ? 4 : 1;
+  for (int q = 0; q < passes; ++q) {
+    const uint32_t span = (1u << 24) / passes;
+    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins, q * span,
+                                                                     q + 1 == passes ? (1u << 24) : (q + 1) * span);
+    CKL();
+  }
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
   TRY(enqueue_morton(ctx, ctx->d_bitmap));
+  if (init_k > 0) {  // init_centers needs only N': its chosen ranks, gathered by the rank pass
+    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
+    k_init_centers<<<1, KMAX, 0, ctx->stream>>>(nullptr, ctx->d_n, init_k, ctx->d_draws, ndraws, ctx->st);
+    CKL();
+  }
   k_bitmap_scan<<<ntiles, BS_THREADS, 0, ctx->stream>>>(ctx->d_bitmap, n_words, ctx->d_bpre, ctx->tile_state,
                                                         reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles));
   CKL();
   k_rank_from_bitmap<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
       ctx->d_bitmap, ctx->d_bpre, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n,
-      rank_order ? ctx->d_keys : nullptr, ctx->d_counts, ctx->d_first);
-  CKL();
-  return CQB_OK;
-}
-
-// init_centers (kmeans.hpp:53-74) when only the Morton-order samples exist:
-// the chosen ranks, then a gather by rank.
-int enqueue_init_morton(cqb_ctx* ctx, int k, int ndraws) {
-  k_init_centers<<<1, KMAX, 0, ctx->stream>>>(nullptr, ctx->d_n, k, ctx->d_draws, ndraws, ctx->st);
-  CKL();
-  k_gather_chosen<<<ctx->num_sms * 4, KMAX, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mrank, ctx->d_n, k, ctx->st);
+      rank_order ? ctx->d_keys : nullptr, ctx->d_counts, ctx->d_first, init_k > 0 ? ctx->st->chosen : nullptr,
+      &ctx->st->status, init_k, ctx->st->C[0]);
   CKL();
   return CQB_OK;
 }
@@ -416,9 +417,7 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   PROF(0);
   TRY(reset_state(ctx));
-  TRY(enqueue_histogram(ctx, d_img, P, true));
-  PROF(3);
-  TRY(enqueue_init_morton(ctx, k, ndraws));
+  TRY(enqueue_histogram(ctx, d_img, P, true, false, k, ndraws));  // records PROF(1..3)
   PROF(4);
   TRY(launch_loop(ctx, k, term, 1, P, nullptr, 0));
   CK(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -917,8 +916,7 @@ int cqb_shard_prepare(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k
   const int ndraws = k + 64;
   TRY(upload_draws(ctx, seed, ndraws));
   TRY(reset_state(ctx));
-  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels));
-  TRY(enqueue_init_morton(ctx, k, ndraws));
+  TRY(enqueue_histogram(ctx, ctx->d_img, n_pixels, false, false, k, ndraws));
   CK(cudaMemsetAsync(ctx->d_labels, 0, n_pixels, ctx->stream));
   CK(cudaMemcpyAsync(&ctx->h_stage->status, &ctx->st->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));

@@ -18,16 +18,22 @@
 
 namespace cqb {
 
-__device__ __forceinline__ void bin_add(uint2* __restrict__ bins, uint32_t key, uint32_t run, uint32_t first) {
-  uint32_t* b = reinterpret_cast<uint32_t*>(bins + morton_of_key(key));
+__device__ __forceinline__ void bin_add(uint2* __restrict__ bins, uint32_t key, uint32_t run, uint32_t first,
+                                        uint32_t mlo, uint32_t mhi) {
+  const uint32_t m = morton_of_key(key);
+  if (m - mlo >= mhi - mlo) return;  // outside this pass's slice of the table
+  uint32_t* b = reinterpret_cast<uint32_t*>(bins + m);
   atomicAdd(b, run);
   atomicMax(b + 1, ~first);
 }
 
 // K1: one thread per 16-pixel chunk (grid-stride). Consecutive equal colors
 // within a thread's chunk are run-length aggregated into one atomic pair.
+// Only bins in the Morton slice [mlo, mhi) are updated: large images run K1
+// once per half of the 128 MiB table, so each pass's atomics stay in the
+// 126 MB L2 instead of re-fetching sectors from HBM.
 __global__ void __launch_bounds__(HIST_THREADS) k_hist_count(const uint8_t* __restrict__ img, uint64_t P,
-                                                              uint2* __restrict__ bins) {
+                                                              uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi) {
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
   for (uint64_t c = (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x; c < nchunk;
        c += (uint64_t)gridDim.x * HIST_THREADS) {
@@ -41,14 +47,14 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist_count(const uint8_t* __re
         if (keys[s] == cur) {
           ++run;
         } else {
-          bin_add(bins, cur, run, start);
+          bin_add(bins, cur, run, start, mlo, mhi);
           cur = keys[s];
           run = 1;
           start = base + s;
         }
       }
     }
-    bin_add(bins, cur, run, start);
+    bin_add(bins, cur, run, start, mlo, mhi);
   }
 }
 
@@ -286,22 +292,69 @@ __global__ void __launch_bounds__(BS_THREADS) k_bitmap_scan(const uint32_t* __re
 // r, in place. With r_keys (the build_histogram API only), also scatters the
 // histogram into first-occurrence order (keys, counts, first index): random
 // 4-B writes, ~0.7 ms at N' = 10.6M, so the quantize path skips it.
-__global__ void k_rank_from_bitmap(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ pre,
-                                   const uint32_t* __restrict__ m_keys, const uint32_t* __restrict__ m_counts,
-                                   uint32_t* __restrict__ m_rank, const unsigned long long* __restrict__ n_unique,
-                                   uint32_t* __restrict__ r_keys, uint32_t* __restrict__ r_counts,
-                                   uint32_t* __restrict__ r_first) {
-  const uint32_t n = (uint32_t)*n_unique;
+//
+// With `chosen` (k sorted-able distinct ranks from k_init_centers, which ran
+// after K2b), the sample whose rank is chosen[i] also becomes initial center
+// i (kmeans.hpp:67-68): init's gather fused into this pass.
+template <typename Gather>
+__device__ __forceinline__ void rank_pass(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ pre,
+                                          const uint32_t* __restrict__ m_keys, const uint32_t* __restrict__ m_counts,
+                                          uint32_t* __restrict__ m_rank, uint32_t n, uint32_t* __restrict__ r_keys,
+                                          uint32_t* __restrict__ r_counts, uint32_t* __restrict__ r_first,
+                                          Gather gather) {
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
     const uint32_t f = m_rank[s];
     const uint32_t w = f >> 5;
     const uint32_t r = pre[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
     m_rank[s] = r;
+    gather(r, s);
     if (r_keys) {
       r_keys[r] = m_keys[s];
       r_counts[r] = m_counts[s];
       r_first[r] = f;
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rank_from_bitmap(
+    const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ pre, const uint32_t* __restrict__ m_keys,
+    const uint32_t* __restrict__ m_counts, uint32_t* __restrict__ m_rank, const unsigned long long* __restrict__ n_unique,
+    uint32_t* __restrict__ r_keys, uint32_t* __restrict__ r_counts, uint32_t* __restrict__ r_first,
+    const uint32_t* __restrict__ chosen, const int* __restrict__ status, int k, double* __restrict__ centers) {
+  __shared__ uint32_t sr[256];
+  __shared__ uint32_t si[256];
+  __shared__ uint32_t sc[256];
+  const uint32_t n = (uint32_t)*n_unique;
+  const bool do_gather = chosen && *status == 0 && k <= 256;
+  if (do_gather) {  // sort the chosen ranks (distinct) by rank counting
+    const int tid = threadIdx.x;
+    const uint32_t r0 = tid < k ? chosen[tid] : 0u;
+    if (tid < k) sc[tid] = r0;
+    __syncthreads();
+    if (tid < k) {
+      int pos = 0;
+      for (int u = 0; u < k; ++u) pos += sc[u] < r0;
+      sr[pos] = r0;
+      si[pos] = (uint32_t)tid;
+    }
+    __syncthreads();
+    rank_pass(bitmap, pre, m_keys, m_counts, m_rank, n, r_keys, r_counts, r_first, [&](uint32_t r, uint32_t s) {
+      int lo = 0, hi = k;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sr[mid] < r) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < k && sr[lo] == r) {
+        const int i = (int)si[lo];
+        const uint32_t key = m_keys[s];
+        centers[3 * i + 0] = (double)key_r(key);
+        centers[3 * i + 1] = (double)key_g(key);
+        centers[3 * i + 2] = (double)key_b(key);
+      }
+    });
+  } else {
+    rank_pass(bitmap, pre, m_keys, m_counts, m_rank, n, r_keys, r_counts, r_first, [](uint32_t, uint32_t) {});
   }
 }
 
