@@ -1,7 +1,7 @@
 # Build of the B200-native WSM path (sm_100a only) and its CPU checkers.
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v $(EXTRA)
 CSRC      := paper_1011_0093_b200/csrc
 LIB       := paper_1011_0093_b200/lib/libcolorq_b200.so
 SHIM_TEST := build/shim_test

@@ -6,7 +6,10 @@
 namespace cqb {
 
 constexpr int KMAX = 256;            // palette sizes handled on device (u8 labels)
-constexpr int LOOP_THREADS = 1024;   // persistent WSM loop block size (one block per SM)
+#ifndef CQB_LOOP_THREADS
+#define CQB_LOOP_THREADS 1024
+#endif
+constexpr int LOOP_THREADS = CQB_LOOP_THREADS;  // persistent WSM loop block size (one block per SM)
 constexpr int MAXBLK = 1024;         // max persistent blocks (reseed candidate slots)
 constexpr int HIST_THREADS = 256;    // histogram / compaction block size
 constexpr int PX_PER_THREAD = 16;    // 16 pixels = 48 B = 3 x 16-B vector loads

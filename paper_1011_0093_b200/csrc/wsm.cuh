@@ -278,7 +278,7 @@ struct RowStage {
 // only the distances are rewritten. Otherwise (early iterations) the row is
 // re-sorted by rank counting, half of the block per row, u-range split in 2.
 __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental) {
-  static_assert(LOOP_THREADS == 4 * KMAX, "tables layout assumes 1024 threads");
+  static_assert(LOOP_THREADS == 4 * KMAX || LOOP_THREADS == 2 * KMAX, "tables layout: 512 or 1024 threads");
   const int tid = threadIdx.x;
   const int r = tid >> 9;                     // which row of the pair
   const int t = tid & (KMAX - 1);             // element / position
@@ -356,7 +356,12 @@ __device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, boo
   if (first < 0) return;
   for (int p = first; p < k; p += 2 * stride) {
     const int q = p + stride;
-    tables_rows2(S, st, p, q < k ? q : -1, k, incremental);
+    if (LOOP_THREADS == 4 * KMAX) {
+      tables_rows2(S, st, p, q < k ? q : -1, k, incremental);
+    } else {  // 512 threads: one row per pass
+      tables_rows2(S, st, p, -1, k, incremental);
+      if (q < k) tables_rows2(S, st, q, -1, k, incremental);
+    }
   }
 }
 
