@@ -61,6 +61,7 @@ struct cqb_ctx {
   uint32_t* d_counts = nullptr;
   uint32_t* d_first = nullptr;
   uint32_t* d_bitmap = nullptr;  // P-bit first-occurrence bitmap (+ pad)
+  uint32_t* d_occ = nullptr;     // 2^24-bit bin occupancy map (small images; all-zero between calls)
   uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
   uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
   uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
@@ -287,6 +288,10 @@ int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
 //                            the build_histogram API, the histogram in
 //                            first-occurrence order)
 // Everything after K1 is N'-proportional; no pass re-reads the pixels.
+// Images below this size compact the bin table through K1's occupancy map
+// (their tables are sparse: cfg2's 0.37M colors touch 2% of the bins).
+constexpr uint64_t OCC_MAX_PIXELS = 2u << 20;
+
 int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamps = false,
                       bool rank_order = false, int init_k = 0, int ndraws = 0) {
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
@@ -296,15 +301,27 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
   const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-  const int passes = P >= (4u << 20) && !(ctx->debug_flags & 8) ? 4 : 1;
+  // Sparse tables (small images) are compacted through the occupancy map;
+  // dense ones by scanning all 128 MiB (k_bins_compact), whose K1 runs in
+  // 4 Morton slices so each pass's atomics stay in L2.
+  const bool sparse = P < OCC_MAX_PIXELS && !(ctx->debug_flags & 16);
+  const int passes = P >= (4u << 20) ? 4 : 1;
   for (int q = 0; q < passes; ++q) {
     const uint32_t span = (1u << 24) / passes;
-    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins, q * span,
-                                                                     q + 1 == passes ? (1u << 24) : (q + 1) * span);
+    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(
+        d_img, P, ctx->bins, q * span, q + 1 == passes ? (1u << 24) : (q + 1) * span, sparse ? ctx->d_occ : nullptr);
     CKL();
   }
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
-  TRY(enqueue_morton(ctx, ctx->d_bitmap));
+  if (sparse) {
+    CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_OCC_TILES + 1), ctx->stream));
+    k_occ_compact<<<N_OCC_TILES, OC_THREADS, 0, ctx->stream>>>(
+        ctx->d_occ, ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
+        reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_OCC_TILES), ctx->d_n, ctx->d_bitmap);
+    CKL();
+  } else {
+    TRY(enqueue_morton(ctx, ctx->d_bitmap));
+  }
   if (init_k > 0) {  // init_centers needs only N': its chosen ranks, gathered by the rank pass
     if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
     k_init_centers<<<1, KMAX, 0, ctx->stream>>>(nullptr, ctx->d_n, init_k, ctx->d_draws, ndraws, ctx->st);
@@ -475,6 +492,8 @@ int cqb_create(int device, cqb_ctx** out) {
     ctx->stream = ctx->own_stream;
     CK(cudaMalloc(&ctx->bins, sizeof(uint2) << 24));
     CK(cudaMemset(ctx->bins, 0, sizeof(uint2) << 24));
+    CK(cudaMalloc(&ctx->d_occ, sizeof(uint32_t) << 19));
+    CK(cudaMemset(ctx->d_occ, 0, sizeof(uint32_t) << 19));
     CK(cudaMalloc(&ctx->lut, (size_t)1 << 24));
     CK(cudaMalloc(&ctx->bin_tile_state, sizeof(unsigned long long) * (N_BIN_TILES + 1)));
     CK(cudaMalloc(&ctx->st, sizeof(WsmState)));
@@ -518,7 +537,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
-                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,

@@ -19,12 +19,13 @@
 namespace cqb {
 
 __device__ __forceinline__ void bin_add(uint2* __restrict__ bins, uint32_t key, uint32_t run, uint32_t first,
-                                        uint32_t mlo, uint32_t mhi) {
+                                        uint32_t mlo, uint32_t mhi, uint32_t* __restrict__ occ) {
   const uint32_t m = morton_of_key(key);
   if (m - mlo >= mhi - mlo) return;  // outside this pass's slice of the table
   uint32_t* b = reinterpret_cast<uint32_t*>(bins + m);
   atomicAdd(b, run);
   atomicMax(b + 1, ~first);
+  if (occ) atomicOr(&occ[m >> 5], 1u << (m & 31));
 }
 
 // K1: one thread per 16-pixel chunk (grid-stride). Consecutive equal colors
@@ -32,8 +33,11 @@ __device__ __forceinline__ void bin_add(uint2* __restrict__ bins, uint32_t key, 
 // Only bins in the Morton slice [mlo, mhi) are updated: large images run K1
 // once per half of the 128 MiB table, so each pass's atomics stay in the
 // 126 MB L2 instead of re-fetching sectors from HBM.
+// With `occ`, K1 also marks every touched bin in a 2^24-bit occupancy map
+// (2 MiB), so small images can compact the table without scanning 128 MiB.
 __global__ void __launch_bounds__(HIST_THREADS) k_hist_count(const uint8_t* __restrict__ img, uint64_t P,
-                                                              uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi) {
+                                                              uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi,
+                                                              uint32_t* __restrict__ occ) {
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
   for (uint64_t c = (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x; c < nchunk;
        c += (uint64_t)gridDim.x * HIST_THREADS) {
@@ -47,14 +51,14 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist_count(const uint8_t* __re
         if (keys[s] == cur) {
           ++run;
         } else {
-          bin_add(bins, cur, run, start, mlo, mhi);
+          bin_add(bins, cur, run, start, mlo, mhi, occ);
           cur = keys[s];
           run = 1;
           start = base + s;
         }
       }
     }
-    bin_add(bins, cur, run, start, mlo, mhi);
+    bin_add(bins, cur, run, start, mlo, mhi, occ);
   }
 }
 
@@ -190,6 +194,124 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
     }
   }
   if (tile == N_BIN_TILES - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
+}
+
+// K2b for sparse tables (small images): the same Morton-order samples as
+// k_bins_compact, found through K1's occupancy map. A thread owns 4 map words
+// (128 bins); set bits are counted, scanned (decoupled look-back over tiles),
+// and each touched bin is read, emitted {key, count, first pixel}, zeroed,
+// and its first pixel marked in the first-occurrence bitmap. The occupancy
+// words are cleared for the next call. Reads 2 MiB + the touched bins only.
+constexpr int OC_THREADS = 256;
+constexpr int OC_WORDS = OC_THREADS * 4;            // occupancy words per tile
+constexpr int N_OCC_TILES = (1 << 19) / OC_WORDS;   // 2^24 bins / 32 per word
+
+__global__ void __launch_bounds__(OC_THREADS) k_occ_compact(uint32_t* __restrict__ occ, uint2* __restrict__ bins,
+                                                            uint32_t* __restrict__ m_keys,
+                                                            uint32_t* __restrict__ m_counts,
+                                                            uint32_t* __restrict__ m_first,
+                                                            unsigned long long* tile_state, unsigned int* ticket,
+                                                            unsigned long long* n_unique,
+                                                            uint32_t* __restrict__ bitmap) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[OC_THREADS / 32];
+  __shared__ uint32_t s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t w0 = tile * OC_WORDS + tid * 4;
+  uint4 wv = *reinterpret_cast<const uint4*>(occ + w0);
+  const uint32_t cnt = __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < OC_THREADS / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    if (lane < OC_THREADS / 32) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t block_total = s_warp[OC_THREADS / 32 - 1];
+  const uint32_t excl = incl - cnt + (wid ? s_warp[wid - 1] : 0);
+  if (wid == 0) {
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) atomicExch(tile_state, LB_PRE | block_total);
+    } else {
+      if (lane == 0) atomicExch(tile_state + tile, LB_AGG | block_total);
+      int j = (int)tile - 1;
+      while (true) {
+        const int idx = j - lane;
+        unsigned long long st = idx >= 0 ? lb_load(tile_state + idx) : (LB_PRE | 0ull);
+        while (__any_sync(0xffffffffu, (st >> 32) == 0)) {
+          if ((st >> 32) == 0) st = lb_load(tile_state + idx);
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+        const uint32_t val = (uint32_t)st;
+        if (pmask) {
+          const int first_p = __ffs(pmask) - 1;
+          prefix += warp_sum(lane <= first_p ? val : 0u);
+          break;
+        }
+        prefix += warp_sum(val);
+        j -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(tile_state + tile, LB_PRE | (prefix + block_total));
+      }
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  if (cnt) {
+    uint32_t pos = s_prefix + excl;
+    uint32_t words[4] = {wv.x, wv.y, wv.z, wv.w};
+    int q = 0;
+    // batches of up to 8 touched bins: their loads are issued together
+    // (memory-level parallelism for the scattered bin reads)
+    while (true) {
+      uint32_t ms[8];
+      int nb = 0;
+      while (nb < 8 && q < 4) {
+        if (words[q] == 0u) {
+          ++q;
+          continue;
+        }
+        ms[nb++] = (w0 + q) * 32 + (__ffs(words[q]) - 1);
+        words[q] &= words[q] - 1u;
+      }
+      if (nb == 0) break;
+      uint2 v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e < nb) v[e] = bins[ms[e]];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e < nb) {
+          const uint32_t f = ~v[e].y;
+          m_keys[pos] = key_of_morton(ms[e]);
+          m_counts[pos] = v[e].x;
+          m_first[pos] = f;
+          asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bitmap + (f >> 5)), "r"(1u << (f & 31)) : "memory");
+          bins[ms[e]] = make_uint2(0u, 0u);
+          ++pos;
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(occ + w0) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (tile == N_OCC_TILES - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
 }
 
 // First-occurrence ranks from the P-bit bitmap of first pixel indices
