@@ -132,6 +132,16 @@ int cqb_wsm_iterate(cqb_ctx* ctx, const uint32_t* keys, const uint32_t* counts, 
 int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
                  uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
                  uint8_t* rgb_out, cqb_report* report);
+/* cqb_quantize plus error_out (nullable): error_image(image, mapped)
+ * (image_ops.hpp:55-71), fused into the map pass. This is the CLI quantize
+ * command's outputs (tools/colorq.cpp:96-109) in one call. */
+int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                    uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
+                    uint8_t* rgb_out, uint8_t* error_out, cqb_report* report);
+/* error_image(original, quantized) (image_ops.hpp:55-71): per channel
+ * 255 - min(255, 4|o - q|). Host buffers of n_pixels u8x3 pixels. */
+int cqb_error_image(cqb_ctx* ctx, const uint8_t* original, const uint8_t* quantized, uint64_t n_pixels,
+                    uint8_t* out);
 
 /* Same pipeline with DEVICE-resident image and outputs (all pointers are
  * device pointers on the context's device; outputs nullable). Enqueued on

@@ -117,6 +117,12 @@ class Oracle:
             f("quantize_many").argtypes = [C.POINTER(_u8p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_double, C.c_int, C.c_uint64, C.c_int, _f64p, _i32p]
             f("quantize_many").restype = C.c_double
+            f("write_ppm").argtypes = [_u8p, C.c_int, C.c_int, _u8p, C.c_int64]
+            f("write_ppm").restype = C.c_int64
+            f("read_ppm").argtypes = [_u8p, C.c_int64, _u8p, C.c_int64, _i32p, _i32p]
+            f("palette_text").argtypes = [_f64p, C.c_int, C.c_char_p, C.c_int64]
+            f("palette_text").restype = C.c_int64
+            f("error_image").argtypes = [_u8p, _u8p, C.c_uint64, _u8p]
         f("mse").argtypes = [_u8p, _u8p, C.c_uint64]
         f("mse").restype = C.c_double
 
@@ -260,6 +266,48 @@ class Oracle:
             raise ValueError("quantize failed")
         return dict(centers=C_out.reshape(k, 3), iterations=int(it[0]), sse=float(sse[0]), dist_evals=int(ev[0]),
                     mapped=out, mse=float(m[0]), palette_ms=float(pms[0]), map_ms=float(mms[0]))
+
+    # -- §8(f) f1: file formats (reference only) ---------------------------
+    PPM_KINDS = {0: "ok", 1: "BadMagic", 2: "BadHeader", 3: "BadMaxval", 4: "Truncated", -1: "runtime"}
+
+    def write_ppm(self, img: np.ndarray) -> bytes:
+        assert self.kind == "reference"
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape[:2]
+        n = self._f("write_ppm")(_p(img, _u8p), w, h, None, 0)
+        out = np.zeros(n, np.uint8)
+        self._f("write_ppm")(_p(img, _u8p), w, h, _p(out, _u8p), n)
+        return out.tobytes()
+
+    def read_ppm(self, data: bytes):
+        """(kind, image or None) with kind in PPM_KINDS."""
+        assert self.kind == "reference"
+        buf = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+        w = np.zeros(1, np.int32)
+        h = np.zeros(1, np.int32)
+        cap = max(len(data) * 3, 16)
+        out = np.zeros(cap, np.uint8)
+        rc = self._f("read_ppm")(_p(buf, _u8p), len(data), _p(out, _u8p), cap, _p(w, _i32p), _p(h, _i32p))
+        if rc != 0:
+            return self.PPM_KINDS[rc], None
+        return "ok", out[: 3 * int(w[0]) * int(h[0])].reshape(int(h[0]), int(w[0]), 3).copy()
+
+    def palette_text(self, centers: np.ndarray) -> str:
+        assert self.kind == "reference"
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        k = c.size // 3
+        n = self._f("palette_text")(_p(c, _f64p), k, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        self._f("palette_text")(_p(c, _f64p), k, buf, n)
+        return buf.raw[:n].decode()
+
+    def error_image(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        assert self.kind == "reference"
+        a = np.ascontiguousarray(a, np.uint8)
+        b = np.ascontiguousarray(b, np.uint8)
+        out = np.zeros_like(a)
+        self._f("error_image")(_p(a, _u8p), _p(b, _u8p), a.size // 3, _p(out, _u8p))
+        return out
 
     def quantize_many(self, imgs, k: int, nthreads: int, mode: int = 1, max_iters: int = 10, eps: float = 1e-4,
                       cap: int = 100, seed: int = 1):

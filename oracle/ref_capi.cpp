@@ -23,6 +23,8 @@
 #include "colorq/kmeans.hpp"
 #include "colorq/methods.hpp"
 #include "colorq/metrics.hpp"
+#include "colorq/palette.hpp"
+#include "colorq/ppm.hpp"
 
 using namespace colorq;
 
@@ -245,6 +247,45 @@ double ref_quantize_many(const std::uint8_t* const* imgs, int count, int w, int 
   for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
   for (auto& t : pool) t.join();
   return watch.elapsed_ms();
+}
+
+// ---- §8(f) row f1: file formats and error_image (ppm.hpp, palette.hpp,
+// image_ops.hpp:55-71), for the CLI parity tests.
+
+// write_ppm bytes of a w x h image; returns the byte count (or the needed
+// capacity when cap is too small).
+std::int64_t ref_write_ppm(const std::uint8_t* rgb, int w, int h, std::uint8_t* out, std::int64_t cap) {
+  const std::vector<unsigned char> b = write_ppm(make_image(rgb, std::uint64_t(w), std::uint64_t(h)));
+  if (std::int64_t(b.size()) <= cap) std::memcpy(out, b.data(), b.size());
+  return std::int64_t(b.size());
+}
+
+// read_ppm: 0 ok (w, h, pixels into rgb_out if it fits), 1..4 = PpmError kind
+// + 1 (BadMagic, BadHeader, BadMaxval, Truncated), -1 other error.
+int ref_read_ppm(const std::uint8_t* bytes, std::int64_t n, std::uint8_t* rgb_out, std::int64_t cap, int* w,
+                 int* h) {
+  try {
+    const RgbImage img = read_ppm(std::span<const unsigned char>(bytes, std::size_t(n)));
+    *w = img.width;
+    *h = img.height;
+    if (std::int64_t(img.size()) * 3 <= cap) std::memcpy(rgb_out, img.pixels.data(), img.size() * 3);
+    return 0;
+  } catch (const PpmError& e) {
+    return int(e.kind) + 1;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+std::int64_t ref_palette_text(const double* C, int k, char* out, std::int64_t cap) {
+  const std::string t = palette_to_text(make_palette(C, k));
+  if (std::int64_t(t.size()) <= cap) std::memcpy(out, t.data(), t.size());
+  return std::int64_t(t.size());
+}
+
+void ref_error_image(const std::uint8_t* a, const std::uint8_t* b, std::uint64_t n, std::uint8_t* out) {
+  const RgbImage e = error_image(make_image(a, n, 1), make_image(b, n, 1));
+  std::memcpy(out, e.pixels.data(), 3 * n);
 }
 
 }  // extern "C"

@@ -126,6 +126,7 @@ class QuantizeOutcome:
     report: RunReport
     index_map: np.ndarray | None = None
     mapped: np.ndarray | None = None
+    error: np.ndarray | None = None
 
 
 @dataclass(frozen=True)
@@ -230,9 +231,11 @@ def wsm_iterate(hist: ColorHistogram, centers: np.ndarray, labels: np.ndarray, t
 
 def quantize(img: np.ndarray, k: int, term: Termination | None = None, seed: int = 1, index_map: bool = True,
              mapped: bool = True, device: int = 0, out_index: np.ndarray | None = None,
-             out_mapped: np.ndarray | None = None) -> QuantizeOutcome:
+             out_mapped: np.ndarray | None = None, error: bool = False) -> QuantizeOutcome:
     """Histogram + WSM + map + MSE in one device pass (host buffers).
-    ``out_index`` / ``out_mapped`` may be caller-owned (e.g. pinned) arrays."""
+    ``out_index`` / ``out_mapped`` may be caller-owned (e.g. pinned) arrays.
+    ``error=True`` also returns error_image(img, mapped) (image_ops.hpp:55-71)
+    in ``QuantizeOutcome.error``, fused into the map pass."""
     a = _rgb(img)
     if a.ndim == 3:
         h, w = a.shape[0], a.shape[1]
@@ -249,12 +252,14 @@ def quantize(img: np.ndarray, k: int, term: Termination | None = None, seed: int
         assert idx.flags.c_contiguous and idx.dtype == np.uint8 and idx.size == a.size // 3
     if out is not None:
         assert out.flags.c_contiguous and out.dtype == np.uint8 and out.size == a.size
+    err = np.empty_like(a) if error else None
     rep = N.Report()
     t = term.native()
-    ctx.check(ctx.lib.cqb_quantize(ctx.h, _p(a, _u8p), w, h, k, C.byref(t), seed, _p(centers, _f64p),
-                                   _p(hist_out, _f64p), cap, _p(idx, _u8p), _p(out, _u8p), C.byref(rep)))
+    ctx.check(ctx.lib.cqb_quantize_ex(ctx.h, _p(a, _u8p), w, h, k, C.byref(t), seed, _p(centers, _f64p),
+                                      _p(hist_out, _f64p), cap, _p(idx, _u8p), _p(out, _u8p), _p(err, _u8p),
+                                      C.byref(rep)))
     r = _report_from(rep, "wsm-c" if term.mode == "convergent" else "wsm", hist_out)
-    return QuantizeOutcome(centers.reshape(-1, 3)[:k].copy(), r, idx, out)
+    return QuantizeOutcome(centers.reshape(-1, 3)[:k].copy(), r, idx, out, err)
 
 
 def quantize_batch_device(images, k: int, term: Termination | None = None, seed: int = 1, lanes: int = 4,
@@ -301,6 +306,17 @@ def generate_palette(img: np.ndarray, mp: MethodParams, k: int, seed: int, devic
     q.report.method = mp.id
     q.report.mse = 0.0  # the caller fills mse (methods.hpp:104-106)
     return q
+
+
+def error_image(original: np.ndarray, quantized: np.ndarray, device: int = 0) -> np.ndarray:
+    """image_ops.hpp:55-71: per channel 255 - min(255, 4|o - q|) (device kernel)."""
+    a, b = _rgb(original), _rgb(quantized)
+    if a.shape != b.shape:
+        raise CqbInvalidArgument(N.CQB_ERR_INVALID_ARGUMENT, "error_image: dimension mismatch")
+    out = np.empty_like(a)
+    ctx = context(device)
+    ctx.check(ctx.lib.cqb_error_image(ctx.h, _p(a, _u8p), _p(b, _u8p), a.size // 3, _p(out, _u8p)))
+    return out
 
 
 def map_pixels_indexed(img: np.ndarray, palette: np.ndarray, device: int = 0):

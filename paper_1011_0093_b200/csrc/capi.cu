@@ -61,7 +61,9 @@ struct cqb_ctx {
   uint32_t* d_counts = nullptr;
   uint32_t* d_first = nullptr;
   uint32_t* d_bitmap = nullptr;  // P-bit first-occurrence bitmap (+ pad)
-  uint32_t* d_occ = nullptr;     // 2^24-bit bin occupancy map (small images; all-zero between calls)
+  uint32_t* d_occ = nullptr;
+  uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
+  uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output     // 2^24-bit bin occupancy map (small images; all-zero between calls)
   uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
   uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
   uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
@@ -168,6 +170,7 @@ int ensure_pixels(cqb_ctx* ctx, size_t P) {
   TRY(grow(ctx, &ctx->d_img2, 3 * cap));
   TRY(grow(ctx, &ctx->d_index, cap));
   TRY(grow(ctx, &ctx->d_rgb, 3 * cap));
+  TRY(grow(ctx, &ctx->d_err, 3 * cap));
   TRY(grow(ctx, &ctx->d_bitmap, cap / 32 + 64));
   TRY(grow(ctx, &ctx->d_bpre, cap / 32 + 64));
   ctx->cap_px = cap;
@@ -446,11 +449,12 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
                                             ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey, ctx->lut, &ctx->st->mse_err);
   CKL();
   PROF(6);
-  if (d_index || d_rgb_out) {
+  uint8_t* d_err_out = ctx->err_target;
+  if (d_index || d_rgb_out || d_err_out) {
     const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
     const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
     k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->lut, ctx->d_palkey, k, d_index,
-                                                                   d_rgb_out);
+                                                                   d_rgb_out, d_err_out);
     CKL();
   }
   PROF(7);
@@ -536,7 +540,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   if (!ctx) return CQB_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->tile_state,
+  void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->d_err, ctx->tile_state,
                  ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
@@ -846,6 +850,13 @@ int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, 
 int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
                  uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
                  uint8_t* rgb_out, cqb_report* report) {
+  return cqb_quantize_ex(ctx, rgb, width, height, k, term, seed, centers_out, sse_history, hist_cap, index_out,
+                         rgb_out, nullptr, report);
+}
+
+int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                    uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
+                    uint8_t* rgb_out, uint8_t* error_out, cqb_report* report) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
   if (width <= 0 || height <= 0 || !rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "image dimensions must be positive");
   TRY(check_k(ctx, k));
@@ -855,12 +866,33 @@ int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k,
   TRY(ensure_pixels(ctx, P));
   CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
   cqb_report rep{};
-  TRY(cqb_quantize_device(ctx, ctx->d_img, P, k, term, seed, index_out ? ctx->d_index : nullptr,
-                          rgb_out ? ctx->d_rgb : nullptr, 1, centers_out, sse_history, hist_cap, &rep));
+  ctx->err_target = error_out ? ctx->d_err : nullptr;
+  const int rc = cqb_quantize_device(ctx, ctx->d_img, P, k, term, seed, index_out ? ctx->d_index : nullptr,
+                                     rgb_out ? ctx->d_rgb : nullptr, 1, centers_out, sse_history, hist_cap, &rep);
+  ctx->err_target = nullptr;
+  TRY(rc);
   if (index_out) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
   if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+  if (error_out) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (report) *report = rep;
+  return CQB_OK;
+}
+
+int cqb_error_image(cqb_ctx* ctx, const uint8_t* original, const uint8_t* quantized, uint64_t n_pixels,
+                    uint8_t* out) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (n_pixels == 0) return CQB_OK;
+  if (!original || !quantized || !out) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "error_image: null buffer");
+  CK(cudaSetDevice(ctx->device));
+  ctx->launches = 0;
+  TRY(ensure_pixels(ctx, n_pixels));
+  CK(cudaMemcpyAsync(ctx->d_img, original, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_rgb, quantized, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  k_error_image<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->d_img, ctx->d_rgb, 3 * n_pixels, ctx->d_err);
+  CKL();
+  CK(cudaMemcpyAsync(out, ctx->d_err, 3 * n_pixels, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return CQB_OK;
 }
 
@@ -889,7 +921,7 @@ int cqb_map_pixels(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, const do
   const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
   k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(ctx->d_img, n_pixels, ctx->lut, ctx->d_palkey, k,
                                                                  index_out ? ctx->d_index : nullptr,
-                                                                 rgb_out ? ctx->d_rgb : nullptr);
+                                                                 rgb_out ? ctx->d_rgb : nullptr, nullptr);
   CKL();
   CK(cudaMemcpyAsync(ctx->h_scalar, &ctx->st->mse_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      ctx->stream));

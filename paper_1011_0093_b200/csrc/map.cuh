@@ -112,11 +112,38 @@ __global__ void __launch_bounds__(256) k_map_unique(const uint32_t* __restrict__
 }
 
 // Per pixel: index map (u8) and mapped RGB (u8x3), 16 pixels per thread.
+// Per byte: 255 - min(255, 4 |a - b|) (saturating SIMD adds).
+__device__ __forceinline__ uint32_t err_bytes(uint32_t a, uint32_t b) {
+  const uint32_t d = __vabsdiffu4(a, b);
+  const uint32_t d2 = __vaddus4(d, d);
+  return ~__vaddus4(d2, d2);
+}
+
+// Standalone error_image over two rasters of P pixels (bytes, any alignment).
+__global__ void k_error_image(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, uint64_t nbytes,
+                              uint8_t* __restrict__ out) {
+  const uint64_t n4 = nbytes / 4;
+  const bool al = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) & 3) == 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (al) {
+      reinterpret_cast<uint32_t*>(out)[i] =
+          err_bytes(reinterpret_cast<const uint32_t*>(a)[i], reinterpret_cast<const uint32_t*>(b)[i]);
+    } else {
+      for (int j = 0; j < 4; ++j) out[4 * i + j] = (uint8_t)err_bytes(a[4 * i + j], b[4 * i + j]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < nbytes - 4 * n4) {
+    const uint64_t j = 4 * n4 + threadIdx.x;
+    out[j] = (uint8_t)err_bytes(a[j], b[j]);
+  }
+}
+
 __global__ void __launch_bounds__(HIST_THREADS) k_map_pixels(const uint8_t* __restrict__ img, uint64_t P,
                                                               const uint8_t* __restrict__ lut,
                                                               const uint32_t* __restrict__ pal_key, int k,
                                                               uint8_t* __restrict__ out_index,
-                                                              uint8_t* __restrict__ out_rgb) {
+                                                              uint8_t* __restrict__ out_rgb,
+                                                              uint8_t* __restrict__ out_err) {
   __shared__ uint32_t s_pal[KMAX];  // bytes (r, g, b, 0) in memory order
   for (int t = threadIdx.x; t < k; t += blockDim.x) {
     const uint32_t key = pal_key[t];
@@ -141,7 +168,7 @@ __global__ void __launch_bounds__(HIST_THREADS) k_map_pixels(const uint8_t* __re
         v.w = idx[12] | (idx[13] << 8) | (idx[14] << 16) | (idx[15] << 24);
         *reinterpret_cast<uint4*>(out_index + p0) = v;
       }
-      if (out_rgb) {
+      if (out_rgb || out_err) {
         uint32_t pc[PX_PER_THREAD];
 #pragma unroll
         for (int s = 0; s < PX_PER_THREAD; ++s) pc[s] = s_pal[idx[s]];
@@ -153,19 +180,40 @@ __global__ void __launch_bounds__(HIST_THREADS) k_map_pixels(const uint8_t* __re
           w[3 * g + 1] = (b >> 8) | (cc << 16);
           w[3 * g + 2] = (cc >> 16) | (d << 8);
         }
-        uint4* dst = reinterpret_cast<uint4*>(out_rgb + p0 * 3);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        dst[2] = make_uint4(w[8], w[9], w[10], w[11]);
+        if (out_rgb) {
+          uint4* dst = reinterpret_cast<uint4*>(out_rgb + p0 * 3);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          dst[2] = make_uint4(w[8], w[9], w[10], w[11]);
+        }
+        if (out_err) {  // error_image (image_ops.hpp:55-71): 255 - min(255, 4|o - q|) per byte
+          const uint4* src = reinterpret_cast<const uint4*>(img + p0 * 3);
+          const uint4 a = __ldg(src), b = __ldg(src + 1), d = __ldg(src + 2);
+          const uint32_t o[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+          uint32_t e[12];
+#pragma unroll
+          for (int i = 0; i < 12; ++i) e[i] = err_bytes(o[i], w[i]);
+          uint4* dst = reinterpret_cast<uint4*>(out_err + p0 * 3);
+          dst[0] = make_uint4(e[0], e[1], e[2], e[3]);
+          dst[1] = make_uint4(e[4], e[5], e[6], e[7]);
+          dst[2] = make_uint4(e[8], e[9], e[10], e[11]);
+        }
       }
     } else {
       for (int s = 0; s < n; ++s) {
         if (out_index) out_index[p0 + s] = (uint8_t)idx[s];
+        const uint32_t pc = s_pal[idx[s]];
         if (out_rgb) {
-          const uint32_t pc = s_pal[idx[s]];
           out_rgb[3 * (p0 + s)] = (uint8_t)pc;
           out_rgb[3 * (p0 + s) + 1] = (uint8_t)(pc >> 8);
           out_rgb[3 * (p0 + s) + 2] = (uint8_t)(pc >> 16);
+        }
+        if (out_err) {
+          const uint32_t o = img[3 * (p0 + s)] | (img[3 * (p0 + s) + 1] << 8) | (img[3 * (p0 + s) + 2] << 16);
+          const uint32_t e = err_bytes(o, pc);
+          out_err[3 * (p0 + s)] = (uint8_t)e;
+          out_err[3 * (p0 + s) + 1] = (uint8_t)(e >> 8);
+          out_err[3 * (p0 + s) + 2] = (uint8_t)(e >> 16);
         }
       }
     }

@@ -1,0 +1,86 @@
+"""GPU: the CLI quantize command on the B200 library (build/colorq_b200,
+SURVEY.md §8(f) row f1) against the reference's composition of the same
+command (tools/colorq.cpp:96-112) run through oracle/_ref: byte-identical
+output PPM, palette text, error image and histogram CSV, the same summary
+line (except time), and the reference's exit codes."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, available
+from paper_1011_0093_b200 import api
+from paper_1011_0093_b200.configs import gmm_image
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not available("reference"), reason="oracle/_ref not built")]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "build", "colorq_b200")
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return Oracle("reference")
+
+
+def _fmt_g6(v):
+    return "%.6g" % v
+
+
+def _run(args, timeout=300):
+    return subprocess.run([CLI] + args, capture_output=True, text=True, timeout=timeout)
+
+
+@pytest.mark.parametrize("method,k", [("wsm-c", 16), ("wsm", 32)])
+def test_cli_quantize_byte_identical(method, k, ref, tmp_path):
+    img = gmm_image(128, 64, 24, 77)  # P = 8192 (power of two: bit-exact centers)
+    src = tmp_path / "in.ppm"
+    src.write_bytes(ref.write_ppm(img))
+    out, pal, err, hist = (tmp_path / n for n in ("out.ppm", "pal.txt", "err.ppm", "hist.csv"))
+    r = _run(["quantize", str(src), "-o", str(out), "-m", method, "-k", str(k), "-s", "3", "--palette", str(pal),
+              "--error-image", str(err), "--dump-histogram", str(hist)])
+    assert r.returncode == 0, r.stderr
+    # the reference CLI: MethodParams defaults, Termination::convergent(1e-4) = cap 1000 (kmeans.hpp:34)
+    mode = 1 if method == "wsm-c" else 0
+    q = ref.quantize(img, k, mode=mode, max_iters=10, eps=1e-4, cap=1000, seed=3)
+    assert out.read_bytes() == ref.write_ppm(q["mapped"])
+    assert pal.read_text() == ref.palette_text(q["centers"])
+    assert err.read_bytes() == ref.write_ppm(ref.error_image(img, q["mapped"]))
+    h = ref.build_histogram(img)
+    lines = ["r,g,b,count"] + [f"{(kk >> 16) & 255},{(kk >> 8) & 255},{kk & 255},{c}" for kk, c in
+                               zip(h.keys.tolist(), h.counts.tolist())]
+    assert hist.read_text() == "\n".join(lines) + "\n"
+    fields = dict(f.split("=", 1) for f in r.stdout.split())
+    assert fields["method"] == method and fields["k"] == str(k) and fields["seed"] == "3"
+    assert int(fields["iterations"]) == q["iterations"]
+    assert fields["mse"] == _fmt_g6(q["mse"])
+    assert fields["psnr"] == _fmt_g6(20 * np.log10(255 / np.sqrt(q["mse"])))
+
+
+def test_cli_exit_codes(ref, tmp_path):
+    img = gmm_image(32, 16, 4, 5)
+    good = tmp_path / "g.ppm"
+    good.write_bytes(ref.write_ppm(img))
+    bad = tmp_path / "b.ppm"
+    bad.write_bytes(b"P3 1 1 255\n1 2 3\n")
+    few = tmp_path / "few.ppm"
+    few.write_bytes(ref.write_ppm(np.zeros((4, 4, 3), np.uint8)))  # N' = 1
+    o = str(tmp_path / "o.ppm")
+    assert _run(["quantize", str(tmp_path / "missing.ppm"), "-o", o]).returncode == 2
+    assert _run(["quantize", str(bad), "-o", o]).returncode == 2
+    assert _run(["quantize", str(good), "-o", o, "-m", "nope"]).returncode == 3
+    assert _run(["quantize", str(good), "-o", o, "-m", "mc"]).returncode == 3  # not provided on this path
+    assert _run(["quantize", str(good), "-o", o, "-k", "0"]).returncode == 4
+    assert _run(["quantize", str(few), "-o", o, "-k", "2"]).returncode == 4  # k > N' (kmeans.hpp:55-56)
+    assert _run(["quantize", str(good), "-o", o, "-k", "4"]).returncode == 0
+
+
+def test_error_image_api(ref):
+    rng = np.random.default_rng(9)
+    a = rng.integers(0, 256, (37, 29, 3), dtype=np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-80, 80, a.shape), 0, 255).astype(np.uint8)
+    np.testing.assert_array_equal(api.error_image(a, b), ref.error_image(a, b))
+    q = api.quantize(a, 8, api.Termination.convergent(1e-4, 100), seed=1, error=True)
+    np.testing.assert_array_equal(q.error, ref.error_image(a, q.mapped))
