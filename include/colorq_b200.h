@@ -138,6 +138,14 @@ int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k,
 int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
                     uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,
                     uint8_t* rgb_out, uint8_t* error_out, cqb_report* report);
+/* run_km_full (kmeans.hpp:409-426), the KM / KM-C branch of generate_palette
+ * (methods.hpp:155-160): conventional k-means over
+ * every pixel with the exhaustive assignment (assign_naive, kmeans.hpp:83-106),
+ * initialized like run_wsm. Runs on the unique colors weighted by their
+ * counts (the same memberships, sums and SSE); report->dist_evals is the
+ * reference's P*k per iteration. report->mse is 0 (filled by the caller). */
+int cqb_run_km_full(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                    uint64_t seed, double* centers_out, double* sse_history, int hist_cap, cqb_report* report);
 /* error_image(original, quantized) (image_ops.hpp:55-71): per channel
  * 255 - min(255, 4|o - q|). Host buffers of n_pixels u8x3 pixels. */
 int cqb_error_image(cqb_ctx* ctx, const uint8_t* original, const uint8_t* quantized, uint64_t n_pixels,

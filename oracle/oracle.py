@@ -123,6 +123,8 @@ class Oracle:
             f("palette_text").argtypes = [_f64p, C.c_int, C.c_char_p, C.c_int64]
             f("palette_text").restype = C.c_int64
             f("error_image").argtypes = [_u8p, _u8p, C.c_uint64, _u8p]
+            f("run_km_full").argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                         C.c_uint64, _f64p, _f64p, _u64p, _f64p, C.c_int]
         f("mse").argtypes = [_u8p, _u8p, C.c_uint64]
         f("mse").restype = C.c_double
 
@@ -300,6 +302,23 @@ class Oracle:
         buf = C.create_string_buffer(int(n) + 1)
         self._f("palette_text")(_p(c, _f64p), k, buf, n)
         return buf.raw[:n].decode()
+
+    def run_km_full(self, img: np.ndarray, k: int, mode: int = 1, max_iters: int = 10, eps: float = 1e-4,
+                    cap: int = 100, seed: int = 1):
+        """run_km_full (kmeans.hpp:409-426): KM / KM-C over every pixel."""
+        assert self.kind == "reference"
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape[:2]
+        C_out = np.zeros(3 * k)
+        sse = np.zeros(1)
+        ev = np.zeros(1, np.uint64)
+        hist = np.zeros(max(cap, max_iters) + 1)
+        it = self._f("run_km_full")(_p(img, _u8p), w, h, k, mode, max_iters, eps, cap, seed, _p(C_out, _f64p),
+                                    _p(sse, _f64p), _p(ev, _u64p), _p(hist, _f64p), hist.size)
+        if it < 0:
+            raise ValueError("run_km_full failed")
+        return dict(centers=C_out.reshape(k, 3), iterations=int(it), sse=float(sse[0]), dist_evals=int(ev[0]),
+                    sse_history=hist[:it].copy())
 
     def error_image(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
         assert self.kind == "reference"

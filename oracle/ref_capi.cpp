@@ -249,6 +249,22 @@ double ref_quantize_many(const std::uint8_t* const* imgs, int count, int w, int 
   return watch.elapsed_ms();
 }
 
+// run_km_full (kmeans.hpp:409-426), §8(f) row f3: returns iterations or -1.
+int ref_run_km_full(const std::uint8_t* rgb, int w, int h, int k, int mode, int max_iters, double eps, int cap,
+                    std::uint64_t seed, double* C_out, double* sse, std::uint64_t* evals, double* hist, int hist_cap) {
+  try {
+    const RgbImage img = make_image(rgb, std::uint64_t(w), std::uint64_t(h));
+    const KmRunResult r = run_km_full(img, k, make_term(mode, max_iters, eps, cap), seed);
+    store_palette(r.palette, C_out);
+    *sse = r.report.sse;
+    *evals = r.report.dist_evals;
+    for (int i = 0; i < std::min<int>(hist_cap, int(r.report.sse_history.size())); ++i) hist[i] = r.report.sse_history[i];
+    return r.report.iterations;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 // ---- §8(f) row f1: file formats and error_image (ppm.hpp, palette.hpp,
 // image_ops.hpp:55-71), for the CLI parity tests.
 

@@ -133,13 +133,13 @@ class QuantizeOutcome:
 class MethodParams:
     """methods.hpp:71-85 (the WSM-relevant knobs)."""
 
-    id: str = "wsm"  # "wsm" (fixed iters) or "wsm-c" (convergent)
+    id: str = "wsm"  # "wsm" / "km" (fixed iters) or "wsm-c" / "km-c" (convergent)
     iters: int = 10
     epsilon: float = 1e-4
     hard_cap: int = 1000
 
     def termination(self) -> Termination:
-        if self.id == "wsm-c":
+        if self.id in ("wsm-c", "km-c"):
             return Termination.convergent(self.epsilon, self.hard_cap)
         return Termination.fixed(self.iters)
 
@@ -300,6 +300,10 @@ def generate_palette(img: np.ndarray, mp: MethodParams, k: int, seed: int, devic
     quantizers are outside this framework's scope)."""
     if k < 1:
         raise ValueError("k must be >= 1")
+    if mp.id in ("km", "km-c"):  # methods.hpp:155-160 (SURVEY.md §8(f) row f3)
+        q = run_km_full(img, k, mp.termination(), seed, device=device)
+        q.report.method = mp.id
+        return q
     if mp.id not in ("wsm", "wsm-c"):
         raise UnknownMethodError(f"method '{mp.id}' is not provided by the B200 WSM path")
     q = quantize(img, k, mp.termination(), seed, index_map=False, mapped=False, device=device)
@@ -317,6 +321,26 @@ def error_image(original: np.ndarray, quantized: np.ndarray, device: int = 0) ->
     ctx = context(device)
     ctx.check(ctx.lib.cqb_error_image(ctx.h, _p(a, _u8p), _p(b, _u8p), a.size // 3, _p(out, _u8p)))
     return out
+
+
+def run_km_full(img: np.ndarray, k: int, term: Termination | None = None, seed: int = 1,
+                device: int = 0) -> QuantizeOutcome:
+    """Conventional k-means over every pixel (kmeans.hpp:409-426): KM / KM-C."""
+    a = _rgb(img)
+    if a.ndim != 3:
+        raise CqbInvalidArgument(N.CQB_ERR_INVALID_ARGUMENT, "run_km_full: expects an H x W x 3 image")
+    h, w = a.shape[0], a.shape[1]
+    term = term or Termination.convergent()
+    ctx = context(device)
+    cap = term.iteration_budget
+    centers = np.zeros(3 * max(k, 1))
+    hist_out = np.zeros(cap)
+    rep = N.Report()
+    t = term.native()
+    ctx.check(ctx.lib.cqb_run_km_full(ctx.h, _p(a, _u8p), w, h, k, C.byref(t), seed, _p(centers, _f64p),
+                                      _p(hist_out, _f64p), cap, C.byref(rep)))
+    r = _report_from(rep, "km-c" if term.mode == "convergent" else "km", hist_out)
+    return QuantizeOutcome(centers.reshape(-1, 3)[:k].copy(), r)
 
 
 def map_pixels_indexed(img: np.ndarray, palette: np.ndarray, device: int = 0):

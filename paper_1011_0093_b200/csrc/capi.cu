@@ -61,9 +61,10 @@ struct cqb_ctx {
   uint32_t* d_counts = nullptr;
   uint32_t* d_first = nullptr;
   uint32_t* d_bitmap = nullptr;  // P-bit first-occurrence bitmap (+ pad)
-  uint32_t* d_occ = nullptr;
+  uint32_t* d_occ = nullptr;     // 2^24-bit bin occupancy map (small images; all-zero between calls)
   uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
-  uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output     // 2^24-bit bin occupancy map (small images; all-zero between calls)
+  uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output
+  int naive_mode = 0;             // set only while cqb_run_km_full enqueues: exhaustive assign (KM)
   uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
   uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
   uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
@@ -368,6 +369,7 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.block_times = ctx->profiling ? ctx->d_block_times : nullptr;
   L.stamp_iter = ctx->stamp_iter;
   L.debug_flags = ctx->debug_flags;
+  L.naive = ctx->naive_mode;
   if (ctx->profiling)
     CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
   void* args[] = {&L};
@@ -875,6 +877,22 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
   if (error_out) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (report) *report = rep;
+  return CQB_OK;
+}
+
+int cqb_run_km_full(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                    uint64_t seed, double* centers_out, double* sse_history, int hist_cap, cqb_report* report) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  cqb_report rep{};
+  ctx->naive_mode = 1;
+  const int rc = cqb_quantize_ex(ctx, rgb, width, height, k, term, seed, centers_out, sse_history, hist_cap, nullptr,
+                                 nullptr, nullptr, &rep);
+  ctx->naive_mode = 0;
+  TRY(rc);
+  // assign_naive counts every (pixel, center) pair (kmeans.hpp:104); no tables
+  rep.dist_evals = (uint64_t)rep.iterations * (uint64_t)width * (uint64_t)height * (uint64_t)k;
+  rep.mse = 0.0;  // run_km_full leaves mse to the caller (methods.hpp:104-106)
   if (report) *report = rep;
   return CQB_OK;
 }

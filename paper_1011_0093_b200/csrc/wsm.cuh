@@ -78,6 +78,7 @@ struct LoopParams {
   int traj_cap;
   unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (8 per iteration)
   int moments_only;  // sharded step: stop after assign + flush (global sums = this shard's moments)
+  int naive;         // run_km_full (kmeans.hpp:409-426): exhaustive assign, no center tables
   int debug_flags;   // diagnostics only (tools/ablate.py): 1 = skip the candidate scan (results wrong)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
   int stamp_iter;
@@ -492,6 +493,7 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
   }
 }
 
+template <bool Naive>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
@@ -547,8 +549,16 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       int best = p;
       const double* rd = gd + p * KMAX;
       const uint8_t* ro = go + p * KMAX;
-      // the reference's scan (kmeans.hpp:217-231), two entries per step
       int J = 1;
+      if constexpr (Naive) {
+        // assign_naive (kmeans.hpp:83-106): every center, strict < from c_0,
+        // i.e. the lexicographic (d, index) minimum over all k (the start
+        // from the previous label does not change that minimum).
+        for (int t = 0; t < k; ++t)
+          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+        J = 0;  // dist_evals are P*k per iteration, set by the host
+      } else
+      // the reference's scan (kmeans.hpp:217-231), two entries per step
       if (k > 1 && rd[1] < bound && !(L.debug_flags & 1)) {
         n_active += 1;
         int j = 1;
@@ -805,9 +815,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     L.block_times[7 * gridDim.x + blockIdx.x] = 0ull;
   }
   // prologue: tables of the initial centers (all pairs evaluated: non-incremental)
-  tables_all(S, st, k, false);
+  if (!L.naive) tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
-  unsigned long long pair_evals = (unsigned long long)k * (unsigned long long)(k - 1) / 2;  // block 0 only
+  // pair evaluations of the center tables (block 0 only); none in naive mode
+  unsigned long long pair_evals = L.naive ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
   grid.sync();
 
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
@@ -831,7 +842,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      if (L.naive)
+        assign_sort_means<true>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      else
+        assign_sort_means<false>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -926,7 +940,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         // pair evaluations of the incremental table update (kmeans.hpp:137-155)
         if (!stop) {
           const unsigned long long still = (unsigned long long)(k - moved);
-          pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
+          if (!L.naive)
+            pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
         }
       }
       if (L.traj && it <= L.traj_cap)
@@ -953,7 +968,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     __syncthreads();
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
-    tables_all(S, st, k, true);  // wasted work on the final iteration only
+    if (!L.naive) tables_all(S, st, k, true);  // wasted work on the final iteration only
     if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
     BLOCK_STAMP(5);
     grid.sync();

@@ -33,7 +33,7 @@ def _run(args, timeout=300):
     return subprocess.run([CLI] + args, capture_output=True, text=True, timeout=timeout)
 
 
-@pytest.mark.parametrize("method,k", [("wsm-c", 16), ("wsm", 32)])
+@pytest.mark.parametrize("method,k", [("wsm-c", 16), ("wsm", 32), ("km-c", 8)])
 def test_cli_quantize_byte_identical(method, k, ref, tmp_path):
     img = gmm_image(128, 64, 24, 77)  # P = 8192 (power of two: bit-exact centers)
     src = tmp_path / "in.ppm"
@@ -43,8 +43,13 @@ def test_cli_quantize_byte_identical(method, k, ref, tmp_path):
               "--error-image", str(err), "--dump-histogram", str(hist)])
     assert r.returncode == 0, r.stderr
     # the reference CLI: MethodParams defaults, Termination::convergent(1e-4) = cap 1000 (kmeans.hpp:34)
-    mode = 1 if method == "wsm-c" else 0
-    q = ref.quantize(img, k, mode=mode, max_iters=10, eps=1e-4, cap=1000, seed=3)
+    mode = 1 if method.endswith("-c") else 0
+    if method.startswith("km"):  # run_km_full, then map_pixels + mse (tools/colorq.cpp:96-102)
+        o = ref.run_km_full(img, k, mode=mode, max_iters=10, eps=1e-4, cap=1000, seed=3)
+        mapped, _ = ref.map_pixels(img, o["centers"])
+        q = dict(centers=o["centers"], iterations=o["iterations"], mapped=mapped, mse=ref.mse(img, mapped))
+    else:
+        q = ref.quantize(img, k, mode=mode, max_iters=10, eps=1e-4, cap=1000, seed=3)
     assert out.read_bytes() == ref.write_ppm(q["mapped"])
     assert pal.read_text() == ref.palette_text(q["centers"])
     assert err.read_bytes() == ref.write_ppm(ref.error_image(img, q["mapped"]))

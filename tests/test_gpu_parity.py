@@ -337,3 +337,27 @@ def test_cfg4_properties(port):
     again, idx2, _ = api.map_pixels_indexed(q.mapped, q.palette)
     np.testing.assert_array_equal(again, q.mapped)
     assert q.report.mse == pytest.approx(api.mse(img, q.mapped), rel=0, abs=0)
+
+
+# --------------------------------------------------------------------------- §8(f) f3: KM / KM-C
+@pytest.mark.parametrize("case,k,mode", [("gmm128x64", 16, 1), ("gmm128x64", 8, 0), ("gmm96x64", 12, 1),
+                                         ("gmm101x77", 8, 1)])
+def test_run_km_full_matches_reference(case, k, mode, images, ref):
+    """run_km_full (kmeans.hpp:409-426): exhaustive assignment over every
+    pixel; memberships, centers, SSE history and the reference's P*k
+    dist_evals per iteration."""
+    img = images[case]
+    P = img.shape[0] * img.shape[1]
+    term = api.Termination.convergent(1e-4, 100) if mode else api.Termination.fixed(7)
+    q = api.run_km_full(img, k, term, seed=2)
+    o = ref.run_km_full(img, k, mode=mode, max_iters=7, eps=1e-4, cap=100, seed=2)
+    assert q.report.iterations == o["iterations"]
+    assert q.report.dist_evals == o["dist_evals"] == o["iterations"] * P * k
+    if _pow2(P):
+        np.testing.assert_array_equal(q.palette, o["centers"])
+    else:
+        np.testing.assert_allclose(q.palette, o["centers"], rtol=CENTER_RTOL)
+    np.testing.assert_allclose(q.report.sse_history, o["sse_history"], rtol=SSE_RTOL)
+    g = api.generate_palette(img, api.MethodParams("km-c" if mode else "km", iters=7), k, 2)
+    np.testing.assert_array_equal(g.palette, q.palette)
+    assert g.report.method == ("km-c" if mode else "km")

@@ -7,7 +7,7 @@
 //               [--iters N] [--epsilon E]
 //
 // Exit codes follow the reference (tools/colorq.cpp:21-43): 2 I/O or PPM
-// error, 3 unknown / unsupported method, 4 invalid parameters. Only the WSM
+// error, 3 unknown / unsupported method, 4 invalid parameters. The WSM and KM
 // methods are provided; the reference's other method names exit with 3.
 // Argument parsing is hand-written (the reference uses CLI11).
 #include <cstdio>
@@ -74,11 +74,29 @@ int quantize(const Args& a) {
     mp.id = *id;
     if (a.iters > 0) mp.iters = a.iters;
     if (a.epsilon > 0) mp.epsilon = a.epsilon;
-    if (mp.id != colorq::MethodId::Wsm && mp.id != colorq::MethodId::WsmC)
-      throw colorq::UnknownMethodError("method '" + a.method + "' is not provided by the B200 WSM path");
+    const bool km = mp.id == colorq::MethodId::Km || mp.id == colorq::MethodId::KmC;
+    if (mp.id != colorq::MethodId::Wsm && mp.id != colorq::MethodId::WsmC && !km)
+      throw colorq::UnknownMethodError("method '" + a.method + "' is not provided by the B200 path");
 
     const colorq::RgbImage image = colorq::load_ppm(a.input);
     if (a.k < 1) throw std::invalid_argument("k must be >= 1");  // methods.hpp:109, after the load as in the reference
+    if (km) {  // run_km_full, then map / mse / error image as the reference CLI composes them
+      colorq::QuantizeOutcome qo = colorq::generate_palette(image, mp, a.k, a.seed);
+      const colorq::RgbImage mapped = colorq::map_pixels(image, qo.palette);
+      qo.report.mse = colorq::mse(image, mapped);
+      colorq::save_ppm(mapped, a.output);
+      if (!a.palette.empty()) colorq::save_palette(qo.palette, a.palette);
+      if (!a.error_image.empty()) colorq::save_ppm(colorq::error_image(image, mapped), a.error_image);
+      if (!a.hist_csv.empty()) {
+        std::ofstream out(a.hist_csv);
+        if (!out) throw std::runtime_error("cannot open " + a.hist_csv + " for writing");
+        colorq::write_histogram_csv(out, colorq::build_histogram(image));
+      }
+      std::printf("method=%s k=%d seed=%llu iterations=%d mse=%s psnr=%s time_ms=%s\n", qo.report.method.c_str(),
+                  a.k, (unsigned long long)a.seed, qo.report.iterations, colorq::fmt_g6(qo.report.mse).c_str(),
+                  colorq::fmt_g6(colorq::psnr(qo.report.mse)).c_str(), colorq::fmt_g6(qo.report.elapsed_ms).c_str());
+      return 0;
+    }
     // generate_palette + map_pixels + mse + error_image in one device pass
     const colorq::Termination term = mp.termination();
     const cqb_termination t = colorq::b200::native(term);
