@@ -146,6 +146,15 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
  * reference's P*k per iteration. report->mse is 0 (filled by the caller). */
 int cqb_run_km_full(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
                     uint64_t seed, double* centers_out, double* sse_history, int hist_cap, cqb_report* report);
+/* run_fkm (fast_variants.hpp:20-81), the FKM / FKM-C branch of
+ * generate_palette (methods.hpp:163-178): iteration 1
+ * exhaustive, then each point searches only the k_prime centers nearest to
+ * its previous one (the first k_prime entries of its sorted center row).
+ * Initialized like run_wsm; report->dist_evals follows the reference
+ * (P*k, then P*k' per iteration, plus the center-table pairs). */
+int cqb_run_fkm(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, int k_prime,
+                const cqb_termination* term, uint64_t seed, double* centers_out, double* sse_history, int hist_cap,
+                cqb_report* report);
 /* error_image(original, quantized) (image_ops.hpp:55-71): per channel
  * 255 - min(255, 4|o - q|). Host buffers of n_pixels u8x3 pixels. */
 int cqb_error_image(cqb_ctx* ctx, const uint8_t* original, const uint8_t* quantized, uint64_t n_pixels,

@@ -139,8 +139,10 @@ struct MethodParams {
   MethodId id = MethodId::Wsm;
   int iters = 10;
   double epsilon = 1e-4;
+  int k_prime = 8;  // fkm neighbour count (methods.hpp:75)
   Termination termination() const {
-    return id == MethodId::WsmC || id == MethodId::KmC ? Termination::convergent(epsilon) : Termination::fixed(iters);
+    return id == MethodId::WsmC || id == MethodId::KmC || id == MethodId::FkmC ? Termination::convergent(epsilon)
+                                                                                 : Termination::fixed(iters);
   }
 };
 
@@ -263,8 +265,9 @@ inline KmRunResult run_wsm(const ColorHistogram& hist, int k, const Termination&
 // outside the B200 path and raise UnknownMethodError.
 inline QuantizeOutcome generate_palette(const RgbImage& image, const MethodParams& mp, int k, std::uint64_t seed) {
   if (k < 1) throw std::invalid_argument("k must be >= 1");
-  const bool km = mp.id == MethodId::Km || mp.id == MethodId::KmC;  // run_km_full, methods.hpp:155-160
-  if (mp.id != MethodId::Wsm && mp.id != MethodId::WsmC && !km)
+  const bool km = mp.id == MethodId::Km || mp.id == MethodId::KmC;     // run_km_full, methods.hpp:155-160
+  const bool fkm = mp.id == MethodId::Fkm || mp.id == MethodId::FkmC;  // run_fkm, methods.hpp:163-178
+  if (mp.id != MethodId::Wsm && mp.id != MethodId::WsmC && !km && !fkm)
     throw UnknownMethodError("method not provided by the B200 path");
   if (image.size() == 0) throw std::invalid_argument("build_histogram: empty image");
   const auto t0 = std::chrono::steady_clock::now();
@@ -276,12 +279,17 @@ inline QuantizeOutcome generate_palette(const RgbImage& image, const MethodParam
   if (km)
     b200::check(cqb_run_km_full(b200::context(), b200::bytes(image), image.width, image.height, k, &t, seed,
                                 centers.data(), hist_out.data(), cap, &rep));
+  else if (fkm)
+    b200::check(cqb_run_fkm(b200::context(), b200::bytes(image), image.width, image.height, k, mp.k_prime, &t, seed,
+                            centers.data(), hist_out.data(), cap, &rep));
   else
     b200::check(cqb_quantize(b200::context(), b200::bytes(image), image.width, image.height, k, &t, seed,
                              centers.data(), hist_out.data(), cap, nullptr, nullptr, &rep));
   QuantizeOutcome out;
   out.palette = b200::palette_from(centers.data(), k);
-  out.report.method = km ? (mp.id == MethodId::KmC ? "km-c" : "km") : (mp.id == MethodId::WsmC ? "wsm-c" : "wsm");
+  out.report.method = km    ? (mp.id == MethodId::KmC ? "km-c" : "km")
+                      : fkm ? (mp.id == MethodId::FkmC ? "fkm-c" : "fkm")
+                            : (mp.id == MethodId::WsmC ? "wsm-c" : "wsm");
   out.report.k = k;
   out.report.seed = seed;
   out.report.iterations = rep.iterations;

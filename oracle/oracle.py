@@ -123,6 +123,8 @@ class Oracle:
             f("palette_text").argtypes = [_f64p, C.c_int, C.c_char_p, C.c_int64]
             f("palette_text").restype = C.c_int64
             f("error_image").argtypes = [_u8p, _u8p, C.c_uint64, _u8p]
+            f("run_fkm").argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                     C.c_uint64, _f64p, _f64p, _u64p, _f64p, C.c_int]
             f("run_km_full").argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                          C.c_uint64, _f64p, _f64p, _u64p, _f64p, C.c_int]
         f("mse").argtypes = [_u8p, _u8p, C.c_uint64]
@@ -317,6 +319,23 @@ class Oracle:
                                     _p(sse, _f64p), _p(ev, _u64p), _p(hist, _f64p), hist.size)
         if it < 0:
             raise ValueError("run_km_full failed")
+        return dict(centers=C_out.reshape(k, 3), iterations=int(it), sse=float(sse[0]), dist_evals=int(ev[0]),
+                    sse_history=hist[:it].copy())
+
+    def run_fkm(self, img: np.ndarray, k: int, k_prime: int = 8, mode: int = 1, max_iters: int = 10,
+                eps: float = 1e-4, seed: int = 1):
+        """generate_palette FKM / FKM-C (methods.hpp:163-178; hard cap 1000)."""
+        assert self.kind == "reference"
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape[:2]
+        C_out = np.zeros(3 * k)
+        sse = np.zeros(1)
+        ev = np.zeros(1, np.uint64)
+        hist = np.zeros(1001)
+        it = self._f("run_fkm")(_p(img, _u8p), w, h, k, k_prime, mode, max_iters, eps, seed, _p(C_out, _f64p),
+                                _p(sse, _f64p), _p(ev, _u64p), _p(hist, _f64p), hist.size)
+        if it < 0:
+            raise ValueError("run_fkm failed")
         return dict(centers=C_out.reshape(k, 3), iterations=int(it), sse=float(sse[0]), dist_evals=int(ev[0]),
                     sse_history=hist[:it].copy())
 

@@ -265,6 +265,27 @@ int ref_run_km_full(const std::uint8_t* rgb, int w, int h, int k, int mode, int 
   }
 }
 
+// run_fkm through generate_palette's FKM branch (methods.hpp:163-178), §8(f) row f4.
+int ref_run_fkm(const std::uint8_t* rgb, int w, int h, int k, int k_prime, int mode, int max_iters, double eps,
+                std::uint64_t seed, double* C_out, double* sse, std::uint64_t* evals, double* hist, int hist_cap) {
+  try {
+    const RgbImage img = make_image(rgb, std::uint64_t(w), std::uint64_t(h));
+    MethodParams mp;
+    mp.id = mode ? MethodId::FkmC : MethodId::Fkm;
+    mp.iters = max_iters;
+    mp.epsilon = eps;
+    mp.k_prime = k_prime;
+    const QuantizeOutcome r = generate_palette(img, mp, k, seed);
+    store_palette(r.palette, C_out);
+    *sse = r.report.sse;
+    *evals = r.report.dist_evals;
+    for (int i = 0; i < std::min<int>(hist_cap, int(r.report.sse_history.size())); ++i) hist[i] = r.report.sse_history[i];
+    return r.report.iterations;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 // ---- §8(f) row f1: file formats and error_image (ppm.hpp, palette.hpp,
 // image_ops.hpp:55-71), for the CLI parity tests.
 

@@ -133,13 +133,14 @@ class QuantizeOutcome:
 class MethodParams:
     """methods.hpp:71-85 (the WSM-relevant knobs)."""
 
-    id: str = "wsm"  # "wsm" / "km" (fixed iters) or "wsm-c" / "km-c" (convergent)
+    id: str = "wsm"  # "wsm" / "km" / "fkm" (fixed iters) or "wsm-c" / "km-c" / "fkm-c" (convergent)
     iters: int = 10
     epsilon: float = 1e-4
     hard_cap: int = 1000
+    k_prime: int = 8  # fkm neighbour count (methods.hpp:75)
 
     def termination(self) -> Termination:
-        if self.id in ("wsm-c", "km-c"):
+        if self.id in ("wsm-c", "km-c", "fkm-c"):
             return Termination.convergent(self.epsilon, self.hard_cap)
         return Termination.fixed(self.iters)
 
@@ -304,6 +305,10 @@ def generate_palette(img: np.ndarray, mp: MethodParams, k: int, seed: int, devic
         q = run_km_full(img, k, mp.termination(), seed, device=device)
         q.report.method = mp.id
         return q
+    if mp.id in ("fkm", "fkm-c"):  # methods.hpp:163-178 (row f4)
+        q = run_fkm(img, k, mp.k_prime, mp.termination(), seed, device=device)
+        q.report.method = mp.id
+        return q
     if mp.id not in ("wsm", "wsm-c"):
         raise UnknownMethodError(f"method '{mp.id}' is not provided by the B200 WSM path")
     q = quantize(img, k, mp.termination(), seed, index_map=False, mapped=False, device=device)
@@ -340,6 +345,26 @@ def run_km_full(img: np.ndarray, k: int, term: Termination | None = None, seed: 
     ctx.check(ctx.lib.cqb_run_km_full(ctx.h, _p(a, _u8p), w, h, k, C.byref(t), seed, _p(centers, _f64p),
                                       _p(hist_out, _f64p), cap, C.byref(rep)))
     r = _report_from(rep, "km-c" if term.mode == "convergent" else "km", hist_out)
+    return QuantizeOutcome(centers.reshape(-1, 3)[:k].copy(), r)
+
+
+def run_fkm(img: np.ndarray, k: int, k_prime: int = 8, term: Termination | None = None, seed: int = 1,
+            device: int = 0) -> QuantizeOutcome:
+    """Finite-state k-means over every pixel (fast_variants.hpp:20-81): FKM / FKM-C."""
+    a = _rgb(img)
+    if a.ndim != 3:
+        raise CqbInvalidArgument(N.CQB_ERR_INVALID_ARGUMENT, "run_fkm: expects an H x W x 3 image")
+    h, w = a.shape[0], a.shape[1]
+    term = term or Termination.convergent()
+    ctx = context(device)
+    cap = term.iteration_budget
+    centers = np.zeros(3 * max(k, 1))
+    hist_out = np.zeros(cap)
+    rep = N.Report()
+    t = term.native()
+    ctx.check(ctx.lib.cqb_run_fkm(ctx.h, _p(a, _u8p), w, h, k, k_prime, C.byref(t), seed, _p(centers, _f64p),
+                                  _p(hist_out, _f64p), cap, C.byref(rep)))
+    r = _report_from(rep, "fkm-c" if term.mode == "convergent" else "fkm", hist_out)
     return QuantizeOutcome(centers.reshape(-1, 3)[:k].copy(), r)
 
 

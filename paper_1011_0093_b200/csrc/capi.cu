@@ -65,6 +65,7 @@ struct cqb_ctx {
   uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
   uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output
   int naive_mode = 0;             // set only while cqb_run_km_full enqueues: exhaustive assign (KM)
+  int fkm_kprime = 0;             // set only while cqb_run_fkm enqueues: FKM neighbour count
   uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
   uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
   uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
@@ -370,6 +371,7 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.stamp_iter = ctx->stamp_iter;
   L.debug_flags = ctx->debug_flags;
   L.naive = ctx->naive_mode;
+  L.fkm_kprime = ctx->fkm_kprime;
   if (ctx->profiling)
     CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
   void* args[] = {&L};
@@ -893,6 +895,26 @@ int cqb_run_km_full(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   // assign_naive counts every (pixel, center) pair (kmeans.hpp:104); no tables
   rep.dist_evals = (uint64_t)rep.iterations * (uint64_t)width * (uint64_t)height * (uint64_t)k;
   rep.mse = 0.0;  // run_km_full leaves mse to the caller (methods.hpp:104-106)
+  if (report) *report = rep;
+  return CQB_OK;
+}
+
+int cqb_run_fkm(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, int k_prime,
+                const cqb_termination* term, uint64_t seed, double* centers_out, double* sse_history, int hist_cap,
+                cqb_report* report) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (k_prime < 1 || k_prime > k) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "run_fkm: need 1 <= k_prime <= k");
+  cqb_report rep{};
+  ctx->fkm_kprime = k_prime;
+  const int rc = cqb_quantize_ex(ctx, rgb, width, height, k, term, seed, centers_out, sse_history, hist_cap, nullptr,
+                                 nullptr, nullptr, &rep);
+  ctx->fkm_kprime = 0;
+  TRY(rc);
+  // iteration 1 is assign_naive (P*k); later ones search k' centers (P*k'),
+  // plus the table pair evaluations already in rep.dist_evals
+  const uint64_t P = (uint64_t)width * (uint64_t)height;
+  rep.dist_evals += P * (uint64_t)k + (uint64_t)(rep.iterations - 1) * P * (uint64_t)k_prime;
+  rep.mse = 0.0;
   if (report) *report = rep;
   return CQB_OK;
 }

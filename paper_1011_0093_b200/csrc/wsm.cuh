@@ -79,6 +79,7 @@ struct LoopParams {
   unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (8 per iteration)
   int moments_only;  // sharded step: stop after assign + flush (global sums = this shard's moments)
   int naive;         // run_km_full (kmeans.hpp:409-426): exhaustive assign, no center tables
+  int fkm_kprime;    // run_fkm (fast_variants.hpp:20-81): search the k' nearest centers of the previous one
   int debug_flags;   // diagnostics only (tools/ablate.py): 1 = skip the candidate scan (results wrong)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
   int stamp_iter;
@@ -466,7 +467,7 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
           if (S.row0[mid] < bound) lo_j = mid + 1;
           else hi_j = mid;
         }
-        evals += (unsigned long long)lo_j;  // 1 (prev) + (lo_j - 1) candidates
+        if (L.fkm_kprime == 0) evals += (unsigned long long)lo_j;  // 1 (prev) + (lo_j - 1) candidates
         L.labels[i] = (uint8_t)lab;
         cnt = L.counts[i];
       }
@@ -493,7 +494,10 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
   }
 }
 
-template <bool Naive>
+// Assign variants: sort-means (WSM), exhaustive (KM), first k' of the row (FKM).
+enum class Assign { SortMeans, Naive, Fkm };
+
+template <Assign Mode>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
@@ -550,7 +554,16 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       const double* rd = gd + p * KMAX;
       const uint8_t* ro = go + p * KMAX;
       int J = 1;
-      if constexpr (Naive) {
+      if constexpr (Mode == Assign::Fkm) {
+        // run_fkm (fast_variants.hpp:42-52): lexicographic (d, index) minimum
+        // over order[p][0..k') - self first, then its nearest centers
+        const int kp = L.fkm_kprime;
+        for (int j = 1; j < kp; ++j) {
+          const int t = ro[j];
+          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+        }
+        J = 0;  // dist_evals are P*k' per iteration, set by the host
+      } else if constexpr (Mode == Assign::Naive) {
         // assign_naive (kmeans.hpp:83-106): every center, strict < from c_0,
         // i.e. the lexicographic (d, index) minimum over all k (the start
         // from the previous label does not change that minimum).
@@ -818,7 +831,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   if (!L.naive) tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
-  unsigned long long pair_evals = L.naive ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+  unsigned long long pair_evals =
+      (L.naive || L.fkm_kprime > 0) ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
   grid.sync();
 
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
@@ -843,9 +857,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
       if (L.naive)
-        assign_sort_means<true>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+        assign_sort_means<Assign::Naive>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      else if (L.fkm_kprime > 0)
+        assign_sort_means<Assign::Fkm>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       else
-        assign_sort_means<false>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+        assign_sort_means<Assign::SortMeans>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -940,7 +956,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         // pair evaluations of the incremental table update (kmeans.hpp:137-155)
         if (!stop) {
           const unsigned long long still = (unsigned long long)(k - moved);
-          if (!L.naive)
+          // FKM builds its first tables for iteration 2 (fast_variants.hpp:42): all pairs
+          if (L.fkm_kprime > 0 && it == 1)
+            pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+          else if (!L.naive)
             pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
         }
       }

@@ -361,3 +361,27 @@ def test_run_km_full_matches_reference(case, k, mode, images, ref):
     g = api.generate_palette(img, api.MethodParams("km-c" if mode else "km", iters=7), k, 2)
     np.testing.assert_array_equal(g.palette, q.palette)
     assert g.report.method == ("km-c" if mode else "km")
+
+
+# --------------------------------------------------------------------------- §8(f) f4: FKM / FKM-C
+@pytest.mark.parametrize("case,k,kp,mode", [("gmm128x64", 16, 8, 1), ("gmm128x64", 24, 4, 0), ("gmm96x64", 12, 8, 1),
+                                            ("gmm128x64", 8, 8, 1)])
+def test_run_fkm_matches_reference(case, k, kp, mode, images, ref):
+    """run_fkm (fast_variants.hpp:20-81) through generate_palette's FKM branch:
+    centers, iterations, SSE history and dist_evals (P*k, then P*k' per
+    iteration, plus the center-table pairs)."""
+    img = images[case]
+    P = img.shape[0] * img.shape[1]
+    mp = api.MethodParams("fkm-c" if mode else "fkm", iters=6, k_prime=kp)
+    q = api.generate_palette(img, mp, k, 4)
+    o = ref.run_fkm(img, k, kp, mode=mode, max_iters=6, eps=1e-4, seed=4)
+    assert q.report.method == mp.id
+    assert q.report.iterations == o["iterations"]
+    assert q.report.dist_evals == o["dist_evals"]
+    if _pow2(P):
+        np.testing.assert_array_equal(q.palette, o["centers"])
+    else:
+        np.testing.assert_allclose(q.palette, o["centers"], rtol=CENTER_RTOL)
+    np.testing.assert_allclose(q.report.sse_history, o["sse_history"], rtol=SSE_RTOL)
+    with pytest.raises(api.CqbInvalidArgument):
+        api.run_fkm(img, 4, 8)  # k_prime > k (fast_variants.hpp:26)

@@ -7,8 +7,8 @@
 //               [--iters N] [--epsilon E]
 //
 // Exit codes follow the reference (tools/colorq.cpp:21-43): 2 I/O or PPM
-// error, 3 unknown / unsupported method, 4 invalid parameters. The WSM and KM
-// methods are provided; the reference's other method names exit with 3.
+// error, 3 unknown / unsupported method, 4 invalid parameters. The WSM, KM and
+// FKM methods are provided; the reference's other method names exit with 3.
 // Argument parsing is hand-written (the reference uses CLI11).
 #include <cstdio>
 #include <cstdlib>
@@ -74,13 +74,14 @@ int quantize(const Args& a) {
     mp.id = *id;
     if (a.iters > 0) mp.iters = a.iters;
     if (a.epsilon > 0) mp.epsilon = a.epsilon;
-    const bool km = mp.id == colorq::MethodId::Km || mp.id == colorq::MethodId::KmC;
+    const bool km = mp.id == colorq::MethodId::Km || mp.id == colorq::MethodId::KmC ||
+                    mp.id == colorq::MethodId::Fkm || mp.id == colorq::MethodId::FkmC;
     if (mp.id != colorq::MethodId::Wsm && mp.id != colorq::MethodId::WsmC && !km)
       throw colorq::UnknownMethodError("method '" + a.method + "' is not provided by the B200 path");
 
     const colorq::RgbImage image = colorq::load_ppm(a.input);
     if (a.k < 1) throw std::invalid_argument("k must be >= 1");  // methods.hpp:109, after the load as in the reference
-    if (km) {  // run_km_full, then map / mse / error image as the reference CLI composes them
+    if (km) {  // run_km_full / run_fkm, then map / mse / error image as the reference CLI composes them
       colorq::QuantizeOutcome qo = colorq::generate_palette(image, mp, a.k, a.seed);
       const colorq::RgbImage mapped = colorq::map_pixels(image, qo.palette);
       qo.report.mse = colorq::mse(image, mapped);
