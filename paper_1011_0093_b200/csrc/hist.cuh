@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
 // and its first pixel marked in the first-occurrence bitmap. The occupancy
 // words are cleared for the next call. Reads 2 MiB + the touched bins only.
 constexpr int OC_THREADS = 256;
-constexpr int OC_WORDS = OC_THREADS * 4;            // occupancy words per tile
+constexpr int OC_WPT = 1;                            // occupancy words per thread
+constexpr int OC_WORDS = OC_THREADS * OC_WPT;        // occupancy words per tile
 constexpr int N_OCC_TILES = (1 << 19) / OC_WORDS;   // 2^24 bins / 32 per word
 
 __global__ void __launch_bounds__(OC_THREADS) k_occ_compact(uint32_t* __restrict__ occ, uint2* __restrict__ bins,
@@ -220,9 +221,14 @@ __global__ void __launch_bounds__(OC_THREADS) k_occ_compact(uint32_t* __restrict
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t w0 = tile * OC_WORDS + tid * 4;
-  uint4 wv = *reinterpret_cast<const uint4*>(occ + w0);
-  const uint32_t cnt = __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+  const uint32_t w0 = tile * OC_WORDS + tid * OC_WPT;
+  uint32_t words[OC_WPT];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int q = 0; q < OC_WPT; ++q) {
+    words[q] = occ[w0 + q];
+    cnt += __popc(words[q]);
+  }
   uint32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -276,14 +282,13 @@ __global__ void __launch_bounds__(OC_THREADS) k_occ_compact(uint32_t* __restrict
   __syncthreads();
   if (cnt) {
     uint32_t pos = s_prefix + excl;
-    uint32_t words[4] = {wv.x, wv.y, wv.z, wv.w};
     int q = 0;
     // batches of up to 8 touched bins: their loads are issued together
     // (memory-level parallelism for the scattered bin reads)
     while (true) {
       uint32_t ms[8];
       int nb = 0;
-      while (nb < 8 && q < 4) {
+      while (nb < 8 && q < OC_WPT) {
         if (words[q] == 0u) {
           ++q;
           continue;
@@ -309,7 +314,8 @@ __global__ void __launch_bounds__(OC_THREADS) k_occ_compact(uint32_t* __restrict
         }
       }
     }
-    *reinterpret_cast<uint4*>(occ + w0) = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int e = 0; e < OC_WPT; ++e) occ[w0 + e] = 0u;
   }
   if (tile == N_OCC_TILES - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
 }
