@@ -16,6 +16,7 @@
 #include "hist.cuh"
 #include "map.cuh"
 #include "wsm.cuh"
+#include "prep.cuh"
 
 using namespace cqb;
 
@@ -62,6 +63,9 @@ struct cqb_ctx {
   uint32_t* d_first = nullptr;
   uint32_t* d_bitmap = nullptr;  // P-bit first-occurrence bitmap (+ pad)
   uint32_t* d_occ = nullptr;     // 2^24-bit bin occupancy map (small images; all-zero between calls)
+  uint32_t* d_block_counts = nullptr;  // k_prep_small scratch [2 * MAXBLK]
+  uint32_t* d_wofs = nullptr;          // k_prep_small scratch [2^19]
+  int prep_blocks = 0;                 // k_prep_small cooperative grid
   uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
   uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output
   int naive_mode = 0;             // set only while cqb_run_km_full enqueues: exhaustive assign (KM)
@@ -318,6 +322,35 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     CKL();
   }
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
+  if (sparse && ctx->prep_blocks > 0 && !(ctx->debug_flags & 32)) {
+    // compaction, first-occurrence ranks and init in one cooperative launch
+    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
+    PrepParams Q{};
+    Q.occ = ctx->d_occ;
+    Q.bins = ctx->bins;
+    Q.m_keys = ctx->d_mkeys;
+    Q.m_counts = ctx->d_mcounts;
+    Q.m_rank = ctx->d_mrank;
+    Q.n_unique = ctx->d_n;
+    Q.bitmap = ctx->d_bitmap;
+    Q.pre = ctx->d_bpre;
+    Q.n_words = n_words;
+    Q.block_counts = ctx->d_block_counts;
+    Q.wofs = ctx->d_wofs;
+    Q.draws = ctx->d_draws;
+    Q.ndraws = ndraws;
+    Q.k = init_k;
+    Q.st = ctx->st;
+    Q.r_keys = rank_order ? ctx->d_keys : nullptr;
+    Q.r_counts = ctx->d_counts;
+    Q.r_first = ctx->d_first;
+    Q.stamps = ctx->profiling ? ctx->d_block_times + 14 * MAXBLK : nullptr;
+    void* args[] = {&Q};
+    CK(cudaLaunchCooperativeKernel((const void*)k_prep_small, dim3(std::min(ctx->prep_blocks, MAXBLK)),
+                                   dim3(PREP_THREADS), args, 0, ctx->stream));
+    CKL();
+    return CQB_OK;
+  }
   if (sparse) {
     CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_OCC_TILES + 1), ctx->stream));
     k_occ_compact<<<N_OCC_TILES, OC_THREADS, 0, ctx->stream>>>(
@@ -375,8 +408,10 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   if (ctx->profiling)
     CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
   void* args[] = {&L};
-  CK(cudaLaunchCooperativeKernel((const void*)k_wsm_loop, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, 0,
-                                 ctx->stream));
+  const void* kern = L.naive ? (const void*)k_wsm_loop<Assign::Naive>
+                   : L.fkm_kprime > 0 ? (const void*)k_wsm_loop<Assign::Fkm>
+                                      : (const void*)k_wsm_loop<Assign::SortMeans>;
+  CK(cudaLaunchCooperativeKernel(kern, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, 0, ctx->stream));
   CKL();
   return CQB_OK;
 }
@@ -493,7 +528,7 @@ int cqb_create(int device, cqb_ctx** out) {
     if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
     ctx->num_sms = prop.multiProcessorCount;
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop, LOOP_THREADS, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans>, LOOP_THREADS, 0));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
     ctx->loop_blocks_max = std::min(nb, 1) * ctx->num_sms;
     CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
@@ -501,6 +536,11 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMalloc(&ctx->bins, sizeof(uint2) << 24));
     CK(cudaMemset(ctx->bins, 0, sizeof(uint2) << 24));
     CK(cudaMalloc(&ctx->d_occ, sizeof(uint32_t) << 19));
+    CK(cudaMalloc(&ctx->d_block_counts, sizeof(uint32_t) * 2 * MAXBLK));
+    CK(cudaMalloc(&ctx->d_wofs, sizeof(uint32_t) << 19));
+    int pb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_prep_small, PREP_THREADS, 0));
+    ctx->prep_blocks = std::min(std::max(pb, 0), 1) * ctx->num_sms;
     CK(cudaMemset(ctx->d_occ, 0, sizeof(uint32_t) << 19));
     CK(cudaMalloc(&ctx->lut, (size_t)1 << 24));
     CK(cudaMalloc(&ctx->bin_tile_state, sizeof(unsigned long long) * (N_BIN_TILES + 1)));
@@ -545,7 +585,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->d_err, ctx->tile_state,
-                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_block_counts, ctx->d_wofs, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,

@@ -92,10 +92,10 @@ struct LoopParams {
 // for all k draws in parallel (a rejection, probability < N'/2^64 per draw,
 // diverts to the exact sequential path); the k swaps then run in one thread
 // with positions >= k held in a small open-addressing map.
-__global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restrict__ keys,
-                                                      const unsigned long long* __restrict__ n_ptr, int k,
-                                                      const unsigned long long* __restrict__ draws, int ndraws,
-                                                      WsmState* st) {
+// Body of init_centers for one block (any blockDim >= 1; all threads of the
+// block must call it). Returns early, uniformly, on an error status.
+__device__ void init_centers_block(const uint32_t* __restrict__ keys, unsigned long long n, int k,
+                                   const unsigned long long* __restrict__ draws, int ndraws, WsmState* st) {
   // Partial Fisher-Yates (kmeans.hpp:58-68): for i < k, j_i = i + bounded_rand(N'-i),
   // swap(idx[i], idx[j_i]), center i = colors[idx[i]]. Position i is final
   // after step i (later steps swap positions >= i+1), so with
@@ -107,7 +107,6 @@ __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restric
   __shared__ uint32_t wv[2][KMAX];
   __shared__ int s_rejected;
   const int tid = threadIdx.x;
-  const unsigned long long n = *n_ptr;
   if ((unsigned long long)k > n) {
     if (tid == 0) st->status = ST_K_EXCEEDS_N;
     return;
@@ -175,6 +174,13 @@ __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restric
     }
     st->chosen[i] = chosen;
   }
+}
+
+__global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restrict__ keys,
+                                                      const unsigned long long* __restrict__ n_ptr, int k,
+                                                      const unsigned long long* __restrict__ draws, int ndraws,
+                                                      WsmState* st) {
+  init_centers_block(keys, *n_ptr, k, draws, ndraws, st);
 }
 
 // Initial centers from the Morton-order samples: center i = the sample whose
@@ -467,7 +473,7 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
           if (S.row0[mid] < bound) lo_j = mid + 1;
           else hi_j = mid;
         }
-        if (L.fkm_kprime == 0) evals += (unsigned long long)lo_j;  // 1 (prev) + (lo_j - 1) candidates
+        evals += (unsigned long long)lo_j;  // 1 (prev) + (lo_j - 1) candidates (KM/FKM: replaced by the host)
         L.labels[i] = (uint8_t)lab;
         cnt = L.counts[i];
       }
@@ -786,7 +792,11 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 }
 
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
+// One instantiation per assignment variant (WSM, KM, FKM): a single kernel
+// with a runtime switch cost the WSM loop ~1.5% (register allocation).
+template <Assign Mode>
 __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
+  constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
   __shared__ LoopSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
   cg::grid_group grid = cg::this_grid();
@@ -828,11 +838,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     L.block_times[7 * gridDim.x + blockIdx.x] = 0ull;
   }
   // prologue: tables of the initial centers (all pairs evaluated: non-incremental)
-  if (!L.naive) tables_all(S, st, k, false);
+  if (!kNaive) tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
   unsigned long long pair_evals =
-      (L.naive || L.fkm_kprime > 0) ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+      (kNaive || kFkm) ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
   grid.sync();
 
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
@@ -850,18 +860,18 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       }
       __syncthreads();
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
-      assign_dense_first(S, L, lo, hi, evals);
+      if constexpr (Mode == Assign::SortMeans) {
+        assign_dense_first(S, L, lo, hi, evals);
+      } else {  // KM / FKM: the host accounts P*k for iteration 1
+        unsigned long long ev_dense = 0;
+        assign_dense_first(S, L, lo, hi, ev_dense);
+      }
     } else {
       __syncthreads();
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      if (L.naive)
-        assign_sort_means<Assign::Naive>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
-      else if (L.fkm_kprime > 0)
-        assign_sort_means<Assign::Fkm>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
-      else
-        assign_sort_means<Assign::SortMeans>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      assign_sort_means<Mode>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -957,9 +967,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         if (!stop) {
           const unsigned long long still = (unsigned long long)(k - moved);
           // FKM builds its first tables for iteration 2 (fast_variants.hpp:42): all pairs
-          if (L.fkm_kprime > 0 && it == 1)
+          if (kFkm && it == 1)
             pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2;
-          else if (!L.naive)
+          else if (!kNaive)
             pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
         }
       }
@@ -987,7 +997,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     __syncthreads();
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
-    if (!L.naive) tables_all(S, st, k, true);  // wasted work on the final iteration only
+    if (!kNaive) tables_all(S, st, k, true);  // wasted work on the final iteration only
     if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
     BLOCK_STAMP(5);
     grid.sync();
