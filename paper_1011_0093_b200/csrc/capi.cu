@@ -301,19 +301,27 @@ int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
 // (their tables are sparse: cfg2's 0.37M colors touch 2% of the bins).
 constexpr uint64_t OCC_MAX_PIXELS = 2u << 20;
 
+bool sparse_path(const cqb_ctx* ctx, uint64_t P) { return P < OCC_MAX_PIXELS && !(ctx->debug_flags & 16); }
+bool fused_prep(const cqb_ctx* ctx, uint64_t P) {
+  return sparse_path(ctx, P) && ctx->prep_blocks > 0 && !(ctx->debug_flags & 32);
+}
+
+// zero_state (quantize path): the fused small-image kernel also zeroes the
+// bitmap, the moment sums and the run scalars, replacing four host memsets.
 int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamps = false,
-                      bool rank_order = false, int init_k = 0, int ndraws = 0) {
+                      bool rank_order = false, int init_k = 0, int ndraws = 0, bool zero_state = false) {
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
   const uint32_t n_words = (uint32_t)((P + 31) / 32);
   const uint32_t ntiles = (n_words + BS_WORDS - 1) / BS_WORDS;
-  CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
-  CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
+  const bool fused = fused_prep(ctx, P);
+  if (!(fused && zero_state)) CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
+  if (!fused) CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
   const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
   // Sparse tables (small images) are compacted through the occupancy map;
   // dense ones by scanning all 128 MiB (k_bins_compact), whose K1 runs in
   // 4 Morton slices so each pass's atomics stay in L2.
-  const bool sparse = P < OCC_MAX_PIXELS && !(ctx->debug_flags & 16);
+  const bool sparse = sparse_path(ctx, P);
   const int passes = P >= (4u << 20) ? 4 : 1;
   for (int q = 0; q < passes; ++q) {
     const uint32_t span = (1u << 24) / passes;
@@ -322,7 +330,7 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     CKL();
   }
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
-  if (sparse && ctx->prep_blocks > 0 && !(ctx->debug_flags & 32)) {
+  if (fused) {
     // compaction, first-occurrence ranks and init in one cooperative launch
     if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
     PrepParams Q{};
@@ -345,6 +353,7 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     Q.r_counts = ctx->d_counts;
     Q.r_first = ctx->d_first;
     Q.stamps = ctx->profiling ? ctx->d_block_times + 14 * MAXBLK : nullptr;
+    Q.zero_state = zero_state ? 1 : 0;
     void* args[] = {&Q};
     CK(cudaLaunchCooperativeKernel((const void*)k_prep_small, dim3(std::min(ctx->prep_blocks, MAXBLK)),
                                    dim3(PREP_THREADS), args, 0, ctx->stream));
@@ -475,8 +484,9 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   TRY(upload_draws(ctx, seed, ndraws));
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   PROF(0);
-  TRY(reset_state(ctx));
-  TRY(enqueue_histogram(ctx, d_img, P, true, false, k, ndraws));  // records PROF(1..3)
+  const bool fused = fused_prep(ctx, P);
+  if (!fused) TRY(reset_state(ctx));  // else zeroed inside k_prep_small
+  TRY(enqueue_histogram(ctx, d_img, P, true, false, k, ndraws, fused));  // records PROF(1..3)
   PROF(4);
   TRY(launch_loop(ctx, k, term, 1, P, nullptr, 0));
   CK(cudaEventRecord(ctx->ev[1], ctx->stream));

@@ -15,12 +15,16 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <cstddef>
+
 #include "hist.cuh"
 #include "wsm.cuh"
 
 namespace cqb {
 
 constexpr int PREP_THREADS = 1024;
+// zero_state clears exactly these run scalars; keep in sync with WsmState
+static_assert(sizeof(WsmState) - offsetof(WsmState, evals) == 40, "WsmState run scalars changed");
 
 struct PrepParams {
   uint32_t* occ;            // 2^19 words
@@ -42,6 +46,7 @@ struct PrepParams {
   uint32_t* r_counts;
   uint32_t* r_first;
   unsigned long long* stamps;  // profiling: globaltimer at each phase boundary (block 0)
+  int zero_state;              // also zero the bitmap, the moment sums and the run scalars (no host memsets)
 };
 
 __device__ __forceinline__ void prep_stamp(const PrepParams& Q, int i) {
@@ -98,6 +103,21 @@ __global__ void __launch_bounds__(PREP_THREADS, 1) k_prep_small(PrepParams Q) {
   const uint32_t wt0 = min(wb0 + tid * wpt, wb1), wt1 = min(wt0 + wpt, wb1);
   uint32_t cnt = 0;
   for (uint32_t w = wt0; w < wt1; ++w) cnt += __popc(Q.occ[w]);
+  if (Q.zero_state) {  // replaces the host memsets of the quantize path
+    for (uint32_t w = b * PREP_THREADS + tid; w < Q.n_words; w += G * PREP_THREADS) Q.bitmap[w] = 0u;
+    if (b == 0) {
+      for (int i = tid; i < 5 * KMAX; i += PREP_THREADS) Q.st->acc[i] = 0ull;
+      if (tid == 0) {
+        Q.st->evals = 0ull;
+        Q.st->mse_err = 0ull;
+        Q.st->sse = 0.0;
+        Q.st->iterations = 0;
+        Q.st->status = ST_OK;
+        Q.st->n_empty_events = 0;
+        Q.st->stop_it = 0;
+      }
+    }
+  }
   uint32_t btotal;
   const uint32_t tex = prep_block_scan(cnt, s_warp, &btotal);
   {
