@@ -503,14 +503,15 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
 // Assign variants: sort-means (WSM), exhaustive (KM), first k' of the row (FKM).
 enum class Assign { SortMeans, Naive, Fkm };
 
-template <Assign Mode>
+template <Assign Mode, int PPT>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
   // Lane-local scan; 32-bit indexing (N' <= 2^24). The break index J is found
   // by exponential + binary search in the sorted row (most points stop at
   // J = 1 after one comparison), then the J - 1 candidates are evaluated.
-  constexpr int PPT = 2;
+  // PPT chunks per grab (one point per lane per chunk): 2 gives ILP for large
+  // sample sets, 1 finer balance (shorter tails) for small ones.
   const uint32_t lo = (uint32_t)lo64, hi = (uint32_t)hi64;
   const int lane = threadIdx.x & 31;
   // Work split: 32-point Morton chunks dealt round-robin to the blocks
@@ -794,7 +795,7 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
 // One instantiation per assignment variant (WSM, KM, FKM): a single kernel
 // with a runtime switch cost the WSM loop ~1.5% (register allocation).
-template <Assign Mode>
+template <Assign Mode, int PPT>
 __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
   __shared__ LoopSmem S;
@@ -871,7 +872,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means<Mode>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      assign_sort_means<Mode, PPT>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
