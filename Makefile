@@ -21,7 +21,7 @@ $(SHIM_TEST): tests/cpp/shim_test.cpp include/colorq_b200/colorq.hpp include/col
 	    -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))'
 
 # The reference CLI's quantize command on the library (tools/colorq_b200_cli.cpp).
-$(CLI): tools/colorq_b200_cli.cpp include/colorq_b200/colorq.hpp include/colorq_b200/io.hpp include/colorq_b200.h $(LIB)
+$(CLI): tools/colorq_b200_cli.cpp include/colorq_b200/colorq.hpp include/colorq_b200/io.hpp include/colorq_b200/bench.hpp include/colorq_b200.h $(LIB)
 	mkdir -p build
 	g++ -O2 -std=c++20 -Iinclude -o $@ tools/colorq_b200_cli.cpp -L$(dir $(LIB)) -lcolorq_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))'

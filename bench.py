@@ -463,9 +463,18 @@ def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
         traffic_alg = 8.0 * n_unique
         note = "8 B per unique color"
     achieved = traffic_alg / (ms * 1e-3) / 1e9
-    return {"kernel": stage, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": _ncu_traffic(stage, P), "kernel_ms": ms,
-            "algorithmic_bytes": traffic_alg, "peak_source": peaks["source"], "note": note}
+    out = {"kernel": stage, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+           "frac": achieved / peaks["hbm_gbs"], "traffic": _ncu_traffic(stage, P), "kernel_ms": ms,
+           "algorithmic_bytes": traffic_alg, "peak_source": peaks["source"], "note": note}
+    if stage == "wsm_loop" and evals:
+        # BASELINE's second metric: point-center evaluations/s against the FP64
+        # issue roofline (8 FP64 ops per evaluation, no FMA; DADD/DMUL peak
+        # measured by tools/microbench.cu: 62.4 ops/SM/clk -> profiles/r01/microbench_primitives.txt)
+        fp64_ops = 18.16e12
+        out["evals_roofline"] = {"achieved_evals_per_s": evals / (ms * 1e-3), "peak_evals_per_s": fp64_ops / 8,
+                                 "frac": evals / (ms * 1e-3) / (fp64_ops / 8),
+                                 "peak_source": "measured DADD/DMUL throughput / 8 ops per evaluation"}
+    return out
 
 
 def _ncu_traffic(stage, P):

@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -101,6 +102,18 @@ struct RunReport {
   double elapsed_ms = 0.0;
   std::uint64_t dist_evals = 0;
   std::vector<double> sse_history;
+
+  // report.hpp:44-52: the runs CSV columns (6 significant digits for reals)
+  static std::string csv_header() { return "method,k,seed,iterations,sse,mse,elapsed_ms,dist_evals"; }
+  std::string csv_row() const {
+    auto g6 = [](double v) {
+      char b[40];
+      std::snprintf(b, sizeof b, "%.6g", v);
+      return std::string(b);
+    };
+    return method + "," + std::to_string(k) + "," + std::to_string(seed) + "," + std::to_string(iterations) + "," +
+           g6(sse) + "," + g6(mse) + "," + g6(elapsed_ms) + "," + std::to_string(dist_evals);
+  }
 };
 
 struct ColorHistogram {

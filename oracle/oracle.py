@@ -123,6 +123,7 @@ class Oracle:
             f("palette_text").argtypes = [_f64p, C.c_int, C.c_char_p, C.c_int64]
             f("palette_text").restype = C.c_int64
             f("error_image").argtypes = [_u8p, _u8p, C.c_uint64, _u8p]
+            f("run_bench").argtypes = [C.c_char_p, C.c_char_p]
             f("run_fkm").argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                      C.c_uint64, _f64p, _f64p, _u64p, _f64p, C.c_int]
             f("run_km_full").argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
@@ -338,6 +339,12 @@ class Oracle:
             raise ValueError("run_fkm failed")
         return dict(centers=C_out.reshape(k, 3), iterations=int(it), sse=float(sse[0]), dist_evals=int(ev[0]),
                     sse_history=hist[:it].copy())
+
+    def run_bench(self, config_text: str, prefix: str) -> None:
+        """run_bench + write_bench_outputs (bench.hpp:160-313), single thread."""
+        assert self.kind == "reference"
+        if self._f("run_bench")(config_text.encode(), prefix.encode()) != 0:
+            raise ValueError("run_bench failed")
 
     def error_image(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
         assert self.kind == "reference"

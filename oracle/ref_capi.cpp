@@ -15,9 +15,11 @@
 #include <cstring>
 #include <exception>
 #include <random>
+#include <sstream>
 #include <thread>
 #include <vector>
 
+#include "colorq/bench.hpp"
 #include "colorq/histogram.hpp"
 #include "colorq/image_ops.hpp"
 #include "colorq/kmeans.hpp"
@@ -281,6 +283,22 @@ int ref_run_fkm(const std::uint8_t* rgb, int w, int h, int k, int k_prime, int m
     *evals = r.report.dist_evals;
     for (int i = 0; i < std::min<int>(hist_cap, int(r.report.sse_history.size())); ++i) hist[i] = r.report.sse_history[i];
     return r.report.iterations;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// run_bench + write_bench_outputs (bench.hpp:160-313), §8(f) row f2: the
+// config text as the CLI reads it; single-threaded. 0 ok, -1 error.
+int ref_run_bench(const char* config_text, const char* prefix) {
+  try {
+    BenchConfig cfg;
+    std::istringstream in(config_text);
+    apply_config_text(cfg, in);
+    cfg.output_prefix = prefix;
+    cfg.threads = 1;
+    write_bench_outputs(run_bench(cfg), cfg.output_prefix);
+    return 0;
   } catch (const std::exception&) {
     return -1;
   }

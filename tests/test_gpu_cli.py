@@ -89,3 +89,51 @@ def test_error_image_api(ref):
     np.testing.assert_array_equal(api.error_image(a, b), ref.error_image(a, b))
     q = api.quantize(a, 8, api.Termination.convergent(1e-4, 100), seed=1, error=True)
     np.testing.assert_array_equal(q.error, ref.error_image(a, q.mapped))
+
+
+def _csv(path):
+    lines = open(path).read().strip().splitlines()
+    return [ln.split(",") for ln in lines]
+
+
+def test_cli_bench_matches_reference_harness(ref, tmp_path):
+    """`colorq_b200 bench` against the reference's
+    run_bench on the same config: the runs, summary and ranks CSVs agree in
+    every column except the wall-time ones (elapsed_ms, time_mean_ms,
+    time_rank, mean_rank)."""
+    paths = []
+    for i, (w, h) in enumerate([(64, 32), (32, 32)]):  # powers of two: bit-exact centers
+        p = tmp_path / f"img{i}.ppm"
+        p.write_bytes(ref.write_ppm(gmm_image(w, h, 12, 40 + i)))
+        paths.append(str(p))
+    # bench.hpp:106-139: key=value (no blanks around '='), list items trimmed
+    cfg = (f"# grid\nimages={paths[0]}, {paths[1]}\n"
+           "methods=wsm, wsm-c, km(iters=5), fkm(k_prime=4)\n"
+           "k_values=4, 8\nruns=2\nbase_seed=7\n")
+    ours, theirs = str(tmp_path / "ours"), str(tmp_path / "ref")
+    conf = tmp_path / "bench.conf"
+    conf.write_text(cfg + f"output={ours}\n")
+    r = _run(["bench", "-c", str(conf), "--threads", "2"])
+    assert r.returncode == 0, r.stderr
+    ref.run_bench(cfg, theirs)
+    skip = {"_runs.csv": {"elapsed_ms"}, "_summary.csv": {"time_mean_ms"}, "_ranks.csv": {"time_rank", "mean_rank"}}
+    for suffix, drop in skip.items():
+        a, b = _csv(ours + suffix), _csv(theirs + suffix)
+        assert a[0] == b[0] and len(a) == len(b)
+        keep = [j for j, name in enumerate(a[0]) if name not in drop]
+        for ra, rb in zip(a[1:], b[1:]):
+            assert [ra[j] for j in keep] == [rb[j] for j in keep], (suffix, ra, rb)
+
+
+def test_cli_scaling_dist_evals(ref, tmp_path):
+    img = gmm_image(64, 32, 12, 44)
+    src = tmp_path / "s.ppm"
+    src.write_bytes(ref.write_ppm(img))
+    r = _run(["scaling", str(src), "-m", "wsm-c", "--k-values", "2,4,8,16"])
+    assert r.returncode == 0, r.stderr
+    rows = [ln.split(",") for ln in r.stdout.strip().splitlines()]
+    assert rows[0] == ["k", "elapsed_ms", "dist_evals"]
+    for row in rows[1:]:
+        k = int(row[0])
+        q = ref.quantize(img, k, mode=1, max_iters=10, eps=1e-4, cap=1000, seed=1)
+        assert int(row[2]) == q["dist_evals"]

@@ -5,6 +5,12 @@
 //   colorq_b200 quantize INPUT.ppm -o OUT.ppm [-m wsm|wsm-c] [-k K] [-s SEED]
 //               [--palette P.txt] [--error-image E.ppm] [--dump-histogram H.csv]
 //               [--iters N] [--epsilon E]
+//   colorq_b200 bench [-c CONFIG] [--images A,B] [--methods M1,M2] [--k-values K1,K2]
+//               [--runs N] [--base-seed S] [--output PREFIX] [--threads T] [--serial-timing]
+//   colorq_b200 scaling INPUT.ppm [-m METHOD] [--k-values K1,K2] [-s SEED] [-o OUT.csv]
+//
+// bench / scaling are tools/colorq.cpp:121-200 over include/colorq_b200/bench.hpp
+// (SURVEY.md §8(f) row f2).
 //
 // Exit codes follow the reference (tools/colorq.cpp:21-43): 2 I/O or PPM
 // error, 3 unknown / unsupported method, 4 invalid parameters. The WSM, KM and
@@ -18,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "colorq_b200/bench.hpp"
 #include "colorq_b200/colorq.hpp"
 #include "colorq_b200/io.hpp"
 
@@ -35,7 +42,10 @@ int usage(const char* msg) {
   std::cerr << "error: " << msg << "\n"
             << "usage: colorq_b200 quantize INPUT.ppm -o OUT.ppm [-m wsm|wsm-c] [-k K] [-s SEED]\n"
             << "                   [--palette P.txt] [--error-image E.ppm] [--dump-histogram H.csv]\n"
-            << "                   [--iters N] [--epsilon E]\n";
+            << "                   [--iters N] [--epsilon E]\n"
+            << "       colorq_b200 bench [-c CONFIG] [--images ...] [--methods ...] [--k-values ...] [--runs N]\n"
+            << "                   [--base-seed S] [--output PREFIX] [--threads T] [--serial-timing]\n"
+            << "       colorq_b200 scaling INPUT.ppm [-m METHOD] [--k-values ...] [-s SEED] [-o OUT.csv]\n";
   return 1;
 }
 
@@ -130,10 +140,123 @@ int quantize(const Args& a) {
   });
 }
 
+int env_threads() {
+  if (const char* v = std::getenv("COLORQ_THREADS")) {
+    const int n = std::atoi(v);
+    if (n >= 1) return n;
+  }
+  return 1;
+}
+
+std::vector<int> parse_k_list(const std::string& s) {
+  std::vector<int> ks;
+  for (const std::string& t : colorq::benchdetail::split_list(s)) ks.push_back(std::stoi(t));
+  if (ks.empty()) throw std::invalid_argument("empty K list");
+  return ks;
+}
+
+int bench_main(int argc, char** argv) {
+  std::string config, images, methods, ks, output;
+  int runs = -1, threads = -1;
+  long long base_seed = -1;
+  bool serial = false;
+  try {
+    for (int i = 2; i < argc; ++i) {
+      const std::string s = argv[i];
+      auto value = [&](const char* name) -> std::string {
+        if (i + 1 >= argc) throw UsageError(std::string("missing value for ") + name);
+        return argv[++i];
+      };
+      if (s == "-c" || s == "--config") config = value("--config");
+      else if (s == "--images") images = value("--images");
+      else if (s == "--methods") methods = value("--methods");
+      else if (s == "--k-values") ks = value("--k-values");
+      else if (s == "--runs") runs = std::stoi(value("--runs"));
+      else if (s == "--base-seed") base_seed = std::stoll(value("--base-seed"));
+      else if (s == "--output") output = value("--output");
+      else if (s == "--threads") threads = std::stoi(value("--threads"));
+      else if (s == "--serial-timing") serial = true;
+      else throw UsageError("unknown option " + s);
+    }
+  } catch (const std::exception& e) {
+    return usage(e.what());
+  }
+  return guarded([&]() {
+    colorq::BenchConfig cfg;
+    cfg.threads = env_threads();
+    if (!config.empty()) {
+      std::ifstream in(config);
+      if (!in) throw std::runtime_error("cannot open config file " + config);
+      colorq::apply_config_text(cfg, in);
+    }
+    if (!images.empty()) cfg.images = colorq::benchdetail::split_list(images);
+    if (!methods.empty()) {
+      cfg.methods.clear();
+      for (const std::string& t : colorq::benchdetail::split_list(methods))
+        cfg.methods.push_back(colorq::parse_method_spec(t));
+    }
+    if (!ks.empty()) cfg.k_values = parse_k_list(ks);
+    if (runs > 0) cfg.runs = runs;
+    if (base_seed >= 0) cfg.base_seed = std::uint64_t(base_seed);
+    if (!output.empty()) cfg.output_prefix = output;
+    if (threads > 0) cfg.threads = threads;
+    cfg.serial_timing = serial;
+    const colorq::BenchResults res = colorq::run_bench(cfg);
+    for (const auto& p : colorq::write_bench_outputs(res, cfg.output_prefix)) std::cout << "wrote " << p.string() << "\n";
+    std::cout << res.ranks_csv;
+    return 0;
+  });
+}
+
+int scaling_main(int argc, char** argv) {
+  std::string input, method = "wsm-c", ks = "2,4,8,16,32,64,128,256", output;
+  std::uint64_t seed = 1;
+  try {
+    for (int i = 2; i < argc; ++i) {
+      const std::string s = argv[i];
+      auto value = [&](const char* name) -> std::string {
+        if (i + 1 >= argc) throw UsageError(std::string("missing value for ") + name);
+        return argv[++i];
+      };
+      if (s == "-m" || s == "--method") method = value("--method");
+      else if (s == "--k-values") ks = value("--k-values");
+      else if (s == "-s" || s == "--seed") seed = std::stoull(value("--seed"));
+      else if (s == "-o" || s == "--output") output = value("--output");
+      else if (!s.empty() && s[0] == '-') throw UsageError("unknown option " + s);
+      else if (input.empty()) input = s;
+      else throw UsageError("unexpected argument " + s);
+    }
+  } catch (const std::exception& e) {
+    return usage(e.what());
+  }
+  if (input.empty()) return usage("missing INPUT");
+  return guarded([&]() {
+    const colorq::MethodSpec spec = colorq::parse_method_spec(method);
+    const std::vector<int> kv = parse_k_list(ks);
+    const colorq::RgbImage image = colorq::load_ppm(input);
+    std::string csv = "k,elapsed_ms,dist_evals\n";
+    for (const int k : kv) {
+      const colorq::QuantizeOutcome q = colorq::generate_palette(image, spec.params, k, seed);
+      csv += std::to_string(k) + "," + colorq::fmt_g6(q.report.elapsed_ms) + "," + std::to_string(q.report.dist_evals) +
+             "\n";
+    }
+    if (output.empty()) {
+      std::cout << csv;
+    } else {
+      std::ofstream out(output);
+      if (!out) throw std::runtime_error("cannot open " + output + " for writing");
+      out << csv;
+    }
+    return 0;
+  });
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc < 2 || std::strcmp(argv[1], "quantize") != 0) return usage("expected the 'quantize' subcommand");
+  if (argc >= 2 && std::strcmp(argv[1], "bench") == 0) return bench_main(argc, argv);
+  if (argc >= 2 && std::strcmp(argv[1], "scaling") == 0) return scaling_main(argc, argv);
+  if (argc < 2 || std::strcmp(argv[1], "quantize") != 0) return usage("expected a subcommand: quantize, bench, scaling");
   Args a;
   bool have_out = false;
   try {
