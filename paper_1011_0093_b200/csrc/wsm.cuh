@@ -306,7 +306,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
     // rank-count sort.
     int rounds = 0;
     bool again = true;
-    while (again && rounds < 16) {
+    while (again && rounds < 32) {
       int swapped = 0;
 #pragma unroll
       for (int ph = 0; ph < 2; ++ph) {
