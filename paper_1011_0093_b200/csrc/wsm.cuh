@@ -895,26 +895,21 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
 
     // ---------------- finalize(it) ----------------
     // Every block: new centers S/N (FP64, exact integer inputs) + empty count.
-    // k <= KMAX <= blockDim: thread t owns cluster t. The five sums are
-    // loaded unconditionally up front (one L2 round trip, not one per
-    // division) and kept in registers for block 0's SSE below.
-    unsigned long long mS0 = 0, mS1 = 0, mS2 = 0, mN = 0, mQ = 0;
-    if (tid < k) {
-      mS0 = __ldcg(&gacc[0 * KMAX + tid]);
-      mS1 = __ldcg(&gacc[1 * KMAX + tid]);
-      mS2 = __ldcg(&gacc[2 * KMAX + tid]);
-      mN = __ldcg(&gacc[3 * KMAX + tid]);
-      if (blockIdx.x == 0) mQ = __ldcg(&gacc[4 * KMAX + tid]);
-    }
+    // One division per thread: unit u = (channel, cluster) over 3*KMAX units
+    // (one unit per thread at 1024 threads), each loading its sum and N in one
+    // L2 round trip.
     int empt_local = 0;
-    if (tid < k) {
-      if (mN) {
-        const double dn = (double)mN;
-        S.nx[tid] = (double)mS0 / dn;
-        S.ny[tid] = (double)mS1 / dn;
-        S.nz[tid] = (double)mS2 / dn;
-      } else {
-        empt_local = 1;
+    for (int u = tid; u < 3 * KMAX; u += blockDim.x) {
+      const int ch = u / KMAX, t = u % KMAX;
+      if (t < k) {
+        const unsigned long long N = __ldcg(&gacc[3 * KMAX + t]);
+        const unsigned long long Sv = __ldcg(&gacc[ch * KMAX + t]);
+        if (N) {
+          double* dst = ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz);
+          dst[t] = (double)Sv / (double)N;
+        } else if (ch == 0) {
+          empt_local = 1;
+        }
       }
     }
     const int empt = __syncthreads_count(empt_local);  // k <= blockDim: one cluster per thread
@@ -936,6 +931,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (tid < k) {
         const int t = tid;
         moved += (S.nx[t] != S.cx[t]) | (S.ny[t] != S.cy[t]) | (S.nz[t] != S.cz[t]);
+        const unsigned long long mN = __ldcg(&gacc[3 * KMAX + t]);
+        const unsigned long long mS0 = __ldcg(&gacc[0 * KMAX + t]), mS1 = __ldcg(&gacc[1 * KMAX + t]);
+        const unsigned long long mS2 = __ldcg(&gacc[2 * KMAX + t]), mQ = __ldcg(&gacc[4 * KMAX + t]);
         if (mN) {
           const double dn = (double)mN;
           const double Sr = (double)mS0, Sg = (double)mS1;
