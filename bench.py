@@ -49,7 +49,7 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--k", type=int, default=256)
+    ap.add_argument("--k", type=int, default=None, help="default: 256 if the config lists it, else its K")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     return ap.parse_args()
@@ -144,7 +144,8 @@ def run_reference(a, cfg, world, rank):
     cores = _host_cores()
     img = cfg.image()
     P = cfg.pixels
-    imgs = [img] * cores
+    # one image per worker thread (bench.hpp:187-223); config 5's images are distinct
+    imgs = [cfg.image(i) for i in range(cores)] if cfg.images > 1 else [img] * cores
     for _ in range(a.warmup):
         ref.quantize_many(imgs, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
     walls = []
@@ -504,12 +505,100 @@ def _hbm_stages(stage_ms, P, n_unique, peaks):
     return out
 
 
+def run_batch(a, cfg, world, rank, local):
+    """--config cfg5: one step = the batch of cfg.images independent images
+    per rank (replicas), `lanes` images in flight per GPU (cqb_quantize_batch).
+    value = aggregate Mpixel/s over all ranks; e2e adds the H2D copies of the
+    batch (pinned) and the D2H of the index maps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200 import _native as N
+    from paper_1011_0093_b200 import api
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = N.context(local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.check(ctx.lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
+    n = cfg.images
+    host = [torch.from_numpy(cfg.image(i + rank * n).reshape(-1)).pin_memory() for i in range(n)]
+    imgs = [h.to(dev) for h in host]
+    idx = [torch.empty(cfg.pixels, dtype=torch.uint8, device=dev) for _ in range(n)]
+    idx_h = [torch.empty(cfg.pixels, dtype=torch.uint8).pin_memory() for _ in range(n)]
+    term = api.Termination.convergent(EPSILON, HARD_CAP)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lanes = 4
+    with torch.cuda.stream(stream):
+        for _ in range(a.warmup):
+            api.quantize_batch_device(imgs, a.k, term, INIT_SEED, lanes=lanes, index_out=idx)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        tot = 0.0
+        for _ in range(a.steps):
+            flush_buf.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, reps = api.quantize_batch_device(imgs, a.k, term, INIT_SEED, lanes=lanes, index_out=idx)
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        clk = clocks.stop()
+        # e2e: pinned host images -> device, batch, index maps -> host, all timed
+        e2e = 0.0
+        for _ in range(a.steps):
+            flush_buf.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for h, d in zip(host, imgs):
+                d.copy_(h, non_blocking=True)
+            _, reps = api.quantize_batch_device(imgs, a.k, term, INIT_SEED, lanes=lanes, index_out=idx)
+            for h, d in zip(idx_h, idx):
+                h.copy_(d, non_blocking=True)
+            torch.cuda.synchronize()
+            e2e += time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([tot, e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot, e2e = float(t[0].item()), float(t[1].item())
+    px = cfg.pixels * n * world * a.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": px / (tot * 1e-3) / 1e6, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": tot / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {n} x {cfg.width}x{cfg.height} GMM-256 images per rank "
+                                   f"(seeds 1000+i), K={a.k}, convergent(eps={EPSILON}, cap={HARD_CAP})",
+                       "images_per_step_per_rank": n, "lanes": lanes, "parallelism": f"replicas x{world}",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "iterations_first8": [r.iterations for r in reps[:8]]},
+            "e2e": {"value": px / e2e / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": 3 * cfg.pixels * n,
+                    "d2h_bytes_per_step": cfg.pixels * n + n * (8 * 3 * a.k + 64),
+                    "path": "pinned H2D of the batch + cqb_quantize_batch + D2H of the index maps, wall clock"},
+            "gpu_launches": a.steps * n * int(reps[0].gpu_launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = _args()
     world, rank, local = _dist()
     cfg = CONFIGS[a.config]
+    if a.k is None:
+        a.k = 256 if 256 in cfg.ks else cfg.ks[0]
     if a.impl == "reference":
         run_reference(a, cfg, world, rank)
+        return
+    if cfg.images > 1:
+        run_batch(a, cfg, world, rank, local)
         return
     run_ours(a, cfg, world, rank, local)
 

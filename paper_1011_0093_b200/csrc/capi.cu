@@ -355,7 +355,9 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     Q.stamps = ctx->profiling ? ctx->d_block_times + 14 * MAXBLK : nullptr;
     Q.zero_state = zero_state ? 1 : 0;
     void* args[] = {&Q};
-    CK(cudaLaunchCooperativeKernel((const void*)k_prep_small, dim3(std::min(ctx->prep_blocks, MAXBLK)),
+    // honour the lane's SM slice (cqb_quantize_batch) like the loop kernel
+    const int pg = std::max(1, std::min(ctx->prep_blocks, ctx->grid_limit > 0 ? ctx->grid_limit : MAXBLK));
+    CK(cudaLaunchCooperativeKernel((const void*)k_prep_small, dim3(pg),
                                    dim3(PREP_THREADS), args, 0, ctx->stream));
     CKL();
     return CQB_OK;
