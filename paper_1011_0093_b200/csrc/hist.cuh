@@ -449,32 +449,31 @@ __global__ void __launch_bounds__(256) k_rank_from_bitmap(
     const uint32_t* __restrict__ m_counts, uint32_t* __restrict__ m_rank, const unsigned long long* __restrict__ n_unique,
     uint32_t* __restrict__ r_keys, uint32_t* __restrict__ r_counts, uint32_t* __restrict__ r_first,
     const uint32_t* __restrict__ chosen, const int* __restrict__ status, int k, double* __restrict__ centers) {
-  __shared__ uint32_t sr[256];
-  __shared__ uint32_t si[256];
-  __shared__ uint32_t sc[256];
+  // the K chosen ranks in a 1024-slot open-addressing table (load <= 1/4):
+  // ~1 shared load per sample instead of a binary search
+  constexpr uint32_t HS = 1024, EMPTY = 0xFFFFFFFFu;
+  __shared__ uint32_t hk[HS];
+  __shared__ uint32_t hv[HS];
+  auto slot0 = [](uint32_t r) { return (r * 2654435761u) >> 22; };
   const uint32_t n = (uint32_t)*n_unique;
   const bool do_gather = chosen && *status == 0 && k <= 256;
-  if (do_gather) {  // sort the chosen ranks (distinct) by rank counting
+  if (do_gather) {
     const int tid = threadIdx.x;
-    const uint32_t r0 = tid < k ? chosen[tid] : 0u;
-    if (tid < k) sc[tid] = r0;
+    for (uint32_t h = tid; h < HS; h += blockDim.x) hk[h] = EMPTY;
     __syncthreads();
-    if (tid < k) {
-      int pos = 0;
-      for (int u = 0; u < k; ++u) pos += sc[u] < r0;
-      sr[pos] = r0;
-      si[pos] = (uint32_t)tid;
+    if (tid < k) {  // chosen ranks are distinct
+      const uint32_t r0 = chosen[tid];
+      uint32_t h = slot0(r0);
+      while (atomicCAS(&hk[h], EMPTY, r0) != EMPTY) h = (h + 1) & (HS - 1);
+      hv[h] = (uint32_t)tid;
     }
     __syncthreads();
     rank_pass(bitmap, pre, m_keys, m_counts, m_rank, n, r_keys, r_counts, r_first, [&](uint32_t r, uint32_t s) {
-      int lo = 0, hi = k;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sr[mid] < r) lo = mid + 1;
-        else hi = mid;
-      }
-      if (lo < k && sr[lo] == r) {
-        const int i = (int)si[lo];
+      uint32_t h = slot0(r);
+      uint32_t v;
+      while ((v = hk[h]) != r && v != EMPTY) h = (h + 1) & (HS - 1);
+      if (v == r) {
+        const int i = (int)hv[h];
         const uint32_t key = m_keys[s];
         centers[3 * i + 0] = (double)key_r(key);
         centers[3 * i + 1] = (double)key_g(key);
