@@ -70,6 +70,8 @@ struct cqb_ctx {
   uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output
   int naive_mode = 0;             // set only while cqb_run_km_full enqueues: exhaustive assign (KM)
   int fkm_kprime = 0;             // set only while cqb_run_fkm enqueues: FKM neighbour count
+  uint8_t* d_cand = nullptr;      // iteration-1 candidate centers per 16^3 color cell
+  uint16_t* d_cand_n = nullptr;
   uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
   uint8_t* d_labels = nullptr;    // Morton layout (loop + map)
   uint8_t* d_lab_rank = nullptr;  // first-occurrence layout (API in/out)
@@ -415,6 +417,12 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.stamp_iter = ctx->stamp_iter;
   L.debug_flags = ctx->debug_flags;
   L.naive = ctx->naive_mode;
+  if (dense_first && !(ctx->debug_flags & 128)) {  // iteration 1 on per-cell candidate lists
+    k_grid_cands<<<CAND_CELLS, KMAX, 0, ctx->stream>>>(ctx->st, k, ctx->d_cand, ctx->d_cand_n);
+    CKL();
+    L.cand = ctx->d_cand;
+    L.cand_n = ctx->d_cand_n;
+  }
   L.fkm_kprime = ctx->fkm_kprime;
   if (ctx->profiling)
     CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
@@ -555,6 +563,8 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMemset(ctx->bins, 0, sizeof(uint2) << 24));
     CK(cudaMalloc(&ctx->d_occ, sizeof(uint32_t) << 19));
     CK(cudaMalloc(&ctx->d_block_counts, sizeof(uint32_t) * 2 * MAXBLK));
+    CK(cudaMalloc(&ctx->d_cand, (size_t)CAND_CELLS * CAND_CAP));
+    CK(cudaMalloc(&ctx->d_cand_n, sizeof(uint16_t) * CAND_CELLS));
     CK(cudaMalloc(&ctx->d_wofs, sizeof(uint32_t) << 19));
     int pb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_prep_small, PREP_THREADS, 0));
@@ -603,7 +613,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->d_err, ctx->tile_state,
-                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_block_counts, ctx->d_wofs, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_block_counts, ctx->d_wofs, ctx->d_cand, ctx->d_cand_n, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,

@@ -80,6 +80,8 @@ struct LoopParams {
   int moments_only;  // sharded step: stop after assign + flush (global sums = this shard's moments)
   int naive;         // run_km_full (kmeans.hpp:409-426): exhaustive assign, no center tables
   int fkm_kprime;    // run_fkm (fast_variants.hpp:20-81): search the k' nearest centers of the previous one
+  const uint8_t* cand;     // iteration 1: per 16^3 color cell, the centers that can be nearest (null: dense)
+  const uint16_t* cand_n;  // per cell: count, or CAND_OVERFLOW
   int debug_flags;   // diagnostics only (tools/ablate.py): 1 = skip the candidate scan (results wrong)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
   int stamp_iter;
@@ -431,6 +433,62 @@ __device__ __forceinline__ void acc_point_warp(uint2* acc, bool valid, int lab, 
   }
 }
 
+// Iteration 1 candidates. The RGB cube is cut into 16^3 cells of 16^3
+// colors. For a cell, c_t can be the nearest center of some color in it only
+// if mindist2(cell, c_t) <= min_u maxdist2(cell, c_u): any color x in the
+// cell has d(x, nearest) <= maxdist2(cell, c_u) for every u, and d(x, c_t) >=
+// mindist2(cell, c_t). The test is non-strict, so ties stay in, and it is
+// integer arithmetic on integer centers: the candidate list always contains
+// the lexicographic (d, index) minimum. One block per cell, one thread per
+// center; a cell with more than CAND_CAP candidates falls back to all k.
+constexpr int CAND_CELLS = 16 * 16 * 16;
+constexpr int CAND_CAP = 64;
+constexpr uint16_t CAND_OVERFLOW = 0xFFFF;
+
+__global__ void __launch_bounds__(KMAX) k_grid_cands(const WsmState* __restrict__ st, int k,
+                                                     uint8_t* __restrict__ cand, uint16_t* __restrict__ cand_n) {
+  __shared__ int s_min[KMAX / 32];
+  __shared__ int s_cnt[KMAX / 32];
+  const int cell = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  if (st->status != ST_OK) return;
+  const int lo[3] = {(cell >> 8) * 16, ((cell >> 4) & 15) * 16, (cell & 15) * 16};
+  int mind2 = 0, maxd2 = 0x7fffffff;
+  if (t < k) {
+    maxd2 = 0;
+    for (int ch = 0; ch < 3; ++ch) {
+      const int c = (int)st->C[0][3 * t + ch];  // initial centers are sample colors: integers
+      const int a = lo[ch], b = lo[ch] + 15;
+      const int below = a - c, above = c - b;
+      const int dn = below > 0 ? below : (above > 0 ? above : 0);
+      const int fa = c - a, fb = b - c;
+      const int far = max(fa < 0 ? -fa : fa, fb < 0 ? -fb : fb);
+      mind2 += dn * dn;
+      maxd2 += far * far;
+    }
+  }
+  int m = maxd2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) s_min[wid] = m;
+  __syncthreads();
+  int bound = s_min[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) bound = min(bound, s_min[w]);
+  const bool c_in = t < k && mind2 <= bound;
+  const unsigned bal = __ballot_sync(0xffffffffu, c_in);
+  if (lane == 0) s_cnt[wid] = __popc(bal);
+  __syncthreads();
+  int before = 0, total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (w < wid) before += s_cnt[w];
+    total += s_cnt[w];
+  }
+  if (c_in) {
+    const int pos = before + __popc(bal & ((1u << lane) - 1u));
+    if (pos < CAND_CAP) cand[cell * CAND_CAP + pos] = (uint8_t)t;
+  }
+  if (t == 0) cand_n[cell] = total > CAND_CAP ? CAND_OVERFLOW : (uint16_t)total;
+}
+
 // Iteration 1, dense + integer-exact (see header). Full accumulation.
 __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned long long lo, unsigned long long hi,
                                    unsigned long long& evals) {
@@ -451,10 +509,31 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
       x[q] = i < bhi ? L.keys[i] : 0u;
       best[q] = 0x7fffffff;
     }
-    for (int t = 0; t < k; ++t) {
-      const int2 cb = S.cb[t];
+    if (L.cand) {  // only the cell's candidate centers (k_grid_cands)
 #pragma unroll
-      for (int q = 0; q < PPT; ++q) best[q] = min(best[q], cb.y - 512 * key_dot(x[q], (uint32_t)cb.x));
+      for (int q = 0; q < PPT; ++q) {
+        const uint32_t xk = x[q];
+        const int cell = (int)(((xk >> 20) & 15) << 8 | ((xk >> 12) & 15) << 4 | ((xk >> 4) & 15));
+        const int nc = L.cand_n[cell];
+        if (nc == CAND_OVERFLOW) {
+          for (int t = 0; t < k; ++t) {
+            const int2 cb = S.cb[t];
+            best[q] = min(best[q], cb.y - 512 * key_dot(xk, (uint32_t)cb.x));
+          }
+        } else {
+          const uint8_t* cl = L.cand + cell * CAND_CAP;
+          for (int c = 0; c < nc; ++c) {
+            const int2 cb = S.cb[cl[c]];
+            best[q] = min(best[q], cb.y - 512 * key_dot(xk, (uint32_t)cb.x));
+          }
+        }
+      }
+    } else {
+      for (int t = 0; t < k; ++t) {
+        const int2 cb = S.cb[t];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) best[q] = min(best[q], cb.y - 512 * key_dot(x[q], (uint32_t)cb.x));
+      }
     }
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
