@@ -69,6 +69,7 @@ struct cqb_ctx {
   uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
   uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output
   int naive_mode = 0;             // set only while cqb_run_km_full enqueues: exhaustive assign (KM)
+  bool fuse_map = false;          // set only while enqueue_quantize launches the loop: map epilogue
   int fkm_kprime = 0;             // set only while cqb_run_fkm enqueues: FKM neighbour count
   uint8_t* d_cand = nullptr;      // iteration-1 candidate centers per 16^3 color cell
   uint16_t* d_cand_n = nullptr;
@@ -417,6 +418,12 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.stamp_iter = ctx->stamp_iter;
   L.debug_flags = ctx->debug_flags;
   L.naive = ctx->naive_mode;
+  if (ctx->fuse_map && !(ctx->debug_flags & 256)) {
+    L.map_sortedDr = ctx->d_sortedDr;
+    L.map_orderR = ctx->d_orderR;
+    L.map_palkey = ctx->d_palkey;
+    L.map_lut = ctx->lut;
+  }
   if (dense_first && !(ctx->debug_flags & 128)) {  // iteration 1 on per-cell candidate lists
     k_grid_cands<<<CAND_CELLS, KMAX, 0, ctx->stream>>>(ctx->st, k, ctx->d_cand, ctx->d_cand_n);
     CKL();
@@ -504,15 +511,22 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   if (!fused) TRY(reset_state(ctx));  // else zeroed inside k_prep_small
   TRY(enqueue_histogram(ctx, d_img, P, true, false, k, ndraws, fused));  // records PROF(1..3)
   PROF(4);
-  TRY(launch_loop(ctx, k, term, 1, P, nullptr, 0));
+  ctx->fuse_map = true;  // k_map_tables + k_map_unique run in the loop kernel's tail
+  const int lrc = launch_loop(ctx, k, term, 1, P, nullptr, 0);
+  const bool fused_map = !(ctx->debug_flags & 256);
+  ctx->fuse_map = false;
+  TRY(lrc);
   CK(cudaEventRecord(ctx->ev[1], ctx->stream));
   PROF(5);
-  k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->st->final_C, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
-  CKL();
-  const int gu = ctx->num_sms * 4;
-  k_map_unique<<<gu, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, ctx->d_labels, ctx->d_n, k,
-                                            ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey, ctx->lut, &ctx->st->mse_err);
-  CKL();
+  if (!fused_map) {
+    k_map_tables<<<k, 256, 0, ctx->stream>>>(ctx->st->final_C, k, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey);
+    CKL();
+    const int gu = ctx->num_sms * 4;
+    k_map_unique<<<gu, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, ctx->d_labels, ctx->d_n, k,
+                                              ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey, ctx->lut,
+                                              &ctx->st->mse_err);
+    CKL();
+  }
   PROF(6);
   uint8_t* d_err_out = ctx->err_target;
   if (d_index || d_rgb_out || d_err_out) {

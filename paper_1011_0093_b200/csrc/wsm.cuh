@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "map.cuh"
 
 namespace cqb {
 
@@ -81,6 +82,11 @@ struct LoopParams {
   int naive;         // run_km_full (kmeans.hpp:409-426): exhaustive assign, no center tables
   int fkm_kprime;    // run_fkm (fast_variants.hpp:20-81): search the k' nearest centers of the previous one
   const uint8_t* cand;     // iteration 1: per 16^3 color cell, the centers that can be nearest (null: dense)
+  // map epilogue (quantize path; null lut: none): k_map_tables + k_map_unique fused into the loop's tail
+  int* map_sortedDr;
+  uint8_t* map_orderR;
+  uint32_t* map_palkey;
+  uint8_t* map_lut;
   const uint16_t* cand_n;  // per cell: count, or CAND_OVERFLOW
   int debug_flags;   // diagnostics only (tools/ablate.py): 1 = skip the candidate scan (results wrong)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
@@ -872,6 +878,8 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 }
 
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
+__device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n);
+
 // One instantiation per assignment variant (WSM, KM, FKM): a single kernel
 // with a runtime switch cost the WSM loop ~1.5% (register allocation).
 template <Assign Mode, int PPT>
@@ -1091,6 +1099,92 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     unsigned long long tot = blockIdx.x == 0 ? pair_evals : 0ull;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += S.red_u64[w];
     atomicAdd(&st->evals, tot);
+  }
+  if (L.map_lut) map_epilogue(S, L, grid, hi);
+}
+
+// ---------------------------------------------------------------------------
+// map_pixels' per-color work (image_ops.hpp:18-51) fused into the loop's tail,
+// the same computation as k_map_tables + k_map_unique (map.cuh): rounded
+// palette (lround, clamp), integer rows sorted by (d, index) - two rows per
+// block, like the center tables - then, after a grid barrier, each unique
+// color's exact argmin over the rounded palette from its final label with the
+// strict break d(R_p, R_t) > 4 prev, the key -> index LUT and the exact
+// u64 sum of count x error. Saves two launches on the quantize path.
+__device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n) {
+  const int k = L.k, tid = threadIdx.x;
+  const double* C = L.st->final_C;
+  uint32_t* s_key = S.row0;        // rounded palette keys
+  int* s_cc = S.empty_list;        // |R_t|^2
+  for (int t = tid; t < k; t += blockDim.x) {
+    const uint32_t key = (round_chan(C[3 * t]) << 16) | (round_chan(C[3 * t + 1]) << 8) | round_chan(C[3 * t + 2]);
+    s_key[t] = key;
+    s_cc[t] = key_dot(key, key);
+    if (blockIdx.x == 0) L.map_palkey[t] = key;
+  }
+  __syncthreads();
+  {  // rows: same ownership as tables_all
+    const int G = (int)gridDim.x;
+    const int first = G == 1 ? 0 : (int)blockIdx.x - 1;
+    const int stride = G == 1 ? 1 : G - 1;
+    const int r = tid >> 9, t = tid & (KMAX - 1), h = (tid >> 8) & 1;
+    for (int p0 = first; first >= 0 && p0 < k; p0 += 2 * stride) {
+      const int p = r ? (p0 + stride < k ? p0 + stride : -1) : p0;
+      if (p >= 0 && h == 0 && t < k) S.rowd[r][t] = (double)(s_cc[p] + s_cc[t] - 2 * key_dot(s_key[p], s_key[t]));
+      __syncthreads();
+      if (p >= 0 && t < k) {
+        int cnt = 0;
+        if (t != p) {
+          const double dt = S.rowd[r][t];
+          const int u0 = h * (KMAX / 2), u1 = min(k, u0 + KMAX / 2);
+          for (int u = u0; u < u1; ++u) {
+            const double du = S.rowd[r][u];
+            cnt += (u != p) & ((du < dt) | ((du == dt) & (u < t)));
+          }
+        }
+        S.rank_part[r][h][t] = cnt;
+      }
+      __syncthreads();
+      if (p >= 0 && h == 0 && t < k) {
+        const int rank = t == p ? 0 : 1 + S.rank_part[r][0][t] + S.rank_part[r][1][t];
+        L.map_sortedDr[p * KMAX + rank] = t == p ? 0 : (int)S.rowd[r][t];
+        L.map_orderR[p * KMAX + rank] = (uint8_t)t;
+      }
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  unsigned long long err = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t x = L.keys[i];
+    const int xx = key_dot(x, x);
+    const int p = L.labels[i];
+    const int prev = xx + s_cc[p] - 2 * key_dot(x, s_key[p]);
+    const int bound = 4 * prev;
+    int mind = prev, best = p;
+    const int* rowd = L.map_sortedDr + p * KMAX;
+    const uint8_t* rowo = L.map_orderR + p * KMAX;
+    for (int j = 1; j < k; ++j) {
+      if (rowd[j] > bound) break;
+      const int t = rowo[j];
+      const int d = xx + s_cc[t] - 2 * key_dot(x, s_key[t]);
+      if (d < mind || (d == mind && t < best)) {
+        mind = d;
+        best = t;
+      }
+    }
+    L.map_lut[x] = (uint8_t)best;
+    err += (unsigned long long)L.counts[i] * (unsigned long long)mind;
+  }
+  err = warp_sum(err);
+  __syncthreads();
+  if ((tid & 31) == 0) S.red_u64[tid >> 5] = err;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += S.red_u64[w];
+    if (tot) atomicAdd(&L.st->mse_err, tot);
   }
 }
 
