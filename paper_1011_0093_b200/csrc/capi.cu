@@ -325,7 +325,7 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   // dense ones by scanning all 128 MiB (k_bins_compact), whose K1 runs in
   // 4 Morton slices so each pass's atomics stay in L2.
   const bool sparse = sparse_path(ctx, P);
-  const int passes = P >= (4u << 20) ? 4 : 1;
+  const int passes = fused ? 0 : (P >= (4u << 20) ? 4 : 1);  // fused: K1 runs inside k_prep_small
   for (int q = 0; q < passes; ++q) {
     const uint32_t span = (1u << 24) / passes;
     k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(
@@ -337,6 +337,9 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     // compaction, first-occurrence ranks and init in one cooperative launch
     if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
     PrepParams Q{};
+    Q.img = d_img;
+    Q.P = P;
+    Q.hist = 1;
     Q.occ = ctx->d_occ;
     Q.bins = ctx->bins;
     Q.m_keys = ctx->d_mkeys;

@@ -27,6 +27,9 @@ constexpr int PREP_THREADS = 1024;
 static_assert(sizeof(WsmState) - offsetof(WsmState, evals) == 40, "WsmState run scalars changed");
 
 struct PrepParams {
+  const uint8_t* img;       // with hist: K1 runs here too (phase 0)
+  uint64_t P;
+  int hist;
   uint32_t* occ;            // 2^19 words
   uint2* bins;
   uint32_t* m_keys;
@@ -94,6 +97,11 @@ __global__ void __launch_bounds__(PREP_THREADS, 1) k_prep_small(PrepParams Q) {
   const int tid = threadIdx.x;
   const uint32_t G = gridDim.x, b = blockIdx.x;
   prep_stamp(Q, 0);
+  if (Q.hist) {  // ---- 0: K1 (k_hist_count's work) in the same launch
+    // chunk c -> block c % G: the few chunks of a small image spread over all SMs
+    hist_count_chunks(Q.img, Q.P, Q.bins, 0u, 1u << 24, Q.occ, (uint64_t)tid * G + b, (uint64_t)G * PREP_THREADS);
+    grid.sync();
+  }
 
   // ---- A: set bits per block over a contiguous slice of the occupancy map
   constexpr uint32_t OCC_WORDS_ALL = 1u << 19;
