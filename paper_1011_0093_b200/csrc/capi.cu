@@ -446,7 +446,7 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
                                                  : (const void*)k_wsm_loop<Assign::Fkm, 2>)
                                         : (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1>
                                                  : (const void*)k_wsm_loop<Assign::SortMeans, 2>);
-  CK(cudaLaunchCooperativeKernel(kern, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, 0, ctx->stream));
+  CK(cudaLaunchCooperativeKernel(kern, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, LOOP_DYN_SMEM, ctx->stream));
   CKL();
   return CQB_OK;
 }
@@ -571,7 +571,12 @@ int cqb_create(int device, cqb_ctx** out) {
     if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
     ctx->num_sms = prop.multiProcessorCount;
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2>, LOOP_THREADS, 0));
+    for (const void* f : {(const void*)k_wsm_loop<Assign::SortMeans, 1>, (const void*)k_wsm_loop<Assign::SortMeans, 2>,
+                          (const void*)k_wsm_loop<Assign::Naive, 1>, (const void*)k_wsm_loop<Assign::Naive, 2>,
+                          (const void*)k_wsm_loop<Assign::Fkm, 1>, (const void*)k_wsm_loop<Assign::Fkm, 2>})
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2>, LOOP_THREADS,
+                                                     LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
     ctx->loop_blocks_max = std::min(nb, 1) * ctx->num_sms;
     CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));

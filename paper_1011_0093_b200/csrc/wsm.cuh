@@ -588,6 +588,51 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
 // Assign variants: sort-means (WSM), exhaustive (KM), first k' of the row (FKM).
 enum class Assign { SortMeans, Naive, Fkm };
 
+// Longest-first chunk order (dynamic shared memory). A chunk's scan cost
+// changes little between iterations, so each block hands its chunks to the
+// warps in decreasing order of last iteration's cost (the largest break index
+// J in the chunk): the expensive chunks start first and the block's tail -
+// one warp finishing a deep chunk while the others idle - shrinks. Order only
+// affects timing; every sum is an exact integer and labels are per point.
+constexpr int SCHED_MAX = 4096;  // chunks per block (N' <= 2^24 at 148 blocks needs 3543)
+constexpr int SCHED_BUCKETS = 64;
+struct ChunkSched {
+  uint16_t order[SCHED_MAX];
+  uint8_t cost[SCHED_MAX];
+  uint32_t bucket[SCHED_BUCKETS];
+};
+constexpr size_t LOOP_DYN_SMEM = sizeof(ChunkSched);
+__device__ __forceinline__ ChunkSched& chunk_sched() {
+  extern __shared__ __align__(16) unsigned char loop_dyn[];
+  return *reinterpret_cast<ChunkSched*>(loop_dyn);
+}
+
+// Counting sort of this block's chunks by cost, descending (block-wide).
+__device__ void sched_sort(uint32_t my_ch) {
+  ChunkSched& C = chunk_sched();
+  const int tid = threadIdx.x;
+  for (int b = tid; b < SCHED_BUCKETS; b += blockDim.x) C.bucket[b] = 0u;
+  __syncthreads();
+  for (uint32_t j = tid; j < my_ch; j += blockDim.x) atomicAdd(&C.bucket[min((int)C.cost[j], SCHED_BUCKETS - 1)], 1u);
+  __syncthreads();
+  if (tid < 32) {  // exclusive prefix over buckets, high cost first
+    uint32_t a = C.bucket[SCHED_BUCKETS - 1 - 2 * tid], b = C.bucket[SCHED_BUCKETS - 2 - 2 * tid];
+    uint32_t v = a + b, incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (tid >= o) incl += u;
+    }
+    const uint32_t ex = incl - v;
+    C.bucket[SCHED_BUCKETS - 1 - 2 * tid] = ex;
+    C.bucket[SCHED_BUCKETS - 2 - 2 * tid] = ex + a;
+  }
+  __syncthreads();
+  for (uint32_t j = tid; j < my_ch; j += blockDim.x)
+    C.order[atomicAdd(&C.bucket[min((int)C.cost[j], SCHED_BUCKETS - 1)], 1u)] = (uint16_t)j;
+  __syncthreads();
+}
+
 template <Assign Mode, int PPT>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
@@ -622,17 +667,23 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
     if (lane == 0) j = atomicAdd(&S.wq, (unsigned)PPT);
     j = __shfl_sync(0xffffffffu, j, 0);
     if (j >= my_ch) break;
-    uint32_t key[PPT], idx[PPT];
+    uint32_t key[PPT], idx[PPT], chunk[PPT];
     int lab[PPT], nlab[PPT];
+    const bool sched = Mode == Assign::SortMeans && PPT == 1 && my_ch <= (uint32_t)SCHED_MAX;
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
-      const uint32_t jj = j + q;
+      uint32_t jj = j + q;
+      if (sched && jj < my_ch) jj = chunk_sched().order[jj];
+      chunk[q] = jj;
       const uint32_t i = lo + ((blockIdx.x + G * jj) << 5) + lane;
       const bool v = jj < my_ch && i < hi;
       idx[q] = v ? i : hi;
       key[q] = v ? keys[i] : 0u;
       lab[q] = v ? (int)labels[i] : 0;
     }
+    uint32_t J_of[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) J_of[q] = 0u;
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       nlab[q] = lab[q];
@@ -683,7 +734,15 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
         J = j;
       }
       ev += (uint32_t)J;  // prev + (J - 1) candidates: the reference's count
+      J_of[q] = (uint32_t)J;
       nlab[q] = best;
+    }
+    if (sched) {  // this chunk's cost for the next iteration's order
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const uint32_t c = __reduce_max_sync(0xffffffffu, idx[q] < hi ? (unsigned)J_of[q] : 0u);
+        if (lane == 0 && chunk[q] < my_ch) chunk_sched().cost[chunk[q]] = (uint8_t)min(c, 255u);
+      }
     }
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
@@ -918,6 +977,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     S.accp[t] = make_uint2(0u, 0u);
     S.accm[t] = make_uint2(0u, 0u);
   }
+  if (Mode == Assign::SortMeans)
+    for (int j = tid; j < SCHED_MAX; j += blockDim.x) {  // identity order until costs are known
+      chunk_sched().order[j] = (uint16_t)j;
+      chunk_sched().cost[j] = 0;
+    }
   __syncthreads();
   if (L.block_times && tid == 0) {  // profiling: SM of this block, evaluations in stamp_iter
     unsigned int smid;
@@ -973,6 +1037,14 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     if (rec_it) tl[(it - 1) * 8 + 2] = globaltimer();
     BLOCK_STAMP(1);
     flush_moments(S, gacc, k);
+    // next iteration's longest-first chunk order (this block's chunks are
+    // done); small sample sets only (latency-bound), re-sorted at iterations
+    // 2, 4, 8, ... (costs drift slowly; the sort is not free)
+    if (Mode == Assign::SortMeans && PPT == 1 && it >= 2 && (it & (it - 1)) == 0) {
+      const unsigned long long nn = hi - lo, nch = (nn + 31) >> 5;
+      const uint32_t my_ch = nch > blockIdx.x ? (uint32_t)((nch - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+      if (my_ch <= (uint32_t)SCHED_MAX) sched_sort(my_ch);
+    }
     if (rec_it) tl[(it - 1) * 8 + 3] = globaltimer();
     BLOCK_STAMP(2);
     grid.sync();
