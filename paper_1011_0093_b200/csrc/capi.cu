@@ -958,17 +958,27 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   const uint64_t P = (uint64_t)width * (uint64_t)height;
   CK(cudaSetDevice(ctx->device));
   TRY(ensure_pixels(ctx, P));
+  if (P >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
   CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  // H2D, the whole pipeline and the D2H copies are enqueued back to back with
+  // ONE host synchronisation (the rare draw-exhaustion retry re-enqueues)
+  int ndraws = k + 64;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    ctx->err_target = error_out ? ctx->d_err : nullptr;
+    const int rc = enqueue_quantize(ctx, ctx->d_img, P, k, term, seed, index_out ? ctx->d_index : nullptr,
+                                    rgb_out ? ctx->d_rgb : nullptr, ndraws);
+    ctx->err_target = nullptr;
+    TRY(rc);
+    if (index_out) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (error_out) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_stage->status != ST_DRAWS_EXHAUSTED) break;
+    ndraws *= 4;
+  }
+  TRY(check_status(ctx));
   cqb_report rep{};
-  ctx->err_target = error_out ? ctx->d_err : nullptr;
-  const int rc = cqb_quantize_device(ctx, ctx->d_img, P, k, term, seed, index_out ? ctx->d_index : nullptr,
-                                     rgb_out ? ctx->d_rgb : nullptr, 1, centers_out, sse_history, hist_cap, &rep);
-  ctx->err_target = nullptr;
-  TRY(rc);
-  if (index_out) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
-  if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
-  if (error_out) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  fill_report(ctx, k, seed, P, centers_out, sse_history, hist_cap, &rep);
   if (report) *report = rep;
   return CQB_OK;
 }
