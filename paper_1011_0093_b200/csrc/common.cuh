@@ -63,6 +63,31 @@ __device__ __forceinline__ dd dd_scale(dd x, double b) {  // x * b
 }
 __device__ __forceinline__ dd dd_neg(dd x) { return {-x.hi, -x.lo}; }
 
+// New center coordinate from a cluster's exact integer moments (N pixels,
+// channel sum Sv, all-channel sums S0..S2 and square sum Q). The reference
+// forms sum_i w_i x_i / sum_i w_i sequentially in FP64 with w_i = count_i *
+// fl(1/P) (kmeans.hpp:245-296); the exact mean S/N rounded once differs from
+// it only by that rounding. A one-color cluster (N Q == |S|^2, equality in
+// Cauchy-Schwarz) is common when k is near N', and for it the reference value
+// fl(fl(w x) / w) is reproduced exactly, so that such a cluster is stationary
+// exactly when the reference sees it stationary (the pair count of the
+// incremental table update, kmeans.hpp:137-155).
+__device__ __forceinline__ bool one_color_cluster(unsigned long long N, unsigned long long S0, unsigned long long S1,
+                                                  unsigned long long S2, unsigned long long Q) {
+  const unsigned __int128 a = (unsigned __int128)N * Q;
+  const unsigned __int128 b =
+      (unsigned __int128)S0 * S0 + (unsigned __int128)S1 * S1 + (unsigned __int128)S2 * S2;
+  return a == b;
+}
+__device__ __forceinline__ double center_coord(unsigned long long Sv, unsigned long long N, bool one_color,
+                                               double inv_P) {
+  if (one_color) {
+    const double w = __dmul_rn((double)N, inv_P);
+    return __ddiv_rn(__dmul_rn(w, (double)(Sv / N)), w);
+  }
+  return __ddiv_rn((double)Sv, (double)N);
+}
+
 // Exact u8 -> double without I2F: the bits of 2^52 + v are 0x43300000:v.
 __device__ __forceinline__ double u8_to_double(uint32_t v) {
   return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);

@@ -385,3 +385,70 @@ def test_run_fkm_matches_reference(case, k, kp, mode, images, ref):
     np.testing.assert_allclose(q.report.sse_history, o["sse_history"], rtol=SSE_RTOL)
     with pytest.raises(api.CqbInvalidArgument):
         api.run_fkm(img, 4, 8)  # k_prime > k (fast_variants.hpp:26)
+
+
+# --------------------------------------------------------------------------- randomized + large-path parity
+def _random_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for c in range(n):
+        kind = c % 4
+        w, h = int(rng.integers(1, 140)), int(rng.integers(1, 90))
+        if kind == 0:
+            img = gmm_image(w, h, int(rng.integers(1, 20)), int(rng.integers(0, 10**6)))
+        elif kind == 1:
+            img = uniform_image(w, h, int(rng.integers(0, 10**6)))
+        elif kind == 2:  # few colors, many duplicates
+            pal = rng.integers(0, 256, (int(rng.integers(1, 9)), 3), dtype=np.uint8)
+            img = pal[rng.integers(0, pal.shape[0], w * h)].reshape(h, w, 3)
+        else:  # a single color
+            img = np.broadcast_to(rng.integers(0, 256, 3, dtype=np.uint8), (h, w, 3)).copy()
+        out.append(img)
+    return out
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_quantize_random_images_match_oracle(seed, port):
+    """Randomized images (ragged sizes down to 1 pixel, duplicates, a single
+    color) through the full device pipeline - fused small-image prep, loop
+    with longest-first chunk order and cell candidates, map epilogue -
+    against the oracle: iterations, dist_evals, palette, index map, MSE."""
+    rng = np.random.default_rng(100 + seed)
+    for img in _random_cases(12, seed):
+        P = img.shape[0] * img.shape[1]
+        h = port.build_histogram(img)
+        n = len(h.keys)
+        k = int(rng.integers(1, min(n, 256) + 1))
+        mode = int(rng.integers(0, 2))
+        term = api.Termination.convergent(1e-4, 100) if mode else api.Termination.fixed(int(rng.integers(1, 12)))
+        iters = 10 if mode else term.max_iters
+        q = api.quantize(img, k, term, seed=7)
+        o = port.run_wsm(h.keys, h.counts, P, k, mode=mode, max_iters=iters, eps=1e-4, cap=100, seed=7)
+        assert q.report.iterations == o.iterations, (img.shape, k, mode)
+        assert q.report.dist_evals == o.dist_evals, (img.shape, k, mode)
+        assert q.report.n_unique == n
+        if _pow2(P):
+            np.testing.assert_array_equal(q.palette, o.centers)
+        else:
+            np.testing.assert_allclose(q.palette, o.centers, rtol=CENTER_RTOL, atol=1e-9)
+        mine, my_idx = port.map_pixels(img, q.palette)
+        np.testing.assert_array_equal(q.mapped, mine)
+        np.testing.assert_array_equal(q.index_map, my_idx)
+        assert q.report.mse == port.mse(img, q.mapped)
+
+
+def test_quantize_large_path_matches_oracle(port):
+    """P >= 2M pixels takes the dense-table path (4-slice K1, full 128 MiB
+    compaction, bitmap scan + rank kernels, PPT=2 loop): a 2048x1024 GMM image
+    in fixed-iteration mode against the oracle (bit-exact: P is a power of 2)."""
+    img = gmm_image(2048, 1024, 64, 55)
+    P = img.shape[0] * img.shape[1]
+    q = api.quantize(img, 64, api.Termination.fixed(3), seed=2)
+    h = port.build_histogram(img)
+    o = port.run_wsm(h.keys, h.counts, P, 64, mode=0, max_iters=3, seed=2)
+    assert q.report.n_unique == len(h.keys)
+    assert q.report.iterations == 3 and q.report.dist_evals == o.dist_evals
+    np.testing.assert_array_equal(q.palette, o.centers)
+    mine, my_idx = port.map_pixels(img, q.palette)
+    np.testing.assert_array_equal(q.index_map, my_idx)
+    assert q.report.mse == port.mse(img, q.mapped)
