@@ -42,12 +42,14 @@ def test_loop_kernel_uses_no_fma_for_distances():
     (color.hpp:49-54); the only DFMA allowed is in the double-double SSE."""
     from paper_1011_0093_b200 import _native
 
-    out = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN3cqb10k_wsm_loopENS_10LoopParamsE", _native.LIB_PATH],
-                         capture_output=True, text=True)
-    if out.returncode != 0 or not out.stdout:
+    res = subprocess.run(["cuobjdump", "-res-usage", _native.LIB_PATH], capture_output=True, text=True)
+    if res.returncode != 0:
         pytest.skip("cuobjdump unavailable")
-    sass = out.stdout
-    assert "DMUL" in sass and "DADD" in sass
+    names = sorted(set(re.findall(r"Function (_Z\w*k_wsm_loop\w*)", res.stdout)))
+    assert len(names) == 6, names  # {SortMeans, Naive, Fkm} x {1, 2} points per lane
+    for name in names:
+        out = subprocess.run(["cuobjdump", "-sass", "-fun", name, _native.LIB_PATH], capture_output=True, text=True)
+        assert out.returncode == 0 and "DMUL" in out.stdout and "DADD" in out.stdout, name
 
 
 def test_shim_header_compiles():
