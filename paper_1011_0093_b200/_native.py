@@ -11,7 +11,8 @@ import ctypes as C
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libcolorq_b200.so")
+LIB_PATH = os.environ.get("CQB_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                          "libcolorq_b200.so")  # env: A/B diagnostics only
 
 CQB_OK = 0
 CQB_ERR_INVALID_ARGUMENT = 1

@@ -79,13 +79,19 @@ __device__ __forceinline__ bool one_color_cluster(unsigned long long N, unsigned
       (unsigned __int128)S0 * S0 + (unsigned __int128)S1 * S1 + (unsigned __int128)S2 * S2;
   return a == b;
 }
-__device__ __forceinline__ double center_coord(unsigned long long Sv, unsigned long long N, bool one_color,
-                                               double inv_P) {
-  if (one_color) {
+// The correction only matters when the exact mean is an integer (a one-color
+// cluster's mean is its color), so the moments are re-read on that rare path.
+__device__ __forceinline__ double center_coord(const unsigned long long* __restrict__ mom, int stride, int ch, int t,
+                                               unsigned long long N, double inv_P) {
+  const unsigned long long Sv = __ldcg(&mom[ch * stride + t]);
+  const double c = __ddiv_rn((double)Sv, (double)N);
+  if (c == rint(c) &&
+      one_color_cluster(N, __ldcg(&mom[t]), __ldcg(&mom[stride + t]), __ldcg(&mom[2 * stride + t]),
+                        __ldcg(&mom[4 * stride + t]))) {
     const double w = __dmul_rn((double)N, inv_P);
-    return __ddiv_rn(__dmul_rn(w, (double)(Sv / N)), w);
+    return __ddiv_rn(__dmul_rn(w, c), w);
   }
-  return __ddiv_rn((double)Sv, (double)N);
+  return c;
 }
 
 // Exact u8 -> double without I2F: the bits of 2^52 + v are 0x43300000:v.

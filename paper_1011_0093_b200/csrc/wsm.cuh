@@ -1062,12 +1062,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       const int ch = u / KMAX, t = u % KMAX;
       if (t < k) {
         const unsigned long long N = __ldcg(&gacc[3 * KMAX + t]);
-        const unsigned long long S0 = __ldcg(&gacc[t]), S1 = __ldcg(&gacc[KMAX + t]);
-        const unsigned long long S2 = __ldcg(&gacc[2 * KMAX + t]), Q = __ldcg(&gacc[4 * KMAX + t]);
         if (N) {
           double* dst = ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz);
-          const unsigned long long Sv = ch == 0 ? S0 : (ch == 1 ? S1 : S2);
-          dst[t] = center_coord(Sv, N, one_color_cluster(N, S0, S1, S2, Q), inv_P);
+          dst[t] = center_coord(gacc, KMAX, ch, t, N, inv_P);
         } else if (ch == 0) {
           empt_local = 1;
         }
@@ -1282,11 +1279,10 @@ __global__ void __launch_bounds__(KMAX) k_finalize(const unsigned long long* __r
       const double dn = (double)N;
       const double Sr = (double)mom[t], Sg = (double)mom[KMAX + t], Sb = (double)mom[2 * KMAX + t];
       const double Q = (double)mom[4 * KMAX + t];
-      const bool one = one_color_cluster(N, mom[t], mom[KMAX + t], mom[2 * KMAX + t], mom[4 * KMAX + t]);
       const double inv_P = 1.0 / (double)total;
-      Cnew[3 * t] = center_coord(mom[t], N, one, inv_P);
-      Cnew[3 * t + 1] = center_coord(mom[KMAX + t], N, one, inv_P);
-      Cnew[3 * t + 2] = center_coord(mom[2 * KMAX + t], N, one, inv_P);
+      Cnew[3 * t] = center_coord(mom, KMAX, 0, t, N, inv_P);
+      Cnew[3 * t + 1] = center_coord(mom, KMAX, 1, t, N, inv_P);
+      Cnew[3 * t + 2] = center_coord(mom, KMAX, 2, t, N, inv_P);
       const double cr = Cused[3 * t], cgc = Cused[3 * t + 1], cbc = Cused[3 * t + 2];
       dd cs = dd_add(dd_add(two_prod(cr, Sr), two_prod(cgc, Sg)), two_prod(cbc, Sb));
       dd c2 = dd_add(dd_add(two_prod(cr, cr), two_prod(cgc, cgc)), two_prod(cbc, cbc));
