@@ -81,9 +81,8 @@ __device__ __forceinline__ bool one_color_cluster(unsigned long long N, unsigned
 }
 // The correction only matters when the exact mean is an integer (a one-color
 // cluster's mean is its color), so the moments are re-read on that rare path.
-__device__ __forceinline__ double center_coord(const unsigned long long* __restrict__ mom, int stride, int ch, int t,
-                                               unsigned long long N, double inv_P) {
-  const unsigned long long Sv = __ldcg(&mom[ch * stride + t]);
+__device__ __forceinline__ double center_coord(const unsigned long long* __restrict__ mom, int stride, int t,
+                                               unsigned long long Sv, unsigned long long N, double inv_P) {
   const double c = __ddiv_rn((double)Sv, (double)N);
   if (c == rint(c) &&
       one_color_cluster(N, __ldcg(&mom[t]), __ldcg(&mom[stride + t]), __ldcg(&mom[2 * stride + t]),

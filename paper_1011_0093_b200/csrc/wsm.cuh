@@ -260,7 +260,12 @@ struct LoopSmem {
   unsigned int taken[KMAX];
   int n_empty;
   unsigned int wq;                       // assign: next chunk of this block's list
+  unsigned long long* stamp;             // profiling: block_times in the stamped iteration, else null
 };
+#define SUB_STAMP(phase)                                                         \
+  do {                                                                           \
+    if (threadIdx.x == 0 && S.stamp) S.stamp[(phase) * gridDim.x + blockIdx.x] = globaltimer(); \
+  } while (0)
 
 // Per-block phase stamps for one iteration (profiling): bt[phase * G + block].
 #define BLOCK_STAMP(phase)                                                                   \
@@ -306,6 +311,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
     if (incremental) S.rowo[r][t] = st->order[p * KMAX + t];
   }
   __syncthreads();
+  SUB_STAMP(10);
   bool resort = !incremental;
   if (incremental) {
     // Odd-even transposition sort of positions 1..k-1 starting from the
@@ -334,6 +340,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
       ++rounds;
     }
     resort = again;
+    SUB_STAMP(11);
     if (!resort && lead && t < k) {
       const int e = S.rowo[r][t];
       st->sortedD[p * KMAX + t] = S.rowd[r][e];
@@ -633,6 +640,19 @@ __device__ void sched_sort(uint32_t my_ch) {
   __syncthreads();
 }
 
+// Sort-means scans past DEEP_J entries switch to a
+// search for the break index with DEEP_P independent probes per round, then
+// evaluate the candidates below it with no per-entry check: a deep scan is a
+// few L2 round trips instead of one per two entries.
+#ifndef CQB_DEEP_J
+#define CQB_DEEP_J 13
+#endif
+#ifndef CQB_DEEP_P
+#define CQB_DEEP_P 3
+#endif
+constexpr int DEEP_J = CQB_DEEP_J;
+constexpr int DEEP_P = CQB_DEEP_P;
+
 template <Assign Mode, int PPT>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
@@ -648,9 +668,13 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   // (chunk c -> block c % G), so every SM gets the same number of chunks
   // within one and samples every region of color space; inside a block the
   // chunks are handed to the warps dynamically (shared counter), PPT at a
-  // time: a warp held up by deep scans does not hold up the block.
+  // time (small sample sets: longest first, sched_sort): a warp held up by
+  // deep scans does not hold up the block.
   const uint32_t G = gridDim.x, W = blockDim.x >> 5, w = threadIdx.x >> 5;
   const uint32_t nch = (hi - lo + 31u) >> 5;
+  // small sample sets: chunk costs recorded for the longest-first order
+  constexpr bool kSched = Mode == Assign::SortMeans && PPT == 1;
+  constexpr bool kDeep = Mode == Assign::SortMeans;
   const uint32_t my_ch = nch > blockIdx.x ? (nch - 1u - blockIdx.x) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const uint8_t* __restrict__ go = L.st->order;
@@ -669,7 +693,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
     if (j >= my_ch) break;
     uint32_t key[PPT], idx[PPT], chunk[PPT];
     int lab[PPT], nlab[PPT];
-    const bool sched = Mode == Assign::SortMeans && PPT == 1 && my_ch <= (uint32_t)SCHED_MAX;
+    const bool sched = kSched && my_ch <= (uint32_t)SCHED_MAX;
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       uint32_t jj = j + q;
@@ -697,6 +721,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       const double* rd = gd + p * KMAX;
       const uint8_t* ro = go + p * KMAX;
       int J = 1;
+      bool deep = false;
       if constexpr (Mode == Assign::Fkm) {
         // run_fkm (fast_variants.hpp:42-52): lexicographic (d, index) minimum
         // over order[p][0..k') - self first, then its nearest centers
@@ -730,6 +755,38 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
           lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]), t1);
           ++j;
           if (j >= k) break;
+          if (kDeep && j >= DEEP_J) {  // deep scan: find the break index, then evaluate without checks
+            deep = true;
+            break;
+          }
+        }
+        if (kDeep && deep) {
+          // J = min{i in [j, k) : rd[i] >= bound}, or k: the row is sorted, so
+          // DEEP_P independent probes per round cut [lo, hi] to 1/(DEEP_P+1)
+          int a = j, b = k;
+          while (a < b) {
+            int na = a, nb = b;
+#pragma unroll
+            for (int u = DEEP_P; u >= 1; --u) {
+              const int m = a + ((b - a) * u) / (DEEP_P + 1);
+              if (m >= a && m < b) {
+                if (rd[m] >= bound) nb = m;
+                else if (m + 1 > na) na = m + 1;
+              }
+            }
+            if (na == a && nb == b) {  // interval too small for distinct probes: step
+              if (rd[a] >= bound) nb = a;
+              else na = a + 1;
+            }
+            a = na < nb ? na : nb;
+            b = nb;
+          }
+          // candidates j .. b-1 are below the bound: the serial scan's set
+          for (int i2 = j; i2 < b; ++i2) {
+            const int t = ro[i2];
+            lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+          }
+          j = b;
         }
         J = j;
       }
@@ -737,7 +794,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       J_of[q] = (uint32_t)J;
       nlab[q] = best;
     }
-    if (sched) {  // this chunk's cost for the next iteration's order
+    if (kSched) {  // this chunk's cost for the next iteration's order
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         const uint32_t c = __reduce_max_sync(0xffffffffu, idx[q] < hi ? (unsigned)J_of[q] : 0u);
@@ -982,6 +1039,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       chunk_sched().order[j] = (uint16_t)j;
       chunk_sched().cost[j] = 0;
     }
+  if (tid == 0) S.stamp = nullptr;
   __syncthreads();
   if (L.block_times && tid == 0) {  // profiling: SM of this block, evaluations in stamp_iter
     unsigned int smid;
@@ -1062,9 +1120,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       const int ch = u / KMAX, t = u % KMAX;
       if (t < k) {
         const unsigned long long N = __ldcg(&gacc[3 * KMAX + t]);
+        const unsigned long long Sv = __ldcg(&gacc[ch * KMAX + t]);
         if (N) {
           double* dst = ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz);
-          dst[t] = center_coord(gacc, KMAX, ch, t, N, inv_P);
+          dst[t] = center_coord(gacc, KMAX, t, Sv, N, inv_P);
         } else if (ch == 0) {
           empt_local = 1;
         }
@@ -1154,6 +1213,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     __syncthreads();
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
+    if (tid == 0) S.stamp = (L.block_times && it == L.stamp_iter) ? L.block_times : nullptr;
     if (!kNaive) tables_all(S, st, k, true);  // wasted work on the final iteration only
     if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
     BLOCK_STAMP(5);
@@ -1280,9 +1340,9 @@ __global__ void __launch_bounds__(KMAX) k_finalize(const unsigned long long* __r
       const double Sr = (double)mom[t], Sg = (double)mom[KMAX + t], Sb = (double)mom[2 * KMAX + t];
       const double Q = (double)mom[4 * KMAX + t];
       const double inv_P = 1.0 / (double)total;
-      Cnew[3 * t] = center_coord(mom, KMAX, 0, t, N, inv_P);
-      Cnew[3 * t + 1] = center_coord(mom, KMAX, 1, t, N, inv_P);
-      Cnew[3 * t + 2] = center_coord(mom, KMAX, 2, t, N, inv_P);
+      Cnew[3 * t] = center_coord(mom, KMAX, t, mom[t], N, inv_P);
+      Cnew[3 * t + 1] = center_coord(mom, KMAX, t, mom[KMAX + t], N, inv_P);
+      Cnew[3 * t + 2] = center_coord(mom, KMAX, t, mom[2 * KMAX + t], N, inv_P);
       const double cr = Cused[3 * t], cgc = Cused[3 * t + 1], cbc = Cused[3 * t + 2];
       dd cs = dd_add(dd_add(two_prod(cr, Sr), two_prod(cgc, Sg)), two_prod(cbc, Sb));
       dd c2 = dd_add(dd_add(two_prod(cr, cr), two_prod(cgc, cgc)), two_prod(cbc, cbc));

@@ -20,6 +20,7 @@ G = C.c_int()
 lib.cqb_device_info(ctx.h, None, C.byref(G))
 g = G.value
 lib.cqb_set_profiling(ctx.h, int(sys.argv[2]) if len(sys.argv) > 2 else 3)
+lib.cqb_set_debug(ctx.h, int(os.environ.get("CQB_DEBUG", "0")))  # ablations (results wrong)
 term = N.Termination(1, 10, 1e-4, 100)
 rep = N.Report()
 cent = np.zeros(768)
@@ -43,8 +44,18 @@ dur = lambda a, b: (ph[b] - ph[a]) / 1e3  # noqa: E731
 for a, b, n in [(0, 1, "points"), (1, 2, "flush"), (2, 3, "barrier1 wait"), (3, 4, "finalize"), (4, 5, "tables")]:
     v = dur(a, b)
     print(f"dur {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f} block0 {v[0]:6.2f}")
+ph = bt[: 12 * g].reshape(12, g).astype(np.int64)
+rows = np.arange(1, g)  # blocks that own table rows
+for a, b, n in [(3, 8, "fin: centers"), (8, 9, "fin: block0"), (9, 4, "fin: copy"), (4, 10, "tab: dist+load"),
+                (10, 11, "tab: repair"), (11, 5, "tab: write")]:
+    v = dur(a, b)[rows]
+    print(f"sub {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f}")
+for a, b, n in []:
+    v = dur(a, b)
+    print(f"dur {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f} block0 {v[0]:6.2f}")
 
 wd = bt[6 * 1024: 6 * 1024 + 32 * 4].reshape(32, 4).astype(np.int64)
 print("block 0 per warp: phase1 cycles, drain cycles, drains")
 for w in range(32):
     print(f"  w{w:2d} p1 {wd[w,0]:7d}  p2 {wd[w,1]:7d}  drains {wd[w,2]}")
+
