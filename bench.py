@@ -457,6 +457,9 @@ def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
     elif stage == "bins_compact":
         traffic_alg = 8.0 * (1 << 24) + 12.0 * n_unique
         note = "128 MiB bin-table scan + 12 B per unique color written (Morton samples)"
+    elif stage == "prep_small":
+        traffic_alg = 3.0 * P + 2.0 * (1 << 21) + 12.0 * n_unique
+        note = "3P raster read + 2 MiB occupancy bitmap written and read + 12 B per unique color written"
     elif stage == "map_pixels":
         traffic_alg = 7.0 * P
         note = "3P read + P index + 3P RGB written"
@@ -494,10 +497,20 @@ def _ncu_traffic(stage, P):
     return None
 
 
+SMALL_PATH_PIXELS = 2 << 20  # capi.cu OCC_MAX_PIXELS: below it the histogram is K1 + the fused k_prep_small
+
+
 def _hbm_stages(stage_ms, P, n_unique, peaks):
     """Achieved algorithmic GB/s of the HBM-bound stages."""
     out = {}
-    for st in ("hist_count", "bins_compact", "map_pixels"):
+    if P < SMALL_PATH_PIXELS:
+        # the small-image histogram (K1 + k_prep_small) spans the reset .. init_rank events
+        ms = sum(stage_ms.get(st, 0.0) for st in ("reset", "hist_count", "bins_compact", "init_rank"))
+        if ms > 0:
+            r = _roofline("prep_small", ms, P, n_unique, 1, 0, peaks, 0)
+            out["prep_small"] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 4),
+                                 "algorithmic_bytes": r["algorithmic_bytes"], "ms": round(ms, 4), "note": r["note"]}
+    for st in (("map_pixels",) if P < SMALL_PATH_PIXELS else ("hist_count", "bins_compact", "map_pixels")):
         if st in stage_ms and stage_ms[st] > 0:
             r = _roofline(st, stage_ms[st], P, n_unique, 1, 0, peaks, 0)
             out[st] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 4),

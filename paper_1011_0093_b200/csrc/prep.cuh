@@ -24,7 +24,7 @@ namespace cqb {
 
 constexpr int PREP_THREADS = 1024;
 // zero_state clears exactly these run scalars; keep in sync with WsmState
-static_assert(sizeof(WsmState) - offsetof(WsmState, evals) == 40, "WsmState run scalars changed");
+static_assert(offsetof(WsmState, stop_it) + sizeof(int) - offsetof(WsmState, evals) == 40, "WsmState run scalars changed");
 
 struct PrepParams {
   const uint8_t* img;       // with hist: K1 runs here too (phase 0)

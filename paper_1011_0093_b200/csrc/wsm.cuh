@@ -45,6 +45,11 @@ struct WsmState {
   unsigned long long cand_d[2][MAXBLK];   // reseed candidates (d bits, rank, key)
   unsigned int cand_i[2][MAXBLK];
   unsigned int cand_k[2][MAXBLK];
+  // the loop's grid barrier: arrivals in the low 32 bits (monotonic within a
+  // launch, zeroed by block 0 before the prologue barrier), block 0's stop
+  // decision in the high half; alone in its 128-B line
+  alignas(128) unsigned long long bar;
+  unsigned long long bar_pad[15];
   unsigned long long evals;               // point + pair distance evaluations
   unsigned long long mse_err;             // Σ count * int distance (map pass)
   double sse;
@@ -260,6 +265,8 @@ struct LoopSmem {
   unsigned int taken[KMAX];
   int n_empty;
   unsigned int wq;                       // assign: next chunk of this block's list
+  unsigned long long barv;               // grid barrier: the counter value that released this block
+  int stop_flag;                         // block 0: stop after this iteration
   unsigned long long* stamp;             // profiling: block_times in the stamped iteration, else null
 };
 #define SUB_STAMP(phase)                                                         \
@@ -651,6 +658,9 @@ __device__ void sched_sort(uint32_t my_ch) {
 #define CQB_DEEP_P 3
 #endif
 constexpr int DEEP_J = CQB_DEEP_J;
+#ifndef CQB_LOOP_BARRIER
+#define CQB_LOOP_BARRIER 1
+#endif
 constexpr int DEEP_P = CQB_DEEP_P;
 
 template <Assign Mode, int PPT>
@@ -998,6 +1008,29 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
 
 // One instantiation per assignment variant (WSM, KM, FKM): a single kernel
 // with a runtime switch cost the WSM loop ~1.5% (register allocation).
+// Grid barrier of the persistent loop (one per phase boundary). Thread 0 of
+// each block: acq_rel fence (the block's writes, ordered by the preceding
+// bar.sync, become visible), one relaxed add to the counter, then acquire
+// loads until every block has arrived; the other threads wait at bar.sync.
+// Same ordering as cooperative_groups' grid.sync, with a payload: block 0
+// adds its stop decision to the high half, so no block needs a separate L2
+// round trip to learn whether the loop ends.
+__device__ __forceinline__ unsigned long long loop_barrier(LoopSmem& S, unsigned long long* bar, unsigned int target,
+                                                           unsigned long long add) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(bar), "l"(add) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+    } while ((unsigned int)v < target);
+    S.barv = v;
+  }
+  __syncthreads();
+  return S.barv;
+}
+
 template <Assign Mode, int PPT>
 __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
@@ -1053,7 +1086,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   // pair evaluations of the center tables (block 0 only); none in naive mode
   unsigned long long pair_evals =
       (kNaive || kFkm) ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+  if (CQB_LOOP_BARRIER && blockIdx.x == 0 && tid == 0) st->bar = 0ull;  // before the prologue barrier
   grid.sync();
+  unsigned int bar_target = 0;  // loop_barrier episodes x G
 
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
   for (int it = 1;; ++it) {
@@ -1105,7 +1140,12 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     }
     if (rec_it) tl[(it - 1) * 8 + 3] = globaltimer();
     BLOCK_STAMP(2);
-    grid.sync();
+    if (CQB_LOOP_BARRIER) {
+      bar_target += gridDim.x;
+      loop_barrier(S, &st->bar, bar_target, 1ull);
+    } else {
+      grid.sync();
+    }
     if (rec_it) tl[(it - 1) * 8 + 4] = globaltimer();
     BLOCK_STAMP(3);
     if (L.moments_only) break;
@@ -1179,6 +1219,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         st->sse = sse;
         st->n_empty_events += empt;
         if (stop) st->stop_it = it;
+        S.stop_flag = stop;
         // pair evaluations of the incremental table update (kmeans.hpp:137-155)
         if (!stop) {
           const unsigned long long still = (unsigned long long)(k - moved);
@@ -1217,8 +1258,14 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     if (!kNaive) tables_all(S, st, k, true);  // wasted work on the final iteration only
     if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
     BLOCK_STAMP(5);
-    grid.sync();
-    if (*reinterpret_cast<volatile int*>(&st->stop_it) == it) break;
+    if (CQB_LOOP_BARRIER) {
+      bar_target += gridDim.x;
+      const bool stop_here = blockIdx.x == 0 && S.stop_flag;
+      if ((loop_barrier(S, &st->bar, bar_target, 1ull + (stop_here ? (1ull << 32) : 0ull)) >> 32) != 0) break;
+    } else {
+      grid.sync();
+      if (*reinterpret_cast<volatile int*>(&st->stop_it) == it) break;
+    }
   }
   // one evals flush per block (a per-warp atomic every iteration would
   // serialize thousands of same-address atomics in L2)
