@@ -52,6 +52,10 @@ def _args():
     ap.add_argument("--k", type=int, default=None, help="default: 256 if the config lists it, else its K")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="shard the unique samples over the ranks (in-kernel NVLink exchange); default for cfg4 at N>1")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="single GPU: W block groups of the loop act as W sharded ranks (exchange overhead)")
     return ap.parse_args()
 
 
@@ -601,6 +605,148 @@ def run_batch(a, cfg, world, rank, local):
         dist.destroy_process_group()
 
 
+def run_sharded(a, cfg, world, rank, local):
+    """BASELINE config 4 as the north star shards it: every rank holds the
+    image and builds the histogram, the unique samples are split into `world`
+    contiguous Morton ranges, and the per-iteration all-reduce of the K x 5
+    exact moment sums runs INSIDE the persistent loop kernel over NVLink
+    (cqb_quantize_sharded; no host round trip, no NCCL call per iteration).
+    Each rank maps its own pixel range. Strong scaling: one image per step for
+    the whole job. `--emulate-ranks W` (one GPU): the W ranks are block groups
+    of the single launch — the same exchange code, to measure its overhead."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200 import _native as N
+    from paper_1011_0093_b200 import api
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = N.context(local)
+    lib = ctx.lib
+    stream = torch.cuda.Stream(device=dev)
+    ctx.check(lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
+    q = PeerShardedQuantizer(ctx=ctx, emulate=a.emulate_ranks if world == 1 else 0)
+    img = cfg.image()
+    P, k = cfg.pixels, a.k
+    term = api.Termination.convergent(EPSILON, HARD_CAP)
+    d_img = torch.from_numpy(img.reshape(-1)).to(dev)
+    d_idx = torch.empty(P, dtype=torch.uint8, device=dev)
+    d_out = torch.empty(3 * P, dtype=torch.uint8, device=dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def one():
+        return q.enqueue(d_img.data_ptr(), P, k, term, INIT_SEED, d_idx.data_ptr(), d_out.data_ptr())
+
+    def tmax(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with torch.cuda.stream(stream):
+        for _ in range(a.warmup):
+            flush_buf.fill_(1)
+            one()
+            q.fetch()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    with torch.cuda.stream(stream):
+        for i in range(a.steps):
+            flush_buf.fill_(1)
+            evs[i][0].record(stream)
+            one()
+            evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = tmax(sum(x.elapsed_time(y) for x, y in evs))
+    centers, rep, _ = q.fetch()
+    launches = a.steps * int(rep.gpu_launches)
+    evals = int(rep.dist_evals)
+    if world > 1:
+        t = torch.tensor([evals], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        evals = int(t.item())
+    # stage attribution (loop kernel time) on a few profiled steps
+    ctx.check(lib.cqb_set_profiling(ctx.h, 1))
+    st = []
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            flush_buf.fill_(1)
+            one()
+            q.fetch()
+            ms = (C.c_float * 7)()
+            ctx.check(lib.cqb_stage_times(ctx.h, ms, 7))
+            st.append(list(ms))
+            tl = np.zeros(8 * HARD_CAP, np.uint64)
+            ctx.check(lib.cqb_loop_timeline(ctx.h, tl.ctypes.data_as(C.POINTER(C.c_uint64)), HARD_CAP))
+    ctx.check(lib.cqb_set_profiling(ctx.h, 0))
+    stage_ms = {n: float(v) for n, v in zip(N.STAGES, np.median(np.array(st), axis=0))}
+    phases = _loop_phases(tl.reshape(HARD_CAP, 8).astype(np.int64), int(rep.iterations))
+    # e2e: pinned host image in, this rank's slice of the index map + mapped raster out
+    pin_img = torch.from_numpy(img.reshape(-1)).pin_memory()
+    pin_idx = torch.empty(P, dtype=torch.uint8).pin_memory()
+    pin_out = torch.empty(3 * P, dtype=torch.uint8).pin_memory()
+    e2e = []
+    bo = 0
+    for i in range(a.warmup + a.steps):
+        flush_buf.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            d_img.copy_(pin_img, non_blocking=True)
+            lo, hi = one()
+            pin_idx[lo:hi].copy_(d_idx[lo:hi], non_blocking=True)
+            pin_out[3 * lo:3 * hi].copy_(d_out[3 * lo:3 * hi], non_blocking=True)
+            c2, _, _ = q.fetch()
+        stream.synchronize()
+        if i >= a.warmup:
+            e2e.append(time.perf_counter() - t0)
+        bo = 4 * (hi - lo)
+    e2e_s = tmax(sum(e2e))
+    assert np.array_equal(c2, centers)
+    ok = None
+    if rank == 0 and world == 1 and a.emulate_ranks:  # the emulated ranks equal the one-rank path
+        single = api.quantize(img, k, term, INIT_SEED, index_map=False, mapped=False, device=local)
+        ok = bool(np.array_equal(single.palette, centers) and single.report.dist_evals == evals)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        peaks = _peaks()
+        n_unique, iters = int(rep.n_unique), int(rep.iterations)
+        value = P * a.steps / (total_ms * 1e-3) / 1e6
+        ranks = world if world > 1 else max(a.emulate_ranks, 1)
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload(cfg, k), "pixels": P, "n_unique": n_unique, "iterations": iters,
+                       "k": k, "parallelism": (f"sample shards x{world}, in-kernel NVLink exchange" if world > 1 else
+                                               f"sample shards x{ranks} emulated as block groups on one GPU"),
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "timed": "per-step CUDA events on the library stream; value = P*steps / max-rank sum"},
+            "e2e": {"value": P * a.steps / e2e_s / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": 3 * P,
+                    "d2h_bytes_per_step": bo, "path": "cqb_quantize_sharded, pinned host image in, own slice out"},
+            "gpu_launches": launches,
+            "roofline": _roofline("wsm_loop", stage_ms["wsm_loop"], P, n_unique, iters, k, peaks, evals),
+            "stages_ms": {kk: round(v, 5) for kk, v in stage_ms.items()},
+            "loop_phases_us": phases, "dist_evals": evals, "clocks": clk,
+        }
+        if ok is not None:
+            line["matches_single_rank"] = ok
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = _args()
     world, rank, local = _dist()
@@ -612,6 +758,9 @@ def main():
         return
     if cfg.images > 1:
         run_batch(a, cfg, world, rank, local)
+        return
+    if a.shard or a.emulate_ranks > 0 or (cfg.name == "cfg4" and world > 1):
+        run_sharded(a, cfg, world, rank, local)
         return
     run_ours(a, cfg, world, rank, local)
 

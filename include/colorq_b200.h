@@ -212,6 +212,40 @@ int cqb_shard_reseed_candidate(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const dou
                                const uint32_t* taken_ranks, int n_taken, double* d_out, uint32_t* rank_out,
                                uint32_t* key_out);
 
+/* ---- sharded WSM with the exchange inside the persistent loop ------------
+ * BASELINE config 4 at 1..8 GPUs, one process per GPU. Replaces the host
+ * round trip per iteration of the cqb_shard_* path: every rank runs the whole
+ * quantize (histogram of the full image, init, loop, map) on its own GPU; the
+ * loop processes only the rank's contiguous range of the Morton-ordered
+ * samples, and once per iteration each rank writes its exact K x 5 moment
+ * sums into every peer's exchange window over NVLink (plain stores + a
+ * sys-scope flag) and sums the world's contributions itself: no NCCL call and
+ * no host involvement inside the loop. Empty-cluster reseed candidates use
+ * the same mailboxes. At the end the label ranges are all-gathered into every
+ * window, each rank builds the full key -> index table, and maps its own
+ * pixel range. Integer moments make every rank's trajectory bit-identical to
+ * the single-GPU run.
+ *
+ * Setup (collective): cqb_xch_window allocates this rank's window and returns
+ * its cudaIpcMemHandle (CQB_IPC_HANDLE_BYTES bytes); the host all-gathers the
+ * handles (torch.distributed) and passes all of them, in rank order, to
+ * cqb_xch_open. cqb_xch_emulate(v) instead makes v block groups of the one
+ * cooperative launch act as the ranks (single-GPU test of the protocol).
+ *
+ * cqb_quantize_sharded enqueues on the context stream (like
+ * cqb_quantize_device with sync = 0); results via cqb_fetch_results. The
+ * report is complete except dist_evals, which counts this rank's point
+ * evaluations (+ the pair evaluations on rank 0): sum it over the ranks.
+ * px_range (nullable, 2 values) receives the pixel range [lo, hi) this rank
+ * wrote into d_index_out / d_rgb_out (full-image buffers). A peer that does
+ * not answer within 5 s fails the call with CQB_ERR_NCCL instead of hanging. */
+#define CQB_IPC_HANDLE_BYTES 64
+int cqb_xch_window(cqb_ctx* ctx, int world, int rank, void* ipc_handle_out);
+int cqb_xch_open(cqb_ctx* ctx, const void* handles);
+int cqb_xch_emulate(cqb_ctx* ctx, int vranks);
+int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int k, const cqb_termination* term,
+                         uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range);
+
 #ifdef __cplusplus
 }
 #endif

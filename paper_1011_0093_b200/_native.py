@@ -30,8 +30,10 @@ EXPORTS = (
     "cqb_fetch_results", "cqb_quantize_batch", "cqb_quantize_ex", "cqb_error_image", "cqb_run_km_full", "cqb_run_fkm",
     "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
-    "cqb_shard_reseed_candidate", "cqb_set_debug",
+    "cqb_shard_reseed_candidate", "cqb_set_debug", "cqb_xch_window", "cqb_xch_open", "cqb_xch_emulate",
+    "cqb_quantize_sharded",
 )
+IPC_HANDLE_BYTES = 64  # CQB_IPC_HANDLE_BYTES (cudaIpcMemHandle_t)
 # cqb_stage_times intervals: memsets | K1 | K2b | init + bitmap scan + rank (+ gather) | loop | map tables+unique | map pixels
 STAGES = ("reset", "hist_count", "bins_compact", "init_rank", "wsm_loop", "map_unique", "map_pixels")
 
@@ -118,6 +120,10 @@ def load_library() -> C.CDLL:
                                            C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.cqb_shard_reseed_candidate.argtypes = [_vp, C.c_uint64, C.c_uint64, _f64p, _u32p, C.c_int, _f64p, _u32p,
                                                  _u32p]
+        L.cqb_xch_window.argtypes = [_vp, C.c_int, C.c_int, _vp]
+        L.cqb_xch_open.argtypes = [_vp, _vp]
+        L.cqb_xch_emulate.argtypes = [_vp, C.c_int]
+        L.cqb_quantize_sharded.argtypes = [_vp, _vp, C.c_uint64, C.c_int, _T, C.c_uint64, _vp, _vp, _u64p]
         _lib = L
         return L
 

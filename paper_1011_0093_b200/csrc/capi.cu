@@ -106,6 +106,14 @@ struct cqb_ctx {
   int* d_sortedDr = nullptr;
   uint8_t* d_orderR = nullptr;
   uint32_t* d_palkey = nullptr;
+  // in-kernel sharded loop (cqb_xch_*, cqb_quantize_sharded)
+  int xmode = 0;                      // 0 none, 1 one process per GPU (IPC windows), 2 emulated ranks
+  int xw = 0, xrank = -1;
+  unsigned long long* xwin = nullptr;  // own window (mode 1) / the xw windows (mode 2)
+  unsigned long long* xpeer[8] = {};   // every rank's window as mapped here (own = xwin)
+  unsigned long long* xacc = nullptr;  // mode 2: per-group moment sums
+  bool xsharded = false;              // set only while cqb_quantize_sharded enqueues
+  uint64_t px_lo = 0, px_hi = 0;      // sharded: pixel range mapped by this rank
 
   unsigned long long* d_draws = nullptr;
   unsigned long long* h_draws = nullptr;
@@ -436,17 +444,35 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.fkm_kprime = ctx->fkm_kprime;
   if (ctx->profiling)
     CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
+  int X = 0;
+  unsigned grid = (unsigned)loop_grid(ctx);
+  if (ctx->xsharded) {
+    X = ctx->xmode;
+    L.xw = ctx->xw;
+    L.xrank = X == 1 ? ctx->xrank : -1;
+    for (int r = 0; r < ctx->xw; ++r) L.xbox[r] = ctx->xpeer[r];
+    if (X == 1) L.labels = reinterpret_cast<uint8_t*>(ctx->xwin) + XB_LAB_OFF;
+    if (X == 2) {
+      L.xacc = ctx->xacc;
+      grid = grid / (unsigned)ctx->xw * (unsigned)ctx->xw;  // equal block groups
+      CK(cudaMemsetAsync(ctx->xacc, 0, sizeof(unsigned long long) * 5 * KMAX * ctx->xw, ctx->stream));
+    }
+  }
   void* args[] = {&L};
   // one point per lane per grab for small sample sets (N' <= P < 2M): finer
   // balance; two for large ones: more ILP (cfg2 +1.2%, cfg4 +8% respectively)
   const bool small = total < OCC_MAX_PIXELS;
-  const void* kern = L.naive         ? (small ? (const void*)k_wsm_loop<Assign::Naive, 1>
-                                              : (const void*)k_wsm_loop<Assign::Naive, 2>)
-                     : L.fkm_kprime > 0 ? (small ? (const void*)k_wsm_loop<Assign::Fkm, 1>
-                                                 : (const void*)k_wsm_loop<Assign::Fkm, 2>)
-                                        : (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1>
-                                                 : (const void*)k_wsm_loop<Assign::SortMeans, 2>);
-  CK(cudaLaunchCooperativeKernel(kern, dim3(loop_grid(ctx)), dim3(LOOP_THREADS), args, LOOP_DYN_SMEM, ctx->stream));
+  const void* kern = X == 1 ? (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 1>
+                                     : (const void*)k_wsm_loop<Assign::SortMeans, 2, 1>)
+                     : X == 2 ? (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 2>
+                                       : (const void*)k_wsm_loop<Assign::SortMeans, 2, 2>)
+                     : L.naive ? (small ? (const void*)k_wsm_loop<Assign::Naive, 1, 0>
+                                        : (const void*)k_wsm_loop<Assign::Naive, 2, 0>)
+                     : L.fkm_kprime > 0 ? (small ? (const void*)k_wsm_loop<Assign::Fkm, 1, 0>
+                                                 : (const void*)k_wsm_loop<Assign::Fkm, 2, 0>)
+                                        : (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 0>
+                                                 : (const void*)k_wsm_loop<Assign::SortMeans, 2, 0>);
+  CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(LOOP_THREADS), args, LOOP_DYN_SMEM, ctx->stream));
   CKL();
   return CQB_OK;
 }
@@ -469,6 +495,7 @@ int check_status(cqb_ctx* ctx) {
   if (s == ST_K_EXCEEDS_N)
     return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
   if (s == ST_DRAWS_EXHAUSTED) return fail(ctx, CQB_ERR_INTERNAL, "init_centers: raw draw buffer exhausted");
+  if (s == ST_XCH_TIMEOUT) return fail(ctx, CQB_ERR_NCCL, "sharded loop: a peer rank did not answer within 5 s");
   if (s != ST_OK) return fail(ctx, CQB_ERR_INTERNAL, "device status %d", s);
   return CQB_OK;
 }
@@ -532,11 +559,14 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   }
   PROF(6);
   uint8_t* d_err_out = ctx->err_target;
-  if (d_index || d_rgb_out || d_err_out) {
-    const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  // sharded: this rank maps its pixel range only (offsets are multiples of 16 pixels: aligned vectors)
+  const uint64_t plo = ctx->xsharded ? ctx->px_lo : 0, pn = ctx->xsharded ? ctx->px_hi - ctx->px_lo : P;
+  if ((d_index || d_rgb_out || d_err_out) && pn > 0) {
+    const uint64_t nchunk = (pn + PX_PER_THREAD - 1) / PX_PER_THREAD;
     const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-    k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->lut, ctx->d_palkey, k, d_index,
-                                                                   d_rgb_out, d_err_out);
+    k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(
+        d_img + 3 * plo, pn, ctx->lut, ctx->d_palkey, k, d_index ? d_index + plo : nullptr,
+        d_rgb_out ? d_rgb_out + 3 * plo : nullptr, d_err_out ? d_err_out + 3 * plo : nullptr);
     CKL();
   }
   PROF(7);
@@ -571,11 +601,13 @@ int cqb_create(int device, cqb_ctx** out) {
     if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
     ctx->num_sms = prop.multiProcessorCount;
     int nb = 0;
-    for (const void* f : {(const void*)k_wsm_loop<Assign::SortMeans, 1>, (const void*)k_wsm_loop<Assign::SortMeans, 2>,
-                          (const void*)k_wsm_loop<Assign::Naive, 1>, (const void*)k_wsm_loop<Assign::Naive, 2>,
-                          (const void*)k_wsm_loop<Assign::Fkm, 1>, (const void*)k_wsm_loop<Assign::Fkm, 2>})
+    for (const void* f : {(const void*)k_wsm_loop<Assign::SortMeans, 1, 0>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 0>,
+                          (const void*)k_wsm_loop<Assign::Naive, 1, 0>, (const void*)k_wsm_loop<Assign::Naive, 2, 0>,
+                          (const void*)k_wsm_loop<Assign::Fkm, 1, 0>, (const void*)k_wsm_loop<Assign::Fkm, 2, 0>,
+                          (const void*)k_wsm_loop<Assign::SortMeans, 1, 1>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 1>,
+                          (const void*)k_wsm_loop<Assign::SortMeans, 1, 2>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 2>})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2>, LOOP_THREADS,
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2, 0>, LOOP_THREADS,
                                                      LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
     ctx->loop_blocks_max = std::min(nb, 1) * ctx->num_sms;
@@ -647,6 +679,11 @@ int cqb_destroy(cqb_ctx* ctx) {
   if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
   if (ctx->h_scalar) cudaFreeHost(ctx->h_scalar);
   if (ctx->h_mom) cudaFreeHost(ctx->h_mom);
+  if (ctx->xmode == 1)
+    for (int r = 0; r < ctx->xw; ++r)
+      if (r != ctx->xrank && ctx->xpeer[r]) cudaIpcCloseMemHandle(ctx->xpeer[r]);
+  if (ctx->xwin) cudaFree(ctx->xwin);
+  if (ctx->xacc) cudaFree(ctx->xacc);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pev)
@@ -1205,6 +1242,103 @@ int cqb_shard_reseed_candidate(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const dou
   if (rank_out) *rank_out = rk[0];
   if (key_out) *key_out = rk[1];
   return CQB_OK;
+}
+
+/* ---- in-kernel sharded loop --------------------------------------------- */
+
+namespace {
+int xch_reset(cqb_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->xmode == 1)
+    for (int r = 0; r < ctx->xw; ++r)
+      if (r != ctx->xrank && ctx->xpeer[r]) cudaIpcCloseMemHandle(ctx->xpeer[r]);
+  if (ctx->xwin) cudaFree(ctx->xwin);
+  if (ctx->xacc) cudaFree(ctx->xacc);
+  ctx->xwin = ctx->xacc = nullptr;
+  for (auto& p : ctx->xpeer) p = nullptr;
+  ctx->xmode = 0;
+  ctx->xw = 0;
+  ctx->xrank = -1;
+  return CQB_OK;
+}
+}  // namespace
+
+int cqb_xch_window(cqb_ctx* ctx, int world, int rank, void* ipc_handle_out) {
+  if (!ctx || !ipc_handle_out) return CQB_ERR_INVALID_ARGUMENT;
+  if (world < 1 || world > XMAX || rank < 0 || rank >= world)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "exchange: world %d / rank %d (1 <= world <= %d)", world, rank, XMAX);
+  CK(cudaSetDevice(ctx->device));
+  TRY(xch_reset(ctx));
+  CK(cudaMalloc(&ctx->xwin, XB_BYTES));
+  CK(cudaMemset(ctx->xwin, 0, XB_BYTES));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->xwin));
+  memcpy(ipc_handle_out, &h, sizeof(h));
+  ctx->xmode = 1;
+  ctx->xw = world;
+  ctx->xrank = rank;
+  ctx->xpeer[rank] = ctx->xwin;
+  return CQB_OK;
+}
+
+int cqb_xch_open(cqb_ctx* ctx, const void* handles) {
+  if (!ctx || !handles) return CQB_ERR_INVALID_ARGUMENT;
+  if (ctx->xmode != 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_xch_window first");
+  CK(cudaSetDevice(ctx->device));
+  for (int r = 0; r < ctx->xw; ++r) {
+    if (r == ctx->xrank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->xpeer[r] = static_cast<unsigned long long*>(p);
+  }
+  CK(cudaDeviceSynchronize());
+  return CQB_OK;
+}
+
+int cqb_xch_emulate(cqb_ctx* ctx, int vranks) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (vranks < 1 || vranks > XMAX)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "exchange: %d emulated ranks (1..%d)", vranks, XMAX);
+  CK(cudaSetDevice(ctx->device));
+  TRY(xch_reset(ctx));
+  if (loop_grid(ctx) < vranks * vranks) return fail(ctx, CQB_ERR_UNSUPPORTED, "grid too small for %d ranks", vranks);
+  CK(cudaMalloc(&ctx->xwin, XB_LAB_OFF * (size_t)vranks));  // no label region: the groups share the labels
+  CK(cudaMemset(ctx->xwin, 0, XB_LAB_OFF * (size_t)vranks));
+  CK(cudaMalloc(&ctx->xacc, sizeof(unsigned long long) * 5 * KMAX * (size_t)vranks));
+  for (int r = 0; r < vranks; ++r) ctx->xpeer[r] = ctx->xwin + (XB_LAB_OFF / sizeof(unsigned long long)) * r;
+  ctx->xmode = 2;
+  ctx->xw = vranks;
+  ctx->xrank = -1;
+  return CQB_OK;
+}
+
+int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int k, const cqb_termination* term,
+                         uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (ctx->xmode == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_xch_window + cqb_xch_open (or cqb_xch_emulate) first");
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  if (n_pixels == 0 || !d_rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize: empty image");
+  if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  if (!aligned16(d_rgb) || (d_index_out && !aligned16(d_index_out)) || (d_rgb_out && !aligned16(d_rgb_out)))
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "sharded quantize: device buffers must be 16-B aligned");
+  CK(cudaSetDevice(ctx->device));
+  TRY(ensure_pixels(ctx, n_pixels));
+  // pixel range of this rank (multiples of 16 pixels; the emulated ranks share one process: all pixels)
+  const int W = ctx->xmode == 1 ? ctx->xw : 1, r = ctx->xmode == 1 ? ctx->xrank : 0;
+  const uint64_t q = (n_pixels + 15) / 16;
+  ctx->px_lo = std::min(n_pixels, q * (uint64_t)r / (uint64_t)W * 16);
+  ctx->px_hi = r == W - 1 ? n_pixels : std::min(n_pixels, q * (uint64_t)(r + 1) / (uint64_t)W * 16);
+  if (px_range) {
+    px_range[0] = ctx->px_lo;
+    px_range[1] = ctx->px_hi;
+  }
+  ctx->xsharded = true;
+  const int rc = enqueue_quantize(ctx, d_rgb, n_pixels, k, term, seed, d_index_out, d_rgb_out, k + 64);
+  ctx->xsharded = false;
+  return rc;
 }
 
 }  // extern "C"

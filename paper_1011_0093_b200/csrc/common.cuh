@@ -19,6 +19,7 @@ constexpr int TILE_PX = HIST_THREADS * PX_PER_THREAD;  // pixels per compaction 
 constexpr int ST_OK = 0;
 constexpr int ST_K_EXCEEDS_N = 1;    // init_centers: k > N' (kmeans.hpp:55-56)
 constexpr int ST_DRAWS_EXHAUSTED = 2;
+constexpr int ST_XCH_TIMEOUT = 3;    // sharded loop: a peer did not publish within XCH_TIMEOUT_NS
 
 // Squared Euclidean distance exactly as color.hpp:49-54 evaluates it:
 // ((dr*dr + dg*dg) + db*db) in FP64, every operation rounded, NO FMA.
@@ -81,12 +82,20 @@ __device__ __forceinline__ bool one_color_cluster(unsigned long long N, unsigned
 }
 // The correction only matters when the exact mean is an integer (a one-color
 // cluster's mean is its color), so the moments are re-read on that rare path.
+// Moment loads: global sums through L2 (written by other blocks' atomics), or
+// (kShared) the sharded loop's totals in shared memory.
+template <bool kShared>
+__device__ __forceinline__ unsigned long long ldmom(const unsigned long long* p) {
+  if constexpr (kShared) return *p;
+  else return __ldcg(p);
+}
+template <bool kShared = false>
 __device__ __forceinline__ double center_coord(const unsigned long long* __restrict__ mom, int stride, int t,
                                                unsigned long long Sv, unsigned long long N, double inv_P) {
   const double c = __ddiv_rn((double)Sv, (double)N);
   if (c == rint(c) &&
-      one_color_cluster(N, __ldcg(&mom[t]), __ldcg(&mom[stride + t]), __ldcg(&mom[2 * stride + t]),
-                        __ldcg(&mom[4 * stride + t]))) {
+      one_color_cluster(N, ldmom<kShared>(&mom[t]), ldmom<kShared>(&mom[stride + t]),
+                        ldmom<kShared>(&mom[2 * stride + t]), ldmom<kShared>(&mom[4 * stride + t]))) {
     const double w = __dmul_rn((double)N, inv_P);
     return __ddiv_rn(__dmul_rn(w, c), w);
   }

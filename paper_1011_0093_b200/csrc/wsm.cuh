@@ -96,6 +96,17 @@ struct LoopParams {
   int debug_flags;   // diagnostics only (tools/ablate.py): 1 = skip the candidate scan (results wrong)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
   int stamp_iter;
+  // Sharded loop with the moment exchange inside the kernel (xch.cuh; X != 0
+  // instantiations only): xw ranks, each owning the contiguous sample range
+  // shard_range(N', xw, rank). xrank >= 0: one process per GPU, this is rank
+  // xrank and xbox[r] is rank r's exchange window mapped over NVLink (IPC).
+  // xrank < 0: xw block groups of this one cooperative launch act as the
+  // ranks (single-GPU emulation), xbox[g] = group g's window, xacc the
+  // groups' moment sums [xw][5*KMAX].
+  int xw;
+  int xrank;
+  unsigned long long* xbox[8];
+  unsigned long long* xacc;
 };
 
 // ---------------------------------------------------------------------------
@@ -268,6 +279,7 @@ struct LoopSmem {
   unsigned long long barv;               // grid barrier: the counter value that released this block
   int stop_flag;                         // block 0: stop after this iteration
   unsigned long long* stamp;             // profiling: block_times in the stamped iteration, else null
+  unsigned int part_b, part_g;           // emulated ranks (X == 2): block index in its group, group size
 };
 #define SUB_STAMP(phase)                                                         \
   do {                                                                           \
@@ -421,6 +433,19 @@ __device__ __forceinline__ void acc_point(uint2* acc, int k, uint32_t key, uint3
 // shared-memory reads, little divergence), while the round-robin spreads the
 // expensive regions (Voronoi boundaries) evenly over the blocks.
 __device__ __forceinline__ unsigned long long grid_threads() { return (unsigned long long)gridDim.x * blockDim.x; }
+// The block's part of the grid: the whole grid, or (X == 2, emulated ranks)
+// block group blockIdx.x / (gridDim.x / xw). Read from the special registers
+// at each use, so the X == 0 kernels keep no extra live registers.
+template <int X>
+__device__ __forceinline__ unsigned int part_size(const LoopSmem& S) {
+  if constexpr (X == 2) return S.part_g;
+  else return gridDim.x;
+}
+template <int X>
+__device__ __forceinline__ unsigned int part_block(const LoopSmem& S) {
+  if constexpr (X == 2) return S.part_b;
+  else return blockIdx.x;
+}
 
 // Full accumulation of one point per lane; when every valid lane of the warp
 // carries the same label (the common case in Morton order) the five moments
@@ -510,16 +535,18 @@ __global__ void __launch_bounds__(KMAX) k_grid_cands(const WsmState* __restrict_
 }
 
 // Iteration 1, dense + integer-exact (see header). Full accumulation.
+template <int X>
 __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned long long lo, unsigned long long hi,
                                    unsigned long long& evals) {
+  const unsigned int pb = part_block<X>(S), pG = part_size<X>(S);
   const int k = L.k;
   const unsigned long long bhi = hi;
-  const unsigned long long T = grid_threads();
+  const unsigned long long T = (unsigned long long)pG * blockDim.x;
   const int lane = threadIdx.x & 31;
   const int cc0 = S.cb[0].y >> 8;  // |c_0|^2
   const uint32_t c0 = (uint32_t)S.cb[0].x;
   constexpr int PPT = 4;
-  for (unsigned long long base = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; base - lane < bhi;
+  for (unsigned long long base = lo + (unsigned long long)pb * blockDim.x + threadIdx.x; base - lane < bhi;
        base += PPT * T) {
     uint32_t x[PPT];
     int best[PPT];
@@ -663,10 +690,11 @@ constexpr int DEEP_J = CQB_DEEP_J;
 #endif
 constexpr int DEEP_P = CQB_DEEP_P;
 
-template <Assign Mode, int PPT>
+template <Assign Mode, int PPT, int X>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
+  const unsigned int pb = part_block<X>(S), pG = part_size<X>(S);
   // Lane-local scan; 32-bit indexing (N' <= 2^24). The break index J is found
   // by exponential + binary search in the sorted row (most points stop at
   // J = 1 after one comparison), then the J - 1 candidates are evaluated.
@@ -680,12 +708,12 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   // chunks are handed to the warps dynamically (shared counter), PPT at a
   // time (small sample sets: longest first, sched_sort): a warp held up by
   // deep scans does not hold up the block.
-  const uint32_t G = gridDim.x, W = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const uint32_t G = pG, W = blockDim.x >> 5, w = threadIdx.x >> 5;
   const uint32_t nch = (hi - lo + 31u) >> 5;
   // small sample sets: chunk costs recorded for the longest-first order
   constexpr bool kSched = Mode == Assign::SortMeans && PPT == 1;
   constexpr bool kDeep = Mode == Assign::SortMeans;
-  const uint32_t my_ch = nch > blockIdx.x ? (nch - 1u - blockIdx.x) / G + 1u : 0u;
+  const uint32_t my_ch = nch > pb ? (nch - 1u - pb) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const uint8_t* __restrict__ go = L.st->order;
   const uint32_t* __restrict__ keys = L.keys;
@@ -709,7 +737,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       uint32_t jj = j + q;
       if (sched && jj < my_ch) jj = chunk_sched().order[jj];
       chunk[q] = jj;
-      const uint32_t i = lo + ((blockIdx.x + G * jj) << 5) + lane;
+      const uint32_t i = lo + ((pb + G * jj) << 5) + lane;
       const bool v = jj < my_ch && i < hi;
       idx[q] = v ? i : hi;
       key[q] = v ? keys[i] : 0u;
@@ -911,19 +939,80 @@ __device__ __forceinline__ bool cand_better(double d, unsigned int i, double bd,
   return d > bd || (d == bd && i < bi);
 }
 
+// ---------------------------------------------------------------------------
+// In-kernel exchange between ranks (sharded loop, BASELINE config 4).
+//
+// Each rank owns an exchange window (XB_BYTES, cudaMalloc'd, exported by IPC
+// handle so every peer maps it over NVLink/NVSwitch):
+//   u64 flag[src]   at XB_FLAG + 16*src  (own 128-B line per source)
+//   u64 seq         at XB_SEQ            (this rank's exchange counter, kept across launches)
+//   u64 payload[2][XMAX][5*KMAX] at XB_PAY  (slot parity = exchange number & 1)
+//   u8  labels[2^24] at byte XB_LAB_OFF  (the rank's sample labels; all-gathered at the end)
+// Exchange number s: every source writes its payload into slot s&1 of every
+// rank's window with plain stores, then (one thread, after bar.sync) a
+// sys-scope acq_rel fence and a relaxed store of s into flag[source]; a
+// receiver polls its own flags with sys-scope acquire loads until all are
+// >= s and reads the payload from L2 (ld.cg). Slot s&1 is rewritten only by
+// exchange s+2, which a source starts after receiving this rank's exchange
+// s+1, sent after this rank finished reading exchange s; so two slots
+// suffice, and the monotonic counters need no reset between launches (every
+// rank makes the same exchanges: the decisions are computed from identical
+// totals). One exchange per iteration carries the K x 5 exact moment sums;
+// the rare empty-cluster reseed adds one per empty cluster (its candidate).
+constexpr int XMAX = 8;
+constexpr int XB_FLAG = 0;
+constexpr int XB_SEQ = XMAX * 16;
+constexpr int XB_PAY = XB_SEQ + 128;
+constexpr int XB_SLOT = 5 * KMAX;
+constexpr size_t XB_LAB_OFF = 256 * 1024;
+constexpr size_t XB_BYTES = XB_LAB_OFF + (size_t(1) << 24);
+static_assert((XB_PAY + 2 * XMAX * XB_SLOT) * sizeof(unsigned long long) <= XB_LAB_OFF, "window layout");
+constexpr unsigned long long XCH_TIMEOUT_NS = 5000000000ull;  // a dead peer fails the call instead of hanging
+
+__device__ __forceinline__ unsigned long long* xpay(unsigned long long* box, unsigned long long s, int src) {
+  return box + XB_PAY + ((size_t)(s & 1) * XMAX + src) * XB_SLOT;
+}
+// Thread 0 only, after the payload stores are ordered by bar.sync: publish s.
+__device__ __forceinline__ void xch_signal(unsigned long long* box, int src, unsigned long long s) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(box + XB_FLAG + 16 * src), "l"(s) : "memory");
+}
+// Block-wide: wait until all xw sources published exchange s into `box`.
+__device__ __forceinline__ void xch_wait(unsigned long long* box, int xw, unsigned long long s, int* status) {
+  if (threadIdx.x < (unsigned)xw) {
+    const unsigned long long* f = box + XB_FLAG + 16 * threadIdx.x;
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= s) break;
+      if (*reinterpret_cast<volatile int*>(status) == ST_XCH_TIMEOUT) break;
+      if (globaltimer() - t0 > XCH_TIMEOUT_NS) {
+        atomicExch(status, ST_XCH_TIMEOUT);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // Empty-cluster reseed (kmeans.hpp:268-290), grid-wide, all blocks agree.
 // Candidates are ordered by (distance desc, first-occurrence rank asc): the
 // reference's strict '>' scan in sample order. Unique colors are distinct, so
-// "color already taken" is "rank already taken".
+// "color already taken" is "rank already taken". Sharded (X != 0): each part
+// (rank) reduces its own candidates, the parts exchange them (xch above) and
+// every block picks the same global best.
+template <int X>
 __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long lo,
-                             unsigned long long hi) {
+                             unsigned long long hi, int part, unsigned long long& xs) {
   WsmState* st = L.st;
+  const unsigned int pb = part_block<X>(S), pG = part_size<X>(S);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long T = (unsigned long long)pG * blockDim.x;
   for (int e = 0; e < S.n_empty; ++e) {
     double bd = -1.0;
     unsigned int bi = 0xffffffffu, bk = 0u;
-    for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += T) {
+    for (unsigned long long i = lo + (unsigned long long)pb * blockDim.x + threadIdx.x; i < hi; i += T) {
       const unsigned int rk = L.rank[i];
       bool used = false;
       for (int t = 0; t < e; ++t) used |= (S.taken[t] == rk);
@@ -969,10 +1058,34 @@ __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& g
       st->cand_k[e & 1][blockIdx.x] = xk;
     }
     grid.sync();
-    if (threadIdx.x == 0) {
-      double xd = -1.0;
-      unsigned int xi = 0xffffffffu, xk = 0u;
-      for (unsigned int b = 0; b < gridDim.x; ++b) {
+    if constexpr (X == 0) {
+      if (threadIdx.x == 0) {
+        double xd = -1.0;
+        unsigned int xi = 0xffffffffu, xk = 0u;
+        for (unsigned int b = 0; b < gridDim.x; ++b) {
+          const double d = __longlong_as_double((long long)st->cand_d[e & 1][b]);
+          const unsigned int i = st->cand_i[e & 1][b];
+          if (cand_better(d, i, xd, xi)) {
+            xd = d;
+            xi = i;
+            xk = st->cand_k[e & 1][b];
+          }
+        }
+        S.taken[e] = xi;
+        const int ke = S.empty_list[e];
+        S.nx[ke] = (double)key_r(xk);
+        S.ny[ke] = (double)key_g(xk);
+        S.nz[ke] = (double)key_b(xk);
+      }
+      __syncthreads();
+      continue;
+    }
+    // this part's blocks are [blockIdx.x - pb, blockIdx.x - pb + pG)
+    const unsigned int b0 = blockIdx.x - pb, nb = pG;
+    double xd = -1.0;
+    unsigned int xi = 0xffffffffu, xk = 0u;
+    if (threadIdx.x == 0 && pb == 0) {
+      for (unsigned int b = b0; b < b0 + nb; ++b) {
         const double d = __longlong_as_double((long long)st->cand_d[e & 1][b]);
         const unsigned int i = st->cand_i[e & 1][b];
         if (cand_better(d, i, xd, xi)) {
@@ -981,6 +1094,36 @@ __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& g
           xk = st->cand_k[e & 1][b];
         }
       }
+    }
+    if constexpr (X != 0) {
+      const unsigned long long s = ++xs;
+      if (threadIdx.x == 0 && pb == 0)
+        for (int r = 0; r < L.xw; ++r) {
+          unsigned long long* dst = xpay(L.xbox[r], s, part);
+          dst[0] = (unsigned long long)__double_as_longlong(xd);
+          dst[1] = xi;
+          dst[2] = xk;
+          xch_signal(L.xbox[r], part, s);
+        }
+      unsigned long long* own = L.xbox[part];
+      xch_wait(own, L.xw, s, &st->status);
+      if (threadIdx.x == 0) {
+        xd = -1.0;
+        xi = 0xffffffffu;
+        xk = 0u;
+        for (int r = 0; r < L.xw; ++r) {
+          const unsigned long long* src = xpay(own, s, r);
+          const double d = __longlong_as_double((long long)__ldcg(&src[0]));
+          const unsigned int i = (unsigned int)__ldcg(&src[1]);
+          if (cand_better(d, i, xd, xi)) {
+            xd = d;
+            xi = i;
+            xk = (unsigned int)__ldcg(&src[2]);
+          }
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
       S.taken[e] = xi;
       const int ke = S.empty_list[e];
       S.nx[ke] = (double)key_r(xk);
@@ -1004,7 +1147,9 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 }
 
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
-__device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n);
+template <int X>
+__device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
+                             unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs);
 
 // One instantiation per assignment variant (WSM, KM, FKM): a single kernel
 // with a runtime switch cost the WSM loop ~1.5% (register allocation).
@@ -1031,7 +1176,10 @@ __device__ __forceinline__ unsigned long long loop_barrier(LoopSmem& S, unsigned
   return S.barv;
 }
 
-template <Assign Mode, int PPT>
+// X: 0 = one rank (or a host-driven shard step); 1 = one process per GPU,
+// moments exchanged over NVLink inside the loop; 2 = the same exchange among
+// L.xw block groups of this launch (single-GPU emulation of the ranks).
+template <Assign Mode, int PPT, int X>
 __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
   __shared__ LoopSmem S;
@@ -1042,10 +1190,29 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   const int k = L.k;
   if (st->status != ST_OK) return;  // uniform across the grid
   const unsigned long long n = *L.n_ptr;
-  const unsigned long long lo = L.shard_lo < n ? L.shard_lo : n;
-  const unsigned long long hi = L.shard_hi_or_max < n ? L.shard_hi_or_max : n;
+  // this block's part of the grid: the whole grid, or (X == 2) block group
+  // `part` of xw; the part's ranks own shard_range(n, xw, part)
+  const int part = X == 2 ? (int)(blockIdx.x / (gridDim.x / (unsigned)L.xw)) : (X == 1 ? L.xrank : 0);
+  if (X == 2 && tid == 0) {
+    S.part_g = gridDim.x / (unsigned)L.xw;
+    S.part_b = blockIdx.x % S.part_g;
+  }
+  unsigned long long lo, hi;
+  if constexpr (X != 0) {
+    lo = n * (unsigned long long)part / (unsigned long long)L.xw;
+    hi = n * (unsigned long long)(part + 1) / (unsigned long long)L.xw;
+  } else {
+    lo = L.shard_lo < n ? L.shard_lo : n;
+    hi = L.shard_hi_or_max < n ? L.shard_hi_or_max : n;
+  }
   const double inv_P = 1.0 / (double)L.total;
-  unsigned long long* gacc = st->acc;  // exact running sums (zeroed by the host per launch)
+  // exact running sums of this rank's samples (zeroed by the host per launch)
+  unsigned long long* gacc = X == 2 ? L.xacc + (size_t)part * 5 * KMAX : st->acc;
+  // sharded: the totals over all ranks, rebuilt in shared memory every iteration
+  // (the block's delta arrays are idle between the flush and the next assign)
+  unsigned long long* tot = X ? reinterpret_cast<unsigned long long*>(S.accp) : gacc;
+  unsigned long long xs = 0;  // exchange counter (X != 0), identical in every block of every rank
+  if constexpr (X != 0) xs = __ldcg(L.xbox[part] + XB_SEQ);
   unsigned long long* tl = L.timeline;
   const bool rec = tl && blockIdx.x == 0 && tid == 0;
   // Sorted rows are read straight from the global tables: the warps are
@@ -1084,8 +1251,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   if (!kNaive) tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
-  unsigned long long pair_evals =
-      (kNaive || kFkm) ? 0ull : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
+  // (sharded over processes: counted by rank 0 only)
+  unsigned long long pair_evals = (kNaive || kFkm || (X == 1 && L.xrank != 0))
+                                      ? 0ull
+                                      : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
   if (CQB_LOOP_BARRIER && blockIdx.x == 0 && tid == 0) st->bar = 0ull;  // before the prologue barrier
   grid.sync();
   unsigned int bar_target = 0;  // loop_barrier episodes x G
@@ -1106,17 +1275,17 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       __syncthreads();
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       if constexpr (Mode == Assign::SortMeans) {
-        assign_dense_first(S, L, lo, hi, evals);
+        assign_dense_first<X>(S, L, lo, hi, evals);
       } else {  // KM / FKM: the host accounts P*k for iteration 1
         unsigned long long ev_dense = 0;
-        assign_dense_first(S, L, lo, hi, ev_dense);
+        assign_dense_first<X>(S, L, lo, hi, ev_dense);
       }
     } else {
       __syncthreads();
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means<Mode, PPT>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      assign_sort_means<Mode, PPT, X>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -1135,7 +1304,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     // 2, 4, 8, ... (costs drift slowly; the sort is not free)
     if (Mode == Assign::SortMeans && PPT == 1 && it >= 2 && (it & (it - 1)) == 0) {
       const unsigned long long nn = hi - lo, nch = (nn + 31) >> 5;
-      const uint32_t my_ch = nch > blockIdx.x ? (uint32_t)((nch - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+      const uint32_t pb = part_block<X>(S), pG = part_size<X>(S);
+      const uint32_t my_ch = nch > pb ? (uint32_t)((nch - 1 - pb) / pG + 1) : 0u;
       if (my_ch <= (uint32_t)SCHED_MAX) sched_sort(my_ch);
     }
     if (rec_it) tl[(it - 1) * 8 + 3] = globaltimer();
@@ -1149,6 +1319,26 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     if (rec_it) tl[(it - 1) * 8 + 4] = globaltimer();
     BLOCK_STAMP(3);
     if (L.moments_only) break;
+    if constexpr (X != 0) {  // all-reduce of the K x 5 moment sums over the ranks
+      const unsigned long long s = ++xs;
+      const unsigned int pb = part_block<X>(S);
+      if (pb < (unsigned)L.xw) {  // block pb of every part sends to rank pb
+        unsigned long long* dst = xpay(L.xbox[pb], s, part);
+        for (int e = tid; e < 5 * KMAX; e += blockDim.x)
+          if ((e & (KMAX - 1)) < k) dst[e] = __ldcg(&gacc[e]);
+        __syncthreads();
+        if (tid == 0) xch_signal(L.xbox[pb], part, s);
+      }
+      unsigned long long* own = L.xbox[part];
+      xch_wait(own, L.xw, s, &st->status);
+      for (int e = tid; e < 5 * KMAX; e += blockDim.x)
+        if ((e & (KMAX - 1)) < k) {
+          unsigned long long a = 0;
+          for (int r = 0; r < L.xw; ++r) a += __ldcg(xpay(own, s, r) + e);
+          tot[e] = a;
+        }
+      __syncthreads();
+    }
 
     // ---------------- finalize(it) ----------------
     // Every block: new centers S/N (FP64, exact integer inputs) + empty count.
@@ -1159,11 +1349,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     for (int u = tid; u < 3 * KMAX; u += blockDim.x) {
       const int ch = u / KMAX, t = u % KMAX;
       if (t < k) {
-        const unsigned long long N = __ldcg(&gacc[3 * KMAX + t]);
-        const unsigned long long Sv = __ldcg(&gacc[ch * KMAX + t]);
+        const unsigned long long N = ldmom<X != 0>(&tot[3 * KMAX + t]);
+        const unsigned long long Sv = ldmom<X != 0>(&tot[ch * KMAX + t]);
         if (N) {
           double* dst = ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz);
-          dst[t] = center_coord(gacc, KMAX, t, Sv, N, inv_P);
+          dst[t] = center_coord<X != 0>(tot, KMAX, t, Sv, N, inv_P);
         } else if (ch == 0) {
           empt_local = 1;
         }
@@ -1176,10 +1366,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         S.n_empty = empt;
         int m = 0;
         for (int t = 0; t < k; ++t)
-          if (gacc[3 * KMAX + t] == 0ull) S.empty_list[m++] = t;
+          if (ldmom<X != 0>(&tot[3 * KMAX + t]) == 0ull) S.empty_list[m++] = t;
       }
       __syncthreads();
-      reseed_empty(S, L, grid, lo, hi);
+      reseed_empty<X>(S, L, grid, lo, hi, part, xs);
     }
     // Block 0: moment-form SSE, termination (kmeans.hpp:359-369), reporting.
     if (blockIdx.x == 0) {
@@ -1188,9 +1378,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (tid < k) {
         const int t = tid;
         moved += (S.nx[t] != S.cx[t]) | (S.ny[t] != S.cy[t]) | (S.nz[t] != S.cz[t]);
-        const unsigned long long mN = __ldcg(&gacc[3 * KMAX + t]);
-        const unsigned long long mS0 = __ldcg(&gacc[0 * KMAX + t]), mS1 = __ldcg(&gacc[1 * KMAX + t]);
-        const unsigned long long mS2 = __ldcg(&gacc[2 * KMAX + t]), mQ = __ldcg(&gacc[4 * KMAX + t]);
+        const unsigned long long mN = ldmom<X != 0>(&tot[3 * KMAX + t]);
+        const unsigned long long mS0 = ldmom<X != 0>(&tot[0 * KMAX + t]), mS1 = ldmom<X != 0>(&tot[1 * KMAX + t]);
+        const unsigned long long mS2 = ldmom<X != 0>(&tot[2 * KMAX + t]), mQ = ldmom<X != 0>(&tot[4 * KMAX + t]);
         if (mN) {
           const double dn = (double)mN;
           const double Sr = (double)mS0, Sg = (double)mS1;
@@ -1246,6 +1436,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     }
     __syncthreads();
     BLOCK_STAMP(9);
+    if constexpr (X != 0)  // the delta accumulators again
+      for (int e = tid; e < 5 * KMAX; e += blockDim.x) tot[e] = 0ull;
     for (int t = tid; t < k; t += blockDim.x) {
       S.cx[t] = S.nx[t];
       S.cy[t] = S.ny[t];
@@ -1278,7 +1470,14 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += S.red_u64[w];
     atomicAdd(&st->evals, tot);
   }
-  if (L.map_lut) map_epilogue(S, L, grid, hi);
+  if constexpr (X != 0)
+    if (part_block<X>(S) == 0 && tid == 0) L.xbox[part][XB_SEQ] = xs + (L.map_lut ? 1ull : 0ull);  // + the epilogue's exchange
+  if constexpr (X != 0) {
+    if (L.map_lut) map_epilogue<X>(S, L, grid, n, lo, hi, part, xs);
+  } else {
+    unsigned long long none = 0;
+    if (L.map_lut) map_epilogue<0>(S, L, grid, hi, 0, 0, 0, none);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1289,8 +1488,19 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
 // color's exact argmin over the rounded palette from its final label with the
 // strict break d(R_p, R_t) > 4 prev, the key -> index LUT and the exact
 // u64 sum of count x error. Saves two launches on the quantize path.
-__device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n) {
+template <int X>
+__device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
+                             unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs) {
   const int k = L.k, tid = threadIdx.x;
+  if constexpr (X == 1) {  // all-gather of the labels: this rank's range into every peer's window
+    const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
+    for (int r = 0; r < L.xw; ++r) {
+      if (r == part) continue;
+      uint8_t* dst = reinterpret_cast<uint8_t*>(L.xbox[r]) + XB_LAB_OFF;
+      for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + tid; i < hi; i += T)
+        dst[i] = L.labels[i];
+    }
+  }
   const double* C = L.st->final_C;
   uint32_t* s_key = S.row0;        // rounded palette keys
   int* s_cc = S.empty_list;        // |R_t|^2
@@ -1332,12 +1542,19 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
     }
   }
   grid.sync();
+  if constexpr (X != 0) {  // every rank's labels are in place (emulated: shared array, the round is kept)
+    const unsigned long long s = ++xs;
+    const unsigned int pG = X == 2 ? gridDim.x / (unsigned)L.xw : gridDim.x;
+    if (tid == 0 && blockIdx.x % pG == 0)
+      for (int r = 0; r < L.xw; ++r) xch_signal(L.xbox[r], part, s);
+    xch_wait(L.xbox[part], L.xw, s, &L.st->status);
+  }
   unsigned long long err = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t x = L.keys[i];
     const int xx = key_dot(x, x);
-    const int p = L.labels[i];
+    const int p = X ? (int)__ldcg(&L.labels[i]) : (int)L.labels[i];
     const int prev = xx + s_cc[p] - 2 * key_dot(x, s_key[p]);
     const int bound = 4 * prev;
     int mind = prev, best = p;

@@ -218,3 +218,72 @@ def run_wsm_sharded(backend, img: np.ndarray, k: int, mode: int = 1, max_iters: 
     total_evals = coll.allreduce_sum(np.array([evals], np.uint64))[0]
     res.centers, res.iterations, res.sse, res.dist_evals = Cur, it, res.sse_history[-1], int(total_evals)
     return res
+
+
+# --------------------------------------------------------------------------- in-kernel exchange
+class PeerShardedQuantizer:
+    """Config 4 across GPUs with the moment exchange INSIDE the persistent
+    loop kernel (cqb_quantize_sharded): one process per GPU, each rank's loop
+    writes its K x 5 exact moment sums into every peer's exchange window over
+    NVLink once per iteration and sums the world's contributions itself — no
+    host round trip and no collective call per iteration. The windows are
+    cudaIpc-shared; torch.distributed only all-gathers the handles once.
+
+    ``emulate=W`` (single GPU, tests): W block groups of the one cooperative
+    launch act as the W ranks, with the same windows, flags and exchange code.
+    """
+
+    def __init__(self, ctx=None, group=None, emulate: int = 0, device: int = 0):
+        from . import _native
+
+        self.ctx = ctx or _native.context(device)
+        self.lib = self.ctx.lib
+        if emulate:
+            self.world, self.rank, self.emulated = emulate, 0, True
+            self.ctx.check(self.lib.cqb_xch_emulate(self.ctx.h, emulate))
+            return
+        import torch.distributed as dist
+
+        single = not (dist.is_available() and dist.is_initialized())  # one rank: the X = 1 kernel alone
+        self.world = 1 if single else dist.get_world_size(group)
+        self.rank = 0 if single else dist.get_rank(group)
+        self.emulated = False
+        h = (C.c_ubyte * _native.IPC_HANDLE_BYTES)()
+        self.ctx.check(self.lib.cqb_xch_window(self.ctx.h, self.world, self.rank, h))
+        handles = [bytes(h)] if single else exchange_handles(bytes(h), group)
+        buf = C.create_string_buffer(b"".join(handles), len(handles) * _native.IPC_HANDLE_BYTES)
+        self.ctx.check(self.lib.cqb_xch_open(self.ctx.h, buf))
+
+    def enqueue(self, d_rgb: int, n_pixels: int, k: int, term, seed: int = 1, d_index: int | None = None,
+                d_rgb_out: int | None = None) -> tuple[int, int]:
+        """Enqueue one sharded quantize on the context stream (device
+        pointers); returns the pixel range this rank maps."""
+        rng = np.zeros(2, np.uint64)
+        t = term.native()
+        self.ctx.check(self.lib.cqb_quantize_sharded(self.ctx.h, d_rgb, n_pixels, k, C.byref(t), seed, d_index,
+                                                     d_rgb_out, rng.ctypes.data_as(_u64p)))
+        self._k, self._cap = k, term.iteration_budget
+        return int(rng[0]), int(rng[1])
+
+    def fetch(self):
+        """Wait; return (centers [k,3], report, sse_history). report.dist_evals
+        is this rank's share (sum over ranks for the reference's count)."""
+        from . import _native as N
+
+        k, cap = self._k, self._cap
+        centers = np.zeros(3 * k)
+        hist = np.zeros(cap)
+        rep = N.Report()
+        self.ctx.check(self.lib.cqb_fetch_results(self.ctx.h, centers.ctypes.data_as(_f64p),
+                                                  hist.ctypes.data_as(_f64p), cap, C.byref(rep)))
+        return centers.reshape(k, 3), rep, hist[: rep.iterations].copy()
+
+
+def exchange_handles(handle: bytes, group=None) -> list[bytes]:
+    """All-gather of the ranks' IPC handles, in rank order (host plumbing)."""
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    assert all(isinstance(h, bytes) and len(h) == len(handle) for h in out)
+    return out

@@ -9,6 +9,7 @@ SSE history — including the empty-cluster reseed exchanged via allgather.
 import ctypes as C
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -220,3 +221,74 @@ def test_gloo_world2_empty_cluster_reseed(port):
         np.testing.assert_array_equal(centers, traj[-1])
     # the far center was re-seeded onto a sample color in iteration 1
     assert tuple(traj[0][4]) != (999.0, 999.0, 999.0)
+
+
+# --------------------------------------------------------------------------- in-kernel exchange (host side)
+def _handle_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200.distributed import exchange_handles
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = bytes([rank]) * 64  # stands in for this rank's cudaIpcMemHandle_t
+        out_q.put((rank, exchange_handles(mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_ipc_handles_in_rank_order():
+    """PeerShardedQuantizer's setup: every rank receives all windows' IPC
+    handles in rank order (cqb_xch_open indexes them by rank)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handle_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=240) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, hs in outs:
+        assert hs == [bytes([0]) * 64, bytes([1]) * 64]
+
+
+def test_exchange_protocol_two_slots_suffice():
+    """Model of the in-kernel exchange (wsm.cuh, XB_* windows): each rank
+    writes exchange s into slot s&1 of every window, publishes flag = s, waits
+    for all flags >= s, then reads and sums. With ranks running at arbitrary
+    relative speeds no slot is overwritten before its reader is done, so every
+    rank sums exactly the values of exchange s."""
+    import random
+    import threading
+
+    W, N = 4, 300
+    flags = [[0] * W for _ in range(W)]
+    pay = [[[None] * W for _ in range(2)] for _ in range(W)]
+    errors = []
+
+    def rank(r):
+        rnd = random.Random(r)
+        for s in range(1, N + 1):
+            for dst in range(W):  # payload, then flag (release order)
+                pay[dst][s & 1][r] = (s, r)
+                flags[dst][r] = s
+                if rnd.random() < 0.3:
+                    time.sleep(0)
+            while min(flags[r]) < s:
+                time.sleep(0)
+            got = [pay[r][s & 1][src] for src in range(W)]
+            if got != [(s, src) for src in range(W)]:
+                errors.append((r, s, got))
+            if rnd.random() < 0.2:
+                time.sleep(0.0005)
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(W)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[:3]

@@ -30,3 +30,92 @@ def test_device_shards_k256_uniform(port):
     assert res.iterations == single.report.iterations
     np.testing.assert_array_equal(res.centers, single.palette)
     assert res.dist_evals == single.report.dist_evals
+
+
+# --------------------------------------------------------------------------- in-kernel exchange
+def _sharded_run(img, k, world, term=None, seed=1):
+    """cqb_quantize_sharded with `world` emulated ranks (block groups of one
+    cooperative launch; world = 0: the one-process X = 1 kernel, exchanging
+    with itself). Returns (centers, report, sse_history, index map, mapped)."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    term = term or api.Termination.convergent(1e-4, 100)
+    P = img.shape[0] * img.shape[1]
+    ctx = _native.Context(0)
+    q = PeerShardedQuantizer(ctx=ctx, emulate=world)
+    d_img = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+    d_idx = torch.empty(P, dtype=torch.uint8, device="cuda")
+    d_rgb = torch.empty(3 * P, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    lo, hi = q.enqueue(d_img.data_ptr(), P, k, term, seed, d_idx.data_ptr(), d_rgb.data_ptr())
+    assert (lo, hi) == (0, P)
+    centers, rep, hist = q.fetch()
+    out = (centers, rep, hist, d_idx.cpu().numpy().reshape(img.shape[:2]), d_rgb.cpu().numpy().reshape(img.shape))
+    ctx.close()
+    return out
+
+
+@pytest.mark.parametrize("world", [0, 1, 2, 3, 8])
+@pytest.mark.parametrize("case", ["gmm", "uniform"])
+def test_in_kernel_exchange_matches_single_gpu(world, case):
+    """The sharded loop with the moment exchange inside the kernel gives the
+    single-GPU quantize bit for bit: palette, iterations, SSE history,
+    dist_evals, index map, mapped raster and MSE (exact integer moments)."""
+    img = gmm_image(384, 256, 48, 5) if case == "gmm" else uniform_image(1024, 2048, 9)  # small / large paths
+    k = 64 if case == "gmm" else 256
+    single = api.quantize(img, k, api.Termination.convergent(1e-4, 100), seed=1)
+    centers, rep, hist, idx, mapped = _sharded_run(img, k, world)
+    np.testing.assert_array_equal(centers, single.palette)
+    assert rep.iterations == single.report.iterations
+    assert rep.dist_evals == single.report.dist_evals
+    assert rep.n_unique == single.report.n_unique
+    np.testing.assert_array_equal(hist, np.asarray(single.report.sse_history))
+    np.testing.assert_array_equal(idx, single.index_map)
+    np.testing.assert_array_equal(mapped, single.mapped)
+    assert rep.mse == single.report.mse
+
+
+def test_in_kernel_exchange_fixed_iterations_and_repeat():
+    """Fixed termination, and two calls in a row on one context (the exchange
+    counters carry over between launches)."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    img = gmm_image(256, 128, 24, 11)
+    term = api.Termination.fixed(7)
+    single = api.quantize(img, 32, term, seed=3)
+    ctx = _native.Context(0)
+    q = PeerShardedQuantizer(ctx=ctx, emulate=4)
+    d_img = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        q.enqueue(d_img.data_ptr(), img.shape[0] * img.shape[1], 32, term, 3)
+        centers, rep, _ = q.fetch()
+        np.testing.assert_array_equal(centers, single.palette)
+        assert rep.iterations == 7 and rep.dist_evals == single.report.dist_evals
+    ctx.close()
+
+
+@pytest.mark.parametrize("seed,comp,k", [(0, 3, 32), (28, 12, 128), (43, 6, 64)])
+@pytest.mark.parametrize("world", [2, 5])
+def test_in_kernel_exchange_empty_cluster_reseed(seed, comp, k, world, port):
+    """Runs whose trajectory empties clusters (found by tools/find_empty.py):
+    the reseed candidates go through the exchange, and the result equals the
+    single-GPU run and the oracle."""
+    img = gmm_image(48, 40, comp, seed)
+    single = api.quantize(img, k, api.Termination.convergent(1e-4, 100), seed=seed)
+    assert single.report.empty_events > 0
+    centers, rep, hist, idx, mapped = _sharded_run(img, k, world, seed=seed)
+    np.testing.assert_array_equal(centers, single.palette)
+    assert rep.empty_events == single.report.empty_events
+    assert rep.iterations == single.report.iterations and rep.dist_evals == single.report.dist_evals
+    np.testing.assert_array_equal(idx, single.index_map)
+    h = port.build_histogram(img)
+    ref = port.run_wsm(h.keys, h.counts, 48 * 40, k, mode=1, eps=1e-4, cap=100, seed=seed)
+    assert rep.iterations == ref.iterations
+    np.testing.assert_allclose(centers, ref.centers, rtol=1e-12, atol=0)
