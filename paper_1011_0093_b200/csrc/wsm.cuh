@@ -1189,6 +1189,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   const int tid = threadIdx.x;
   const int k = L.k;
   if (st->status != ST_OK) return;  // uniform across the grid
+  if (L.block_times && tid == 0) L.block_times[12 * gridDim.x + blockIdx.x] = globaltimer();  // kernel entry
   const unsigned long long n = *L.n_ptr;
   // this block's part of the grid: the whole grid, or (X == 2) block group
   // `part` of xw; the part's ranks own shard_range(n, xw, part)
@@ -1459,6 +1460,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (*reinterpret_cast<volatile int*>(&st->stop_it) == it) break;
     }
   }
+  if (L.block_times && tid == 0) L.block_times[13 * gridDim.x + blockIdx.x] = globaltimer();  // loop exit
   // one evals flush per block (a per-warp atomic every iteration would
   // serialize thousands of same-address atomics in L2)
   evals = warp_sum(evals);
@@ -1478,6 +1480,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     unsigned long long none = 0;
     if (L.map_lut) map_epilogue<0>(S, L, grid, hi, 0, 0, 0, none);
   }
+  if (L.block_times && tid == 0) L.block_times[14 * gridDim.x + blockIdx.x] = globaltimer();  // kernel exit
 }
 
 // ---------------------------------------------------------------------------
