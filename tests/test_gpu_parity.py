@@ -246,7 +246,7 @@ def test_mse_known_answers(port):
 
 
 # --------------------------------------------------------------------------- end to end
-@pytest.mark.parametrize("case,k", [("gmm96x64", 16), ("gmm101x77", 8), ("cfg1", 32), ("cfg2", 256),
+@pytest.mark.parametrize("case,k", [("gmm96x64", 16), ("gmm101x77", 8), ("cfg1", 32), ("cfg2", 256), ("cfg2", 64),
                                     ("uniform256", 64)])
 def test_quantize_end_to_end(case, k, images, port):
     img = images[case]
@@ -337,6 +337,47 @@ def test_cfg4_properties(port):
     again, idx2, _ = api.map_pixels_indexed(q.mapped, q.palette)
     np.testing.assert_array_equal(again, q.mapped)
     assert q.report.mse == pytest.approx(api.mse(img, q.mapped), rel=0, abs=0)
+
+
+@pytest.mark.slow
+def test_cfg3_full_size(port):
+    """Config 3 (4096^2 value noise, ~2.6M unique colors) at full size:
+    histogram bit-exact, three fixed iterations against the oracle (exact:
+    P is a power of two), and the convergent run's size-independent
+    properties (nonincreasing SSE, idempotent mapping, exact MSE)."""
+    img = CONFIGS["cfg3"].image()
+    P = img.shape[0] * img.shape[1]
+    h = api.build_histogram(img)
+    o = port.build_histogram(img)
+    np.testing.assert_array_equal(h.keys, o.keys)
+    np.testing.assert_array_equal(h.counts, o.counts)
+    q3 = api.quantize(img, 256, api.Termination.fixed(3), seed=1, index_map=False, mapped=False)
+    r3 = port.run_wsm(o.keys, o.counts, P, 256, mode=0, max_iters=3, seed=1)
+    np.testing.assert_array_equal(q3.palette, r3.centers)
+    assert q3.report.dist_evals == r3.dist_evals
+    q = api.quantize(img, 256, api.Termination.convergent(1e-4, 100), seed=1)
+    hist = np.array(q.report.sse_history)
+    assert np.all(np.diff(hist) <= 1e-9 * hist[:-1])
+    again, _, _ = api.map_pixels_indexed(q.mapped, q.palette)
+    np.testing.assert_array_equal(again, q.mapped)
+    assert q.report.mse == api.mse(img, q.mapped)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [64, 256])
+def test_cfg5_image_matches_oracle(k, port):
+    """Config 5's first image (1024^2 GMM-256, seed 1000) through the batch
+    path equals the oracle's full convergent run (P is a power of two)."""
+    import torch
+
+    img = CONFIGS["cfg5"].image(0)
+    P = img.shape[0] * img.shape[1]
+    d = torch.from_numpy(img.reshape(-1)).cuda()
+    pal, reps = api.quantize_batch_device([d], k, api.Termination.convergent(1e-4, 100), seed=1, lanes=1)
+    h = port.build_histogram(img)
+    o = port.run_wsm(h.keys, h.counts, P, k, mode=1, eps=1e-4, cap=100, seed=1)
+    assert reps[0].iterations == o.iterations and reps[0].dist_evals == o.dist_evals
+    np.testing.assert_array_equal(pal[0], o.centers)
 
 
 # --------------------------------------------------------------------------- §8(f) f3: KM / KM-C

@@ -119,3 +119,19 @@ def test_in_kernel_exchange_empty_cluster_reseed(seed, comp, k, world, port):
     ref = port.run_wsm(h.keys, h.counts, 48 * 40, k, mode=1, eps=1e-4, cap=100, seed=seed)
     assert rep.iterations == ref.iterations
     np.testing.assert_allclose(centers, ref.centers, rtol=1e-12, atol=0)
+
+
+@pytest.mark.slow
+def test_in_kernel_exchange_cfg4_full_size():
+    """Config 4 (4096^2 uniform, 10.6M unique colors) with 8 emulated ranks:
+    the same palette, iteration count, dist_evals, MSE and index map as the
+    one-rank run."""
+    from paper_1011_0093_b200.configs import CONFIGS
+
+    img = CONFIGS["cfg4"].image()
+    single = api.quantize(img, 256, api.Termination.convergent(1e-4, 100), seed=1)
+    centers, rep, hist, idx, mapped = _sharded_run(img, 256, 8)
+    np.testing.assert_array_equal(centers, single.palette)
+    assert rep.iterations == single.report.iterations and rep.dist_evals == single.report.dist_evals
+    assert rep.mse == single.report.mse
+    np.testing.assert_array_equal(idx, single.index_map)
