@@ -311,6 +311,7 @@ int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
 // Images below this size compact the bin table through K1's occupancy map
 // (their tables are sparse: cfg2's 0.37M colors touch 2% of the bins).
 constexpr uint64_t OCC_MAX_PIXELS = 2u << 20;
+constexpr size_t RES_DYN_MAX = 160 * 1024;  // resident-sample loop: dynamic shared memory ceiling
 
 bool sparse_path(const cqb_ctx* ctx, uint64_t P) { return P < OCC_MAX_PIXELS && !(ctx->debug_flags & 16); }
 bool fused_prep(const cqb_ctx* ctx, uint64_t P) {
@@ -472,7 +473,17 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
                                                  : (const void*)k_wsm_loop<Assign::Fkm, 2, 0>)
                                         : (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 0>
                                                  : (const void*)k_wsm_loop<Assign::SortMeans, 2, 0>);
-  CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(LOOP_THREADS), args, LOOP_DYN_SMEM, ctx->stream));
+  size_t dyn = LOOP_DYN_SMEM;
+  if (X == 0 && small && !L.naive && L.fkm_kprime == 0 && !(ctx->debug_flags & 512)) {
+    // resident samples when the block's share (bounded by P) fits in shared memory
+    const uint64_t cap = ((total + 31) / 32 + grid - 1) / grid * 32;
+    if (res_smem_bytes((int)std::min<uint64_t>(cap, 1u << 24)) <= RES_DYN_MAX) {
+      L.res_cap = (int)cap;
+      dyn = res_smem_bytes(L.res_cap);
+      kern = (const void*)k_wsm_loop<Assign::SortMeans, 1, 0, true>;
+    }
+  }
+  CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(LOOP_THREADS), args, dyn, ctx->stream));
   CKL();
   return CQB_OK;
 }
@@ -607,6 +618,8 @@ int cqb_create(int device, cqb_ctx** out) {
                           (const void*)k_wsm_loop<Assign::SortMeans, 1, 1>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 1>,
                           (const void*)k_wsm_loop<Assign::SortMeans, 1, 2>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 2>})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
+    CK(cudaFuncSetAttribute((const void*)k_wsm_loop<Assign::SortMeans, 1, 0, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RES_DYN_MAX));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2, 0>, LOOP_THREADS,
                                                      LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");

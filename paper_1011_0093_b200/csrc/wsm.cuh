@@ -103,6 +103,7 @@ struct LoopParams {
   // xrank < 0: xw block groups of this one cooperative launch act as the
   // ranks (single-GPU emulation), xbox[g] = group g's window, xacc the
   // groups' moment sums [xw][5*KMAX].
+  int res_cap;  // resident-sample kernels: samples per block reserved in dynamic shared memory
   int xw;
   int xrank;
   unsigned long long* xbox[8];
@@ -647,6 +648,26 @@ __device__ __forceinline__ ChunkSched& chunk_sched() {
   extern __shared__ __align__(16) unsigned char loop_dyn[];
   return *reinterpret_cast<ChunkSched*>(loop_dyn);
 }
+// Resident samples (small sample sets): the block's chunks - its fixed share
+// of the Morton-ordered samples - stay in dynamic shared memory for the whole
+// loop (key, count, label; local index = chunk * 32 + lane), so a scan starts
+// without the L2 round trip for its sample. Global labels are still written
+// on every change (stores do not stall), so reseed, the map epilogue and the
+// API read them as before. Capacity: res_cap samples per block (host-sized).
+struct ResSamples {
+  uint32_t* key;
+  uint32_t* cnt;
+  uint8_t* lab;
+};
+__device__ __forceinline__ ResSamples res_samples(int cap) {
+  extern __shared__ __align__(16) unsigned char loop_dyn[];
+  unsigned char* b = loop_dyn + ((sizeof(ChunkSched) + 15) & ~size_t(15));
+  return {reinterpret_cast<uint32_t*>(b), reinterpret_cast<uint32_t*>(b) + cap,
+          reinterpret_cast<uint8_t*>(reinterpret_cast<uint32_t*>(b) + 2 * cap)};
+}
+__host__ __device__ constexpr size_t res_smem_bytes(int cap) {
+  return ((sizeof(ChunkSched) + 15) & ~size_t(15)) + (size_t)cap * 9;
+}
 
 // Counting sort of this block's chunks by cost, descending (block-wide).
 __device__ void sched_sort(uint32_t my_ch) {
@@ -690,7 +711,7 @@ constexpr int DEEP_J = CQB_DEEP_J;
 #endif
 constexpr int DEEP_P = CQB_DEEP_P;
 
-template <Assign Mode, int PPT, int X>
+template <Assign Mode, int PPT, int X, bool R>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
@@ -740,8 +761,15 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       const uint32_t i = lo + ((pb + G * jj) << 5) + lane;
       const bool v = jj < my_ch && i < hi;
       idx[q] = v ? i : hi;
-      key[q] = v ? keys[i] : 0u;
-      lab[q] = v ? (int)labels[i] : 0;
+      if constexpr (R) {
+        const ResSamples rs = res_samples(L.res_cap);
+        const uint32_t li = (jj << 5) + lane;
+        key[q] = v ? rs.key[li] : 0u;
+        lab[q] = v ? (int)rs.lab[li] : 0;
+      } else {
+        key[q] = v ? keys[i] : 0u;
+        lab[q] = v ? (int)labels[i] : 0;
+      }
     }
     uint32_t J_of[PPT];
 #pragma unroll
@@ -845,7 +873,14 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       const bool v = i < hi;
       const bool ch = v && nlab[q] != lab[q];
       uint32_t cnt = 0;
-      if (v && (full || ch)) cnt = counts[i];
+      if constexpr (R) {
+        const ResSamples rs = res_samples(L.res_cap);
+        const uint32_t li = (chunk[q] << 5) + lane;
+        if (v && (full || ch)) cnt = rs.cnt[li];
+        if (ch) rs.lab[li] = (uint8_t)nlab[q];
+      } else {
+        if (v && (full || ch)) cnt = counts[i];
+      }
       if (ch) {
         labels[i] = (uint8_t)nlab[q];
         ++n_changed;
@@ -1179,7 +1214,8 @@ __device__ __forceinline__ unsigned long long loop_barrier(LoopSmem& S, unsigned
 // X: 0 = one rank (or a host-driven shard step); 1 = one process per GPU,
 // moments exchanged over NVLink inside the loop; 2 = the same exchange among
 // L.xw block groups of this launch (single-GPU emulation of the ranks).
-template <Assign Mode, int PPT, int X>
+// R: resident samples (ResSamples; small sample sets, X == 0 only).
+template <Assign Mode, int PPT, int X, bool R = false>
 __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
   __shared__ LoopSmem S;
@@ -1249,6 +1285,19 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     L.block_times[7 * gridDim.x + blockIdx.x] = 0ull;
   }
   // prologue: tables of the initial centers (all pairs evaluated: non-incremental)
+  if constexpr (R) {  // the block's chunks into shared memory (labels: unless iteration 1 writes them)
+    const ResSamples rs = res_samples(L.res_cap);
+    const unsigned long long nch = (hi - lo + 31) >> 5;
+    const unsigned long long my = nch > blockIdx.x ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    for (unsigned long long li = tid; li < my * 32; li += blockDim.x) {
+      const unsigned long long i = lo + ((blockIdx.x + gridDim.x * (li >> 5)) << 5) + (li & 31);
+      if (i < hi) {
+        rs.key[li] = L.keys[i];
+        rs.cnt[li] = L.counts[i];
+        if (!L.dense_first) rs.lab[li] = L.labels[i];
+      }
+    }
+  }
   if (!kNaive) tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
@@ -1286,7 +1335,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means<Mode, PPT, X>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      assign_sort_means<Mode, PPT, X, R>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -1320,6 +1369,17 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     if (rec_it) tl[(it - 1) * 8 + 4] = globaltimer();
     BLOCK_STAMP(3);
     if (L.moments_only) break;
+    if constexpr (R) {
+      if (it == 1 && L.dense_first) {  // iteration 1 wrote the labels in its own (dense) order
+        const ResSamples rs = res_samples(L.res_cap);
+        const unsigned long long nch = (hi - lo + 31) >> 5;
+        const unsigned long long my = nch > blockIdx.x ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        for (unsigned long long li = tid; li < my * 32; li += blockDim.x) {
+          const unsigned long long i = lo + ((blockIdx.x + gridDim.x * (li >> 5)) << 5) + (li & 31);
+          if (i < hi) rs.lab[li] = __ldcg(&L.labels[i]);
+        }
+      }
+    }
     if constexpr (X != 0) {  // all-reduce of the K x 5 moment sums over the ranks
       const unsigned long long s = ++xs;
       const unsigned int pb = part_block<X>(S);
