@@ -102,6 +102,18 @@ __device__ __forceinline__ double center_coord(const unsigned long long* __restr
   return c;
 }
 
+// center_coord with all five moments of the cluster already in registers.
+__device__ __forceinline__ double center_coord_v(unsigned long long Sv, unsigned long long N, unsigned long long S0,
+                                                 unsigned long long S1, unsigned long long S2, unsigned long long Q,
+                                                 double inv_P) {
+  const double c = __ddiv_rn((double)Sv, (double)N);
+  if (c == rint(c) && one_color_cluster(N, S0, S1, S2, Q)) {
+    const double w = __dmul_rn((double)N, inv_P);
+    return __ddiv_rn(__dmul_rn(w, c), w);
+  }
+  return c;
+}
+
 // Exact u8 -> double without I2F: the bits of 2^52 + v are 0x43300000:v.
 __device__ __forceinline__ double u8_to_double(uint32_t v) {
   return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);

@@ -268,7 +268,8 @@ struct LoopSmem {
   uint32_t row0[KMAX];                   // dense path: sorted d(c_0, .) as integers
   double rowd[2][KMAX];                  // tables scratch (two rows per pass)
   int rank_part[2][2][KMAX];             // tables: [row][half of u-range][t]
-  uint8_t rowo[2][KMAX];                 // tables: permutation being repaired
+  uint8_t rowo[2][KMAX];                 // tables: permutation being repaired (kept: the block's rows' order)
+  int rowo_row[2];                       // row whose final permutation rowo[r] holds (-1: none)
   unsigned long long red_u64[LOOP_THREADS / 32];
   double red_hi[LOOP_THREADS / 32], red_lo[LOOP_THREADS / 32];
   int red_i[LOOP_THREADS / 32];
@@ -281,6 +282,7 @@ struct LoopSmem {
   int stop_flag;                         // block 0: stop after this iteration
   unsigned long long* stamp;             // profiling: block_times in the stamped iteration, else null
   unsigned int part_b, part_g;           // emulated ranks (X == 2): block index in its group, group size
+  int debug;                             // LoopParams::debug_flags
 };
 #define SUB_STAMP(phase)                                                         \
   do {                                                                           \
@@ -318,7 +320,7 @@ struct RowStage {
 // still strictly increasing in (d, index) it IS the unique sorted order and
 // only the distances are rewritten. Otherwise (early iterations) the row is
 // re-sorted by rank counting, half of the block per row, u-range split in 2.
-__device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental) {
+__device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental, bool keep) {
   static_assert(LOOP_THREADS == 4 * KMAX || LOOP_THREADS == 2 * KMAX, "tables layout: 512 or 1024 threads");
   const int tid = threadIdx.x;
   const int r = tid >> 9;                     // which row of the pair
@@ -326,9 +328,12 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
   const int h = (tid >> 8) & 1;               // half of the u-range
   const int p = r ? pb : pa;
   const bool lead = p >= 0 && h == 0;         // one thread per (row, element)
+  // the previous permutation: still in shared memory when this block owns the
+  // same row in the same slot every iteration (one pass), else from L2
+  const bool have = keep && S.rowo_row[r] == p;
   if (lead && t < k) {
     S.rowd[r][t] = t == p ? 0.0 : dist2_rn(S.cx[p], S.cy[p], S.cz[p], S.cx[t], S.cy[t], S.cz[t]);
-    if (incremental) S.rowo[r][t] = st->order[p * KMAX + t];
+    if (incremental && !have) S.rowo[r][t] = st->order[p * KMAX + t];
   }
   __syncthreads();
   SUB_STAMP(10);
@@ -385,7 +390,12 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
       const int rank = t == p ? 0 : 1 + S.rank_part[r][0][t] + S.rank_part[r][1][t];
       st->sortedD[p * KMAX + rank] = S.rowd[r][t];
       st->order[p * KMAX + rank] = (uint8_t)t;
+      S.rowo[r][rank] = (uint8_t)t;
     }
+  }
+  if (threadIdx.x == 0) {
+    S.rowo_row[0] = keep ? pa : -1;
+    S.rowo_row[1] = keep ? pb : -1;
   }
   __syncthreads();
 }
@@ -397,13 +407,15 @@ __device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, boo
   const int first = G == 1 ? 0 : (int)blockIdx.x - 1;
   const int stride = G == 1 ? 1 : G - 1;
   if (first < 0) return;
+  // one pass per block (the rows never move between slots): keep the permutations in shared memory
+  const bool keep = LOOP_THREADS == 4 * KMAX && 2 * stride >= k && !(S.debug & 2048);
   for (int p = first; p < k; p += 2 * stride) {
     const int q = p + stride;
     if (LOOP_THREADS == 4 * KMAX) {
-      tables_rows2(S, st, p, q < k ? q : -1, k, incremental);
+      tables_rows2(S, st, p, q < k ? q : -1, k, incremental, keep);
     } else {  // 512 threads: one row per pass
-      tables_rows2(S, st, p, -1, k, incremental);
-      if (q < k) tables_rows2(S, st, q, -1, k, incremental);
+      tables_rows2(S, st, p, -1, k, incremental, false);
+      if (q < k) tables_rows2(S, st, q, -1, k, incremental, false);
     }
   }
 }
@@ -1276,7 +1288,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       chunk_sched().order[j] = (uint16_t)j;
       chunk_sched().cost[j] = 0;
     }
-  if (tid == 0) S.stamp = nullptr;
+  if (tid == 0) {
+    S.stamp = nullptr;
+    S.debug = L.debug_flags;
+    S.rowo_row[0] = S.rowo_row[1] = -1;
+  }
   __syncthreads();
   if (L.block_times && tid == 0) {  // profiling: SM of this block, evaluations in stamp_iter
     unsigned int smid;
@@ -1407,7 +1423,26 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     // (one unit per thread at 1024 threads), each loading its sum and N in one
     // L2 round trip.
     int empt_local = 0;
-    for (int u = tid; u < 3 * KMAX; u += blockDim.x) {
+    // block 0 (SSE + termination): thread t loads all five moments of cluster
+    // t in one L2 round trip and keeps them for the SSE below; the other
+    // blocks split the 3k coordinates over their threads
+    const bool b0f = PPT == 1 && blockIdx.x == 0 && !(S.debug & 4096);  // (PPT 2: register budget)
+    unsigned long long mN = 0, mS0 = 0, mS1 = 0, mS2 = 0, mQ = 0;
+    if (b0f && tid < k) {
+      mN = ldmom<X != 0>(&tot[3 * KMAX + tid]);
+      mS0 = ldmom<X != 0>(&tot[0 * KMAX + tid]);
+      mS1 = ldmom<X != 0>(&tot[1 * KMAX + tid]);
+      mS2 = ldmom<X != 0>(&tot[2 * KMAX + tid]);
+      mQ = ldmom<X != 0>(&tot[4 * KMAX + tid]);
+      if (mN) {
+        S.nx[tid] = center_coord_v(mS0, mN, mS0, mS1, mS2, mQ, inv_P);
+        S.ny[tid] = center_coord_v(mS1, mN, mS0, mS1, mS2, mQ, inv_P);
+        S.nz[tid] = center_coord_v(mS2, mN, mS0, mS1, mS2, mQ, inv_P);
+      } else {
+        empt_local = 1;
+      }
+    }
+    for (int u = tid; u < 3 * KMAX && !b0f; u += blockDim.x) {
       const int ch = u / KMAX, t = u % KMAX;
       if (t < k) {
         const unsigned long long N = ldmom<X != 0>(&tot[3 * KMAX + t]);
@@ -1439,9 +1474,13 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       if (tid < k) {
         const int t = tid;
         moved += (S.nx[t] != S.cx[t]) | (S.ny[t] != S.cy[t]) | (S.nz[t] != S.cz[t]);
-        const unsigned long long mN = ldmom<X != 0>(&tot[3 * KMAX + t]);
-        const unsigned long long mS0 = ldmom<X != 0>(&tot[0 * KMAX + t]), mS1 = ldmom<X != 0>(&tot[1 * KMAX + t]);
-        const unsigned long long mS2 = ldmom<X != 0>(&tot[2 * KMAX + t]), mQ = ldmom<X != 0>(&tot[4 * KMAX + t]);
+        if (!b0f) {
+          mN = ldmom<X != 0>(&tot[3 * KMAX + t]);
+          mS0 = ldmom<X != 0>(&tot[0 * KMAX + t]);
+          mS1 = ldmom<X != 0>(&tot[1 * KMAX + t]);
+          mS2 = ldmom<X != 0>(&tot[2 * KMAX + t]);
+          mQ = ldmom<X != 0>(&tot[4 * KMAX + t]);
+        }
         if (mN) {
           const double dn = (double)mN;
           const double Sr = (double)mS0, Sg = (double)mS1;
