@@ -1442,6 +1442,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         empt_local = 1;
       }
     }
+    double myc = 0.0;  // this thread's coordinate (one unit per thread at 1024 threads)
     for (int u = tid; u < 3 * KMAX && !b0f; u += blockDim.x) {
       const int ch = u / KMAX, t = u % KMAX;
       if (t < k) {
@@ -1449,13 +1450,19 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         const unsigned long long Sv = ldmom<X != 0>(&tot[ch * KMAX + t]);
         if (N) {
           double* dst = ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz);
-          dst[t] = center_coord<X != 0>(tot, KMAX, t, Sv, N, inv_P);
+          myc = center_coord<X != 0>(tot, KMAX, t, Sv, N, inv_P);
+          dst[t] = myc;
         } else if (ch == 0) {
           empt_local = 1;
         }
       }
     }
     const int empt = __syncthreads_count(empt_local);  // k <= blockDim: one cluster per thread
+    // blocks other than 0 need the old centers only for a reseed: with no empty
+    // cluster they write the new ones straight into the current set (no copy pass)
+    const bool direct = LOOP_THREADS >= 3 * KMAX && blockIdx.x != 0 && !empt && !(S.debug & 8192);
+    if (direct && tid < 3 * KMAX && (tid % KMAX) < k)
+      (tid < KMAX ? S.cx : (tid < 2 * KMAX ? S.cy : S.cz))[tid % KMAX] = myc;
     BLOCK_STAMP(8);
     if (empt) {  // rare: empty clusters (uniform across the grid)
       if (tid == 0) {
@@ -1538,12 +1545,14 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     BLOCK_STAMP(9);
     if constexpr (X != 0)  // the delta accumulators again
       for (int e = tid; e < 5 * KMAX; e += blockDim.x) tot[e] = 0ull;
-    for (int t = tid; t < k; t += blockDim.x) {
-      S.cx[t] = S.nx[t];
-      S.cy[t] = S.ny[t];
-      S.cz[t] = S.nz[t];
+    if (!direct) {
+      for (int t = tid; t < k; t += blockDim.x) {
+        S.cx[t] = S.nx[t];
+        S.cy[t] = S.ny[t];
+        S.cz[t] = S.nz[t];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
     if (tid == 0) S.stamp = (L.block_times && it == L.stamp_iter) ? L.block_times : nullptr;
