@@ -359,7 +359,8 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
             swapped = 1;
           }
         }
-        __syncthreads();
+        // the second phase's barrier is the round's vote (bar.red.or orders shared memory too)
+        if (ph == 0) __syncthreads();
       }
       again = __syncthreads_or(swapped) != 0;
       ++rounds;
