@@ -320,7 +320,8 @@ struct RowStage {
 // still strictly increasing in (d, index) it IS the unique sorted order and
 // only the distances are rewritten. Otherwise (early iterations) the row is
 // re-sorted by rank counting, half of the block per row, u-range split in 2.
-__device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental, bool keep) {
+__device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental, bool keep,
+                             bool tail_sync = true) {
   static_assert(LOOP_THREADS == 4 * KMAX || LOOP_THREADS == 2 * KMAX, "tables layout: 512 or 1024 threads");
   const int tid = threadIdx.x;
   const int r = tid >> 9;                     // which row of the pair
@@ -398,7 +399,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
     S.rowo_row[0] = keep ? pa : -1;
     S.rowo_row[1] = keep ? pb : -1;
   }
-  __syncthreads();
+  if (tail_sync) __syncthreads();  // else the caller's next step begins with a block barrier
 }
 
 // Rows are owned by blocks 1..G-1 (block 0 runs the SSE / termination
@@ -413,7 +414,9 @@ __device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, boo
   for (int p = first; p < k; p += 2 * stride) {
     const int q = p + stride;
     if (LOOP_THREADS == 4 * KMAX) {
-      tables_rows2(S, st, p, q < k ? q : -1, k, incremental, keep);
+      // the last pass skips its trailing barrier: the grid barrier (or
+      // grid.sync) after tables_all starts with one
+      tables_rows2(S, st, p, q < k ? q : -1, k, incremental, keep, p + 2 * stride < k);
     } else {  // 512 threads: one row per pass
       tables_rows2(S, st, p, -1, k, incremental, false);
       if (q < k) tables_rows2(S, st, q, -1, k, incremental, false);
@@ -1291,6 +1294,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     }
   if (tid == 0) {
     S.stamp = nullptr;
+    S.wq = 0u;
     S.debug = L.debug_flags;
     S.rowo_row[0] = S.rowo_row[1] = -1;
   }
@@ -1329,7 +1333,6 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   double prev_sse = __longlong_as_double(0x7ff0000000000000LL);  // +inf (block 0)
   for (int it = 1;; ++it) {
     const bool rec_it = rec && it <= L.hist_cap;
-    if (tid == 0) S.wq = 0u;  // read after the __syncthreads preceding assign
     if (rec_it) tl[(it - 1) * 8 + 0] = globaltimer();
     BLOCK_STAMP(0);
     // ---------------- assign(it) ----------------
@@ -1348,7 +1351,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         assign_dense_first<X>(S, L, lo, hi, ev_dense);
       }
     } else {
-      __syncthreads();
+      // no block barrier here: the grid barrier that ended the previous
+      // iteration already ordered everything this assign reads (S.wq was
+      // reset after the previous assign)
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
@@ -1363,6 +1368,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       }
     }
     __syncthreads();
+    if (tid == 0) S.wq = 0u;  // every warp has left the chunk loop; the next assign reads it after two grid barriers
     if (rec_it) tl[(it - 1) * 8 + 2] = globaltimer();
     BLOCK_STAMP(1);
     flush_moments(S, gacc, k);
@@ -1443,27 +1449,37 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
         empt_local = 1;
       }
     }
-    double myc = 0.0;  // this thread's coordinate (one unit per thread at 1024 threads)
+    // blocks other than 0 need the old centers only for a reseed: they write
+    // the new ones straight into the current set (one unit per thread), and
+    // put the old ones back in the rare case that a cluster is empty
+    const bool spec = LOOP_THREADS >= 3 * KMAX && blockIdx.x != 0 && !(S.debug & 8192);
+    double oldc = 0.0;
+    bool wrote = false;
     for (int u = tid; u < 3 * KMAX && !b0f; u += blockDim.x) {
       const int ch = u / KMAX, t = u % KMAX;
       if (t < k) {
         const unsigned long long N = ldmom<X != 0>(&tot[3 * KMAX + t]);
         const unsigned long long Sv = ldmom<X != 0>(&tot[ch * KMAX + t]);
         if (N) {
-          double* dst = ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz);
-          myc = center_coord<X != 0>(tot, KMAX, t, Sv, N, inv_P);
-          dst[t] = myc;
+          const double c = center_coord<X != 0>(tot, KMAX, t, Sv, N, inv_P);
+          (ch == 0 ? S.nx : (ch == 1 ? S.ny : S.nz))[t] = c;
+          if (spec) {
+            double* cur = ch == 0 ? S.cx : (ch == 1 ? S.cy : S.cz);
+            oldc = cur[t];
+            cur[t] = c;
+            wrote = true;
+          }
         } else if (ch == 0) {
           empt_local = 1;
         }
       }
     }
     const int empt = __syncthreads_count(empt_local);  // k <= blockDim: one cluster per thread
-    // blocks other than 0 need the old centers only for a reseed: with no empty
-    // cluster they write the new ones straight into the current set (no copy pass)
-    const bool direct = LOOP_THREADS >= 3 * KMAX && blockIdx.x != 0 && !empt && !(S.debug & 8192);
-    if (direct && tid < 3 * KMAX && (tid % KMAX) < k)
-      (tid < KMAX ? S.cx : (tid < 2 * KMAX ? S.cy : S.cz))[tid % KMAX] = myc;
+    const bool direct = spec && !empt;
+    if (spec && empt) {  // rare: the reseed needs the old centers
+      if (wrote) (tid < KMAX ? S.cx : (tid < 2 * KMAX ? S.cy : S.cz))[tid % KMAX] = oldc;
+      __syncthreads();
+    }
     BLOCK_STAMP(8);
     if (empt) {  // rare: empty clusters (uniform across the grid)
       if (tid == 0) {
@@ -1542,7 +1558,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
           st->final_C[3 * t + 2] = S.nz[t];
         }
     }
-    __syncthreads();
+    if (!direct) __syncthreads();  // (direct: the new centers were written before the count barrier)
     BLOCK_STAMP(9);
     if constexpr (X != 0)  // the delta accumulators again
       for (int e = tid; e < 5 * KMAX; e += blockDim.x) tot[e] = 0ull;
