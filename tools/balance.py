@@ -50,6 +50,8 @@ for a, b, n in [(3, 8, "fin: centers"), (8, 9, "fin: block0"), (9, 4, "fin: copy
                 (10, 11, "tab: repair"), (11, 5, "tab: write")]:
     v = dur(a, b)[rows]
     print(f"sub {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f}")
+for a, b, n in [(3, 8, "block0 centers"), (8, 9, "block0 SSE/term"), (9, 4, "block0 copy")]:
+    print(f"sub {n:16s} {dur(a, b)[0]:6.2f}")
 for a, b, n in []:
     v = dur(a, b)
     print(f"dur {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f} block0 {v[0]:6.2f}")
