@@ -1406,7 +1406,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     if constexpr (X != 0) {  // all-reduce of the K x 5 moment sums over the ranks
       const unsigned long long s = ++xs;
       const unsigned int pb = part_block<X>(S);
-      if (pb < (unsigned)L.xw) {  // block pb of every part sends to rank pb
+      // (debug flag 32768, tests only: part 1 goes silent at iteration 3 - a dead peer)
+      const bool silent = (L.debug_flags & 32768) && part == 1 && it >= 3;
+      if (pb < (unsigned)L.xw && !silent) {  // block pb of every part sends to rank pb
         unsigned long long* dst = xpay(L.xbox[pb], s, part);
         for (int e = tid; e < 5 * KMAX; e += blockDim.x)
           if ((e & (KMAX - 1)) < k) dst[e] = __ldcg(&gacc[e]);

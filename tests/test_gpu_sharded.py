@@ -135,3 +135,36 @@ def test_in_kernel_exchange_cfg4_full_size():
     assert rep.iterations == single.report.iterations and rep.dist_evals == single.report.dist_evals
     assert rep.mse == single.report.mse
     np.testing.assert_array_equal(idx, single.index_map)
+
+
+def test_in_kernel_exchange_dead_peer_fails_instead_of_hanging():
+    """A rank that stops publishing (debug flag: emulated rank 1 goes silent
+    at iteration 3) makes the others give up after the 5 s exchange timeout:
+    the call fails with CQB_ERR_NCCL, the kernel exits, and the context still
+    quantizes afterwards."""
+    import time
+
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    img = gmm_image(128, 64, 16, 3)
+    ctx = _native.Context(0)
+    q = PeerShardedQuantizer(ctx=ctx, emulate=2)
+    d_img = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+    torch.cuda.synchronize()
+    ctx.check(ctx.lib.cqb_set_debug(ctx.h, 32768))
+    t0 = time.time()
+    q.enqueue(d_img.data_ptr(), img.shape[0] * img.shape[1], 16, api.Termination.convergent(1e-4, 100), 1)
+    with pytest.raises(_native.CqbError) as e:
+        q.fetch()
+    assert e.value.code == _native.CQB_ERR_NCCL
+    assert time.time() - t0 < 60
+    ctx.check(ctx.lib.cqb_set_debug(ctx.h, 0))
+    single = api.quantize(img, 16, api.Termination.convergent(1e-4, 100), seed=1)
+    q2 = PeerShardedQuantizer(ctx=ctx, emulate=2)  # fresh windows after a failed exchange
+    q2.enqueue(d_img.data_ptr(), img.shape[0] * img.shape[1], 16, api.Termination.convergent(1e-4, 100), 1)
+    centers, rep, _ = q2.fetch()
+    np.testing.assert_array_equal(centers, single.palette)
+    ctx.close()
