@@ -63,7 +63,8 @@ struct cqb_ctx {
   uint32_t* d_first = nullptr;
   uint32_t* d_bitmap = nullptr;  // P-bit first-occurrence bitmap (+ pad)
   uint32_t* d_occ = nullptr;     // 2^24-bit bin occupancy map (small images; all-zero between calls)
-  uint32_t* d_block_counts = nullptr;  // k_prep_small scratch [2 * MAXBLK]
+  uint32_t* d_block_counts = nullptr;  // k_prep_small scratch [3 * MAXBLK]
+  uint32_t* d_units = nullptr;         // k_prep_small scratch: non-empty 8-bin units, per-block lists
   uint32_t* d_wofs = nullptr;          // k_prep_small scratch [2^19]
   int prep_blocks = 0;                 // k_prep_small cooperative grid
   uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
@@ -360,6 +361,7 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     Q.n_words = n_words;
     Q.block_counts = ctx->d_block_counts;
     Q.wofs = ctx->d_wofs;
+    Q.units = ctx->d_units;
     Q.draws = ctx->d_draws;
     Q.ndraws = ndraws;
     Q.k = init_k;
@@ -629,7 +631,8 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMalloc(&ctx->bins, sizeof(uint2) << 24));
     CK(cudaMemset(ctx->bins, 0, sizeof(uint2) << 24));
     CK(cudaMalloc(&ctx->d_occ, sizeof(uint32_t) << 19));
-    CK(cudaMalloc(&ctx->d_block_counts, sizeof(uint32_t) * 2 * MAXBLK));
+    CK(cudaMalloc(&ctx->d_block_counts, sizeof(uint32_t) * 3 * MAXBLK));
+    CK(cudaMalloc(&ctx->d_units, sizeof(uint32_t) * ((4u << 19) + 4 * MAXBLK)));
     CK(cudaMalloc(&ctx->d_cand, (size_t)CAND_CELLS * CAND_CAP));
     CK(cudaMalloc(&ctx->d_cand_n, sizeof(uint16_t) * CAND_CELLS));
     CK(cudaMalloc(&ctx->d_wofs, sizeof(uint32_t) << 19));
@@ -680,7 +683,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->d_err, ctx->tile_state,
-                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_block_counts, ctx->d_wofs, ctx->d_cand, ctx->d_cand_n, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
+                 ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_block_counts, ctx->d_units, ctx->d_wofs, ctx->d_cand, ctx->d_cand_n, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,

@@ -39,7 +39,8 @@ struct PrepParams {
   uint32_t* bitmap;         // P bits, zeroed by the host
   uint32_t* pre;            // P/32 words
   uint32_t n_words;         // ceil(P / 32)
-  uint32_t* block_counts;   // [2 * gridDim.x] scratch
+  uint32_t* block_counts;   // [3 * gridDim.x] scratch
+  uint32_t* units;          // [gridDim.x][4 * per_block] scratch: the block's non-empty units (word * 4 + byte)
   uint32_t* wofs;           // [2^19] scratch: in-block offset of each occupancy word's first sample
   const unsigned long long* draws;
   int ndraws;
@@ -109,8 +110,12 @@ __global__ void __launch_bounds__(PREP_THREADS, 1) k_prep_small(PrepParams Q) {
   const uint32_t wb0 = min(b * per_block, OCC_WORDS_ALL), wb1 = min(wb0 + per_block, OCC_WORDS_ALL);
   const uint32_t wpt = (per_block + PREP_THREADS - 1) / PREP_THREADS;  // words per thread (contiguous)
   const uint32_t wt0 = min(wb0 + tid * wpt, wb1), wt1 = min(wt0 + wpt, wb1);
-  uint32_t cnt = 0;
-  for (uint32_t w = wt0; w < wt1; ++w) cnt += __popc(Q.occ[w]);
+  uint32_t cnt = 0, ucnt = 0;
+  for (uint32_t w = wt0; w < wt1; ++w) {
+    const uint32_t word = Q.occ[w];
+    cnt += __popc(word);
+    ucnt += (word & 0xFFu ? 1u : 0u) + (word & 0xFF00u ? 1u : 0u) + (word & 0xFF0000u ? 1u : 0u) + (word >> 24 ? 1u : 0u);
+  }
   if (Q.zero_state) {  // replaces the host memsets of the quantize path
     for (uint32_t w = b * PREP_THREADS + tid; w < Q.n_words; w += G * PREP_THREADS) Q.bitmap[w] = 0u;
     if (b == 0) {
@@ -126,41 +131,68 @@ __global__ void __launch_bounds__(PREP_THREADS, 1) k_prep_small(PrepParams Q) {
       }
     }
   }
-  uint32_t btotal;
+  uint32_t btotal, utotal;
   const uint32_t tex = prep_block_scan(cnt, s_warp, &btotal);
+  const uint32_t uex = prep_block_scan(ucnt, s_warp, &utotal);
   {
-    uint32_t run = tex;
+    // the block's non-empty units, in Morton order, into its own list (phase B
+    // deals them out over the whole grid: work follows the samples, not the map)
+    uint32_t* ul = Q.units + (size_t)b * 4 * per_block;
+    uint32_t run = tex, urun = uex;
     for (uint32_t w = wt0; w < wt1; ++w) {
+      const uint32_t word = Q.occ[w];
       Q.wofs[w] = run;
-      run += __popc(Q.occ[w]);
+      run += __popc(word);
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j)
+        if ((word >> (8 * j)) & 0xFFu) ul[urun++] = w * 4 + j;
     }
   }
-  if (tid == 0) Q.block_counts[b] = btotal;
+  if (tid == 0) {
+    Q.block_counts[b] = btotal;
+    Q.block_counts[2 * G + b] = utotal;
+  }
   prep_stamp(Q, 1);
   grid.sync();
   prep_stamp(Q, 2);
 
-  // ---- B: emit samples in Morton order. Words are dealt grid-stride (not
-  // by slice), so dense regions of color space spread over all SMs; word w's
-  // output offset = its block's base + its in-block offset from phase A.
+  // ---- B: emit samples in Morton order. The non-empty units (8 bins of one
+  // occupancy word) listed in phase A are dealt out over blocks 1..G-1 by
+  // their global index, so every thread gets about N'/(8 x threads) units
+  // however the colors cluster; a unit's output offset = its word's block
+  // base + the word's in-block offset (phase A) + the set bits below it.
+  // Block 0 runs init_centers meanwhile (it needs only N').
   __shared__ uint32_t s_bbase[MAXBLK];
+  __shared__ uint32_t s_ubase[MAXBLK + 1];
   if (tid == 0) {
-    uint32_t base = 0;
+    uint32_t base = 0, ubase = 0;
     for (uint32_t c = 0; c < G; ++c) {
       s_bbase[c] = base;
       base += Q.block_counts[c];
+      s_ubase[c] = ubase;
+      ubase += Q.block_counts[2 * G + c];
     }
+    s_ubase[G] = ubase;
     if (b == 0) *Q.n_unique = base;
+    s_base = base;
   }
   __syncthreads();
-  // 4 lanes per map word, 8 bit positions each: a dense word (32 touched
-  // bins) is emitted by 4 threads with one batch of loads each.
-  constexpr uint32_t U = 4;
-  for (uint32_t u = b * PREP_THREADS + tid; u < OCC_WORDS_ALL * U; u += G * PREP_THREADS) {
-    const uint32_t w = u / U, j = u % U;
-    const uint32_t word = Q.occ[w];
-    const uint32_t mine = word & (0xFFu << (8 * j));
-    if (mine) {
+  if (b == 0 && G > 1) {
+    if (Q.k > 0) init_centers_block(nullptr, s_base, Q.k, Q.draws, Q.ndraws, Q.st);  // chosen ranks only
+  } else {
+    const uint32_t nunits = s_ubase[G];
+    const uint32_t B0 = G > 1 ? 1u : 0u, NB = G - B0;
+    for (uint32_t g = (b - B0) * PREP_THREADS + tid; g < nunits; g += NB * PREP_THREADS) {
+      uint32_t lo = 0, hi = G;  // the block c whose list holds unit g: s_ubase[c] <= g < s_ubase[c + 1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_ubase[mid] <= g) lo = mid;
+        else hi = mid;
+      }
+      const uint32_t unit = Q.units[(size_t)lo * 4 * per_block + (g - s_ubase[lo])];
+      const uint32_t w = unit >> 2, j = unit & 3u;
+      const uint32_t word = Q.occ[w];
+      const uint32_t mine = word & (0xFFu << (8 * j));
       uint32_t pos = s_bbase[w / per_block] + Q.wofs[w] + __popc(word & ((1u << (8 * j)) - 1u));
       uint32_t ms[8];
       int nb = 0;
@@ -186,8 +218,6 @@ __global__ void __launch_bounds__(PREP_THREADS, 1) k_prep_small(PrepParams Q) {
         }
       }
     }
-    __syncwarp();  // the word's 4 lanes (consecutive threads) have read it
-    if (j == 0 && word) Q.occ[w] = 0u;
   }
   prep_stamp(Q, 3);
   if (Q.stamps) {  // per-block end of phase B (profiling)
@@ -212,8 +242,9 @@ __global__ void __launch_bounds__(PREP_THREADS, 1) k_prep_small(PrepParams Q) {
   uint32_t xtotal;
   const uint32_t xex = prep_block_scan(bc, s_warp, &xtotal);
   if (tid == 0) Q.block_counts[G + b] = xtotal;
+  for (uint32_t w = wb0 + tid; w < wb1; w += PREP_THREADS) Q.occ[w] = 0u;  // all-zero between calls
   prep_stamp(Q, 5);
-  if (b == 0 && Q.k > 0) init_centers_block(nullptr, n, Q.k, Q.draws, Q.ndraws, Q.st);  // chosen ranks only
+  if (G == 1 && Q.k > 0) init_centers_block(nullptr, n, Q.k, Q.draws, Q.ndraws, Q.st);  // (one block: here)
   prep_stamp(Q, 6);
   grid.sync();
   prep_stamp(Q, 7);
