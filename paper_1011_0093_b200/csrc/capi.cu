@@ -490,9 +490,33 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   return CQB_OK;
 }
 
+// The per-call results into the pinned staging block with one tiny kernel
+// (zero-copy stores into mapped host memory) instead of six small D2H copies.
+__global__ void k_publish(const WsmState* __restrict__ st, const unsigned long long* __restrict__ d_n,
+                          const double* __restrict__ d_hist, int k, int hist_n, Staging* h, double* h_hist) {
+  const int t = threadIdx.x;
+  for (int i = t; i < 3 * k; i += blockDim.x) h->centers[i] = st->final_C[i];
+  const int nh = min(hist_n, st->iterations);
+  for (int i = t; i < nh; i += blockDim.x) h_hist[i] = d_hist[i];
+  if (t == 0) {
+    h->evals = st->evals;
+    h->mse_err = st->mse_err;
+    h->n_unique = *d_n;
+    h->sse = st->sse;
+    h->iterations = st->iterations;
+    h->status = st->status;
+    h->n_empty = st->n_empty_events;
+  }
+}
+
 int stage_results(cqb_ctx* ctx, int k, int hist_n) {
   Staging* h = ctx->h_stage;
   WsmState* st = ctx->st;
+  if (!(ctx->debug_flags & 65536)) {
+    k_publish<<<1, 256, 0, ctx->stream>>>(st, ctx->d_n, ctx->d_hist, k, hist_n, h, ctx->h_hist);
+    CKL();
+    return CQB_OK;
+  }
   CK(cudaMemcpyAsync(h->centers, st->final_C, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(&h->evals, &st->evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(&h->mse_err, &st->mse_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
@@ -592,6 +616,18 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Device view of a pinned, mapped host buffer (16-B aligned), else null.
+uint8_t* mapped_view(void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer || !aligned16(a.devicePointer)) return nullptr;
+  return static_cast<uint8_t*>(a.devicePointer);
+}
 
 }  // namespace
 
@@ -1013,18 +1049,26 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   TRY(ensure_pixels(ctx, P));
   if (P >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
   CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  // Pinned (mapped) host outputs are written by the map kernel directly over
+  // PCIe (zero-copy), overlapping the transfer with the kernel; pageable ones
+  // get the device buffers + one D2H copy each.
+  const bool zc = !(ctx->debug_flags & 65536);
+  uint8_t* zi = zc ? mapped_view(index_out) : nullptr;
+  uint8_t* zr = zc ? mapped_view(rgb_out) : nullptr;
+  uint8_t* ze = zc ? mapped_view(error_out) : nullptr;
   // H2D, the whole pipeline and the D2H copies are enqueued back to back with
   // ONE host synchronisation (the rare draw-exhaustion retry re-enqueues)
   int ndraws = k + 64;
   for (int attempt = 0; attempt < 4; ++attempt) {
-    ctx->err_target = error_out ? ctx->d_err : nullptr;
-    const int rc = enqueue_quantize(ctx, ctx->d_img, P, k, term, seed, index_out ? ctx->d_index : nullptr,
-                                    rgb_out ? ctx->d_rgb : nullptr, ndraws);
+    ctx->err_target = error_out ? (ze ? ze : ctx->d_err) : nullptr;
+    const int rc = enqueue_quantize(ctx, ctx->d_img, P, k, term, seed,
+                                    index_out ? (zi ? zi : ctx->d_index) : nullptr,
+                                    rgb_out ? (zr ? zr : ctx->d_rgb) : nullptr, ndraws);
     ctx->err_target = nullptr;
     TRY(rc);
-    if (index_out) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
-    if (rgb_out) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
-    if (error_out) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (index_out && !zi) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (rgb_out && !zr) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (error_out && !ze) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->h_stage->status != ST_DRAWS_EXHAUSTED) break;
     ndraws *= 4;

@@ -65,3 +65,8 @@ def dev():
 
 
 print("device-resident       %.3f ms" % timeit(dev))
+lib.cqb_set_debug(ctx.h, 65536)  # staging copies + D2H copies (no zero-copy)
+print("[no zero-copy] api.quantize  %.3f ms" % timeit(lambda: api.quantize(h_img, 256, term, 1, out_index=h_idx, out_mapped=h_out)))
+print("[no zero-copy] raw C idx+rgb %.3f ms" % timeit(lambda: raw(True, True)))
+lib.cqb_set_debug(ctx.h, 0)
+print("api.quantize (again)  %.3f ms" % timeit(lambda: api.quantize(h_img, 256, term, 1, out_index=h_idx, out_mapped=h_out)))
