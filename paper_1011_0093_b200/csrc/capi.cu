@@ -618,14 +618,16 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Device view of a pinned, mapped host buffer (16-B aligned), else null.
-uint8_t* mapped_view(void* p) {
+// (allocated while this context's device was current: no cross-device mapping assumptions)
+uint8_t* mapped_view(void* p, int device) {
   if (!p) return nullptr;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  if (a.type != cudaMemoryTypeHost || !a.devicePointer || !aligned16(a.devicePointer)) return nullptr;
+  if (a.type != cudaMemoryTypeHost || a.device != device || !a.devicePointer || !aligned16(a.devicePointer))
+    return nullptr;
   return static_cast<uint8_t*>(a.devicePointer);
 }
 
@@ -1053,9 +1055,9 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   // PCIe (zero-copy), overlapping the transfer with the kernel; pageable ones
   // get the device buffers + one D2H copy each.
   const bool zc = !(ctx->debug_flags & 65536);
-  uint8_t* zi = zc ? mapped_view(index_out) : nullptr;
-  uint8_t* zr = zc ? mapped_view(rgb_out) : nullptr;
-  uint8_t* ze = zc ? mapped_view(error_out) : nullptr;
+  uint8_t* zi = zc ? mapped_view(index_out, ctx->device) : nullptr;
+  uint8_t* zr = zc ? mapped_view(rgb_out, ctx->device) : nullptr;
+  uint8_t* ze = zc ? mapped_view(error_out, ctx->device) : nullptr;
   // H2D, the whole pipeline and the D2H copies are enqueued back to back with
   // ONE host synchronisation (the rare draw-exhaustion retry re-enqueues)
   int ndraws = k + 64;
