@@ -493,3 +493,31 @@ def test_quantize_large_path_matches_oracle(port):
     mine, my_idx = port.map_pixels(img, q.palette)
     np.testing.assert_array_equal(q.index_map, my_idx)
     assert q.report.mse == port.mse(img, q.mapped)
+
+
+@pytest.mark.parametrize("case,k", [("cfg2", 256), ("gmm101x77", 8)])
+def test_quantize_pinned_outputs_zero_copy(case, k, images, port):
+    """Pinned host outputs take the zero-copy path (the map kernel writes them
+    over PCIe, results published by one kernel): index map, mapped raster,
+    error image and report equal the pageable-buffer path and the oracle."""
+    import torch
+
+    img = images[case]
+    h, w = img.shape[:2]
+    term = api.Termination.convergent(1e-4, 100)
+    ref = api.quantize(img, k, term, seed=1, error=True)  # pageable numpy outputs: device buffers + D2H
+    pin_idx = torch.empty(h * w, dtype=torch.uint8).pin_memory().numpy().reshape(h, w)
+    pin_out = torch.empty(h * w * 3, dtype=torch.uint8).pin_memory().numpy().reshape(h, w, 3)
+    pin_idx[:] = 7
+    pin_out[:] = 7
+    for _ in range(2):  # twice: the staging block and the outputs are rewritten, not stale
+        q = api.quantize(img, k, term, seed=1, out_index=pin_idx, out_mapped=pin_out, error=True)
+        np.testing.assert_array_equal(q.palette, ref.palette)
+        np.testing.assert_array_equal(pin_idx, ref.index_map)
+        np.testing.assert_array_equal(pin_out, ref.mapped)
+        np.testing.assert_array_equal(q.error, ref.error)
+        assert q.report.mse == ref.report.mse and q.report.iterations == ref.report.iterations
+        assert q.report.dist_evals == ref.report.dist_evals
+        assert list(q.report.sse_history) == list(ref.report.sse_history)
+    mine, my_idx = port.map_pixels(img, q.palette)
+    np.testing.assert_array_equal(pin_out, mine)

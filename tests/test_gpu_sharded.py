@@ -168,3 +168,26 @@ def test_in_kernel_exchange_dead_peer_fails_instead_of_hanging():
     centers, rep, _ = q2.fetch()
     np.testing.assert_array_equal(centers, single.palette)
     ctx.close()
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_in_kernel_exchange_edge_cases(world, port):
+    """Fewer unique colors than ranks (empty shards), k = 1, k = N', a
+    single-color image, a ragged pixel count: the emulated ranks give the
+    single-GPU result."""
+    rng = np.random.default_rng(world)
+    cases = []
+    few = rng.integers(0, 256, (5, 3), dtype=np.uint8)
+    cases.append((few[rng.integers(0, 5, 17 * 3)].reshape(17, 3, 3), 3))   # N' = 5 < 8 ranks, P = 51
+    cases.append((few[rng.integers(0, 5, 40 * 8)].reshape(40, 8, 3), 1))   # k = 1
+    cases.append((few[rng.integers(0, 5, 16 * 16)].reshape(16, 16, 3), 5))  # k = N'
+    cases.append((np.full((9, 7, 3), 200, np.uint8), 1))                    # one color
+    cases.append((gmm_image(61, 37, 9, 4), 24))                             # ragged P
+    for img, k in cases:
+        single = api.quantize(img, k, api.Termination.convergent(1e-4, 100), seed=1)
+        centers, rep, hist, idx, mapped = _sharded_run(img, k, world)
+        np.testing.assert_array_equal(centers, single.palette)
+        assert rep.iterations == single.report.iterations and rep.dist_evals == single.report.dist_evals
+        np.testing.assert_array_equal(idx, single.index_map)
+        np.testing.assert_array_equal(mapped, single.mapped)
+        assert rep.mse == single.report.mse
