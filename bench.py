@@ -348,6 +348,7 @@ def run_ours(a, cfg, world, rank, local):
         if world == 1 and not a.no_secondary and cfg.name == "cfg2":
             line["secondary"] = secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks)
             line["secondary_cfg5"] = batch_cfg5(ctx, torch, dev, stream, flush, n_images=16, steps=2, warmup=1)
+            line["other_configs"] = other_configs(lib, ctx, torch, dev, stream, flush)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -378,6 +379,23 @@ def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
             "loop_phases_us": phases,
             "roofline": _roofline(dom, stage_ms[dom], cfg.pixels, int(rep.n_unique), int(rep.iterations), 256, peaks,
                                   int(rep.dist_evals))}
+
+
+def other_configs(lib, ctx, torch, dev, stream, flush):
+    """The remaining single-image BASELINE configs at each of their K,
+    device-resident (same protocol as `value`, 5 steps): config 1 (K=32),
+    config 2 at K=64 and config 3 (K=256)."""
+    out = {}
+    for name, k in (("cfg1", 32), ("cfg2", 64), ("cfg3", 256)):
+        cfg = CONFIGS[name]
+        d = torch.from_numpy(cfg.image().reshape(-1)).to(dev)
+        ctx.check(lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
+        times, _, rep, _, _ = measure_device(lib, ctx, torch, d, cfg.pixels, k, 5, 2, stream, flush)
+        ms = sum(times) / len(times)
+        out[f"{name}_k{k}"] = {"value": cfg.pixels / (ms * 1e-3) / 1e6, "unit": "Mpixel/s", "ms_per_step": ms,
+                               "n_unique": int(rep.n_unique), "iterations": int(rep.iterations),
+                               "dist_evals": int(rep.dist_evals)}
+    return out
 
 
 def batch_cfg5(ctx, torch, dev, stream, flush, n_images=16, steps=2, warmup=1, lanes_list=(1, 4)):
