@@ -191,3 +191,52 @@ def test_in_kernel_exchange_edge_cases(world, port):
         np.testing.assert_array_equal(idx, single.index_map)
         np.testing.assert_array_equal(mapped, single.mapped)
         assert rep.mse == single.report.mse
+
+
+def _ipc_worker(rank, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        ctx = _native.Context(0)
+        qz = PeerShardedQuantizer(ctx=ctx)  # cqb_xch_window + handle all-gather + cqb_xch_open of the peer
+        dist.barrier()
+        ctx.close()  # closes the peer mapping, frees the window
+        dist.barrier()
+        q.put((rank, qz.world, qz.rank, "ok"))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, 0, 0, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_windows_open_across_processes():
+    """The real multi-process setup path (no kernels): two processes on this
+    GPU create their exchange windows, all-gather the IPC handles and map
+    each other's window. (Running the X = 1 loop itself needs one GPU per
+    rank: kernels that wait on each other must not share a GPU.)"""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    outs = sorted(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert [o[3] for o in outs] == ["ok", "ok"], outs
+    assert [(o[1], o[2]) for o in outs] == [(2, 0), (2, 1)]
