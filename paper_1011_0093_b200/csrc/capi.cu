@@ -1054,7 +1054,9 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   // Pinned (mapped) host outputs are written by the map kernel directly over
   // PCIe (zero-copy), overlapping the transfer with the kernel; pageable ones
   // get the device buffers + one D2H copy each.
-  const bool zc = !(ctx->debug_flags & 65536);
+  // (small images only: for large rasters the copy engines move the outputs
+  // faster than the kernel's PCIe stores - cfg4 e2e 1595 vs 1309 Mpix/s)
+  const bool zc = !(ctx->debug_flags & 65536) && P < OCC_MAX_PIXELS;
   uint8_t* zi = zc ? mapped_view(index_out, ctx->device) : nullptr;
   uint8_t* zr = zc ? mapped_view(rgb_out, ctx->device) : nullptr;
   uint8_t* ze = zc ? mapped_view(error_out, ctx->device) : nullptr;
