@@ -1382,6 +1382,8 @@ int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, 
                          uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
   if (ctx->xmode == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_xch_window + cqb_xch_open (or cqb_xch_emulate) first");
+  for (int r = 0; r < ctx->xw; ++r)
+    if (!ctx->xpeer[r]) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "exchange window of rank %d not mapped (cqb_xch_open)", r);
   TRY(check_k(ctx, k));
   TRY(check_term(ctx, term));
   if (n_pixels == 0 || !d_rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize: empty image");
