@@ -240,3 +240,27 @@ def test_ipc_windows_open_across_processes():
         p.join(timeout=60)
     assert [o[3] for o in outs] == ["ok", "ok"], outs
     assert [(o[1], o[2]) for o in outs] == [(2, 0), (2, 1)]
+
+
+def test_exchange_argument_errors():
+    """cqb_xch_* / cqb_quantize_sharded argument checks (invalid argument, not a crash)."""
+    import ctypes as C
+
+    from paper_1011_0093_b200 import _native
+
+    ctx = _native.Context(0)
+    lib = ctx.lib
+    t = api.Termination.convergent(1e-4, 100).native()
+    assert lib.cqb_quantize_sharded(ctx.h, None, 16, 4, C.byref(t), 1, None, None, None) == _native.CQB_ERR_INVALID_ARGUMENT
+    assert lib.cqb_xch_emulate(ctx.h, 0) == _native.CQB_ERR_INVALID_ARGUMENT
+    assert lib.cqb_xch_emulate(ctx.h, 9) == _native.CQB_ERR_INVALID_ARGUMENT
+    h = (C.c_ubyte * _native.IPC_HANDLE_BYTES)()
+    assert lib.cqb_xch_window(ctx.h, 2, 2, h) == _native.CQB_ERR_INVALID_ARGUMENT
+    assert lib.cqb_xch_window(ctx.h, 2, 0, h) == _native.CQB_OK
+    # the peer window is not mapped yet: refused, no launch
+    import torch
+
+    d = torch.zeros(48, dtype=torch.uint8, device="cuda")
+    rc = lib.cqb_quantize_sharded(ctx.h, d.data_ptr(), 16, 4, C.byref(t), 1, None, None, None)
+    assert rc == _native.CQB_ERR_INVALID_ARGUMENT and b"not mapped" in lib.cqb_last_error(ctx.h)
+    ctx.close()
