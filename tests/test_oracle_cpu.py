@@ -186,3 +186,32 @@ def test_run_wsm_invariants(port):
     assert r.iterations == 1 and r.sse == 0.0  # kmeans_test.cpp:242-248
     with pytest.raises(ValueError):
         port.run_wsm(h.keys, h.counts, 4096, len(h.keys) + 1, mode=1)
+
+
+# --------------------------------------------------------------------------- full-size pin
+# The port against the reference's own full convergent runs on the BASELINE
+# configs (tests/golden/full_configs.json, generated from oracle/_ref by
+# tests/golden/make_full_golden.py): the largest inputs the GPU tests check.
+FULL = os.path.join(os.path.dirname(__file__), "golden", "full_configs.json")
+
+
+@pytest.mark.parametrize("case", ["cfg2_k256", "cfg2_k64", "cfg3_k256", "cfg4_k256", "cfg5_i3_k256"])
+def test_port_matches_reference_full_configs(case, port):
+    import hashlib
+    import json
+
+    g = json.load(open(FULL))["cases"][case]
+    img = CONFIGS[g["config"]].image(g["image"])
+    P = g["pixels"]
+    h = port.build_histogram(img)
+    dig = hashlib.sha256(h.keys.astype("<u4").tobytes() + h.counts.astype("<u4").tobytes()).hexdigest()
+    assert len(h.keys) == g["n_unique"] and dig == g["histogram_sha256"]
+    r = port.run_wsm(h.keys, h.counts, P, g["k"], mode=1, eps=1e-4, cap=100, seed=1)
+    assert r.iterations == g["iterations"]
+    assert r.dist_evals == g["dist_evals"]
+    np.testing.assert_array_equal(r.centers.reshape(-1), np.array([float.fromhex(x) for x in g["palette"]]))
+    np.testing.assert_array_equal(r.sse_history, np.array([float.fromhex(x) for x in g["sse_history"]]))
+    mapped, idx = port.map_pixels(img, r.centers)
+    assert hashlib.sha256(mapped.tobytes()).hexdigest() == g["mapped_sha256"]
+    assert hashlib.sha256(idx.tobytes()).hexdigest() == g["index_sha256"]
+    assert port.mse(img, mapped) == float.fromhex(g["mse"])
