@@ -48,7 +48,7 @@ def _args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--k", type=int, default=None, help="default: 256 if the config lists it, else its K")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -137,6 +137,13 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- reference arm
 def run_reference(a, cfg, world, rank):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    colorq headers compiled here) on the same config. One step = one full
+    quantize of one image (histogram + WSM-C + map + mse) on one host thread;
+    the steps run `cores` at a time on a native thread pool (the
+    bench.hpp:187-223 pattern), because the reference has no intra-image
+    parallelism. The timed count is rounded up to whole waves of `cores`
+    images so every thread stays busy: value = images * P / wall."""
     if rank != 0:
         return None
     from oracle.oracle import Oracle, available
@@ -146,26 +153,26 @@ def run_reference(a, cfg, world, rank):
         return None
     ref = Oracle("reference")
     cores = _host_cores()
-    img = cfg.image()
     P = cfg.pixels
-    # one image per worker thread (bench.hpp:187-223); config 5's images are distinct
-    imgs = [cfg.image(i) for i in range(cores)] if cfg.images > 1 else [img] * cores
-    for _ in range(a.warmup):
-        ref.quantize_many(imgs, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
-    walls = []
-    for _ in range(a.steps):
-        ms, mses, its = ref.quantize_many(imgs, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
-        walls.append(ms)
-    total_ms = sum(walls)
-    value = P * cores * a.steps / (total_ms * 1e-3) / 1e6
+    n_timed = max(1, math.ceil(a.steps / cores)) * cores
+    distinct = cfg.images > 1  # config 5: every image its own seed
+    imgs = [cfg.image(i) for i in range(min(n_timed, cfg.images))] if distinct else [cfg.image()]
+    if a.warmup > 0:
+        w = [imgs[i % len(imgs)] for i in range(min(a.warmup, cores))]
+        ref.quantize_many(w, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
+    timed = [imgs[i % len(imgs)] for i in range(n_timed)]
+    ms, mses, its = ref.quantize_many(timed, a.k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
+    value = P * n_timed / (ms * 1e-3) / 1e6
     line = {
         "metric": METRIC, "value": value, "unit": "Mpixel/s", "impl": "reference", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _workload(cfg, a.k), "pixels": P, "images_per_step": cores},
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / n_timed,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload(cfg, a.k), "pixels": P, "images_timed": n_timed, "threads": cores,
+                   "timed": "wall clock of the whole timed pool (images_timed full quantizes, `threads` at a time)"},
         "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": cores, "kind": "reference",
-                         "sample": f"{cores} copies of the {cfg.name} image per step, one per thread "
-                                   f"(oracle/_ref, g++ -O2), iterations={int(its[0])}"},
+                         "sample": f"{n_timed} full quantizes of the {cfg.name} image ({P} px, K={a.k}) on "
+                                   f"{cores} threads, one image per thread (oracle/_ref, g++ -O2), "
+                                   f"iterations={int(its[0])}, wall {ms / 1e3:.1f} s"},
         "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -173,19 +180,26 @@ def run_reference(a, cfg, world, rank):
 
 
 def cpu_baseline_sample(cfg, k, img):
-    """oracle/_ref on all host cores, one image per thread (~seconds)."""
+    """oracle/_ref on all host cores, one image per thread, bounded to ~10-30 s:
+    the 4096^2 configs use their top-left 2048x2048 quarter (the reference
+    needs ~50 s per full cfg4 image on one core)."""
     from oracle.oracle import Oracle, available
 
     if not available("reference"):
         return None
     ref = Oracle("reference")
     cores = _host_cores()
-    imgs = [img] * cores
-    ms, _, its = ref.quantize_many(imgs, k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
-    return {"value": cfg.pixels * cores / (ms * 1e-3) / 1e6, "unit": "Mpixel/s", "cores": cores,
-            "kind": "reference",
-            "sample": f"{cores} concurrent copies of the {cfg.name} image (one per thread), full quantize "
-                      f"(histogram+WSM-C+map+mse), {int(its[0])} iterations, wall {ms:.0f} ms"}
+    if cfg.pixels > (8 << 20):
+        sub = np.ascontiguousarray(img[:2048, :2048])
+        what = f"the top-left 2048x2048 quarter of the {cfg.name} image"
+    else:
+        sub = img
+        what = f"the {cfg.name} image"
+    px = sub.shape[0] * sub.shape[1]
+    ms, _, its = ref.quantize_many([sub] * cores, k, cores, mode=1, eps=EPSILON, cap=HARD_CAP, seed=INIT_SEED)
+    return {"value": px * cores / (ms * 1e-3) / 1e6, "unit": "Mpixel/s", "cores": cores, "kind": "reference",
+            "sample": f"{cores} concurrent copies of {what} (one per thread), full quantize "
+                      f"(histogram+WSM-C K={k}+map+mse), {int(its[0])} iterations, wall {ms:.0f} ms"}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -291,7 +305,11 @@ def run_ours(a, cfg, world, rank, local):
     phases = _loop_phases(stage[-1][1], iters)
     peaks = _peaks()
     dom = max(stage_ms, key=stage_ms.get)
-    roof = _roofline(dom, stage_ms[dom], P, n_unique, iters, k, peaks, int(rep.dist_evals))
+    if dom == "wsm_loop":
+        evals1 = first_iteration_evals(lib, ctx, torch, d_img, P, k, stream)
+        roof = _loop_roofline(stage_ms[dom], P, n_unique, iters, k, peaks, int(rep.dist_evals), evals1, phases)
+    else:
+        roof = _roofline(dom, stage_ms[dom], P, n_unique, iters, k, peaks, int(rep.dist_evals))
 
     # ---- e2e through the public C-ABI call with pinned host buffers ----
     pin_img = torch.from_numpy(img.reshape(-1)).pin_memory()
@@ -345,48 +363,22 @@ def run_ours(a, cfg, world, rank, local):
         }
         if world == 1 and not a.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(cfg, k, img)
-        if world == 1 and not a.no_secondary and cfg.name == "cfg2":
-            line["secondary"] = secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks)
+        if world == 1 and not a.no_secondary:
+            line["other_configs"] = other_configs(lib, ctx, torch, dev, stream, flush, skip=(cfg.name, k))
             line["secondary_cfg5"] = batch_cfg5(ctx, torch, dev, stream, flush, n_images=16, steps=2, warmup=1)
-            line["other_configs"] = other_configs(lib, ctx, torch, dev, stream, flush)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return line
 
 
-def secondary_cfg4(lib, ctx, torch, dev, stream, flush, peaks):
-    """Config 4 (4096^2 uniform, ~10.6M unique colors, K=256), device-resident."""
-    from paper_1011_0093_b200 import _native as N
-
-    cfg = CONFIGS["cfg4"]
-    img = cfg.image()
-    d = torch.from_numpy(img.reshape(-1)).to(dev)
-    ctx.check(lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
-    times, _, rep, _, _ = measure_device(lib, ctx, torch, d, cfg.pixels, 256, 3, 2, stream, flush)
-    ctx.check(lib.cqb_set_profiling(ctx.h, 1))
-    _, stage, _, _, _ = measure_device(lib, ctx, torch, d, cfg.pixels, 256, 2, 0, stream, flush, profile=True)
-    ctx.check(lib.cqb_set_profiling(ctx.h, 0))
-    st = np.median(np.array([x[0] for x in stage]), axis=0)
-    stage_ms = {n: float(v) for n, v in zip(N.STAGES, st)}
-    phases = _loop_phases(stage[-1][1], int(rep.iterations))
-    ms = sum(times) / len(times)
-    dom = max(stage_ms, key=stage_ms.get)
-    return {"workload": _workload(cfg, 256), "value": cfg.pixels / (ms * 1e-3) / 1e6, "unit": "Mpixel/s",
-            "ms_per_step": ms, "n_unique": int(rep.n_unique), "iterations": int(rep.iterations),
-            "dist_evals": int(rep.dist_evals), "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-            "hbm_stages": _hbm_stages(stage_ms, cfg.pixels, int(rep.n_unique), peaks),
-            "loop_phases_us": phases,
-            "roofline": _roofline(dom, stage_ms[dom], cfg.pixels, int(rep.n_unique), int(rep.iterations), 256, peaks,
-                                  int(rep.dist_evals))}
-
-
-def other_configs(lib, ctx, torch, dev, stream, flush):
-    """The remaining single-image BASELINE configs at each of their K,
-    device-resident (same protocol as `value`, 5 steps): config 1 (K=32),
-    config 2 at K=64 and config 3 (K=256)."""
+def other_configs(lib, ctx, torch, dev, stream, flush, skip=None):
+    """The other single-image BASELINE configs at each of their K,
+    device-resident (same protocol as `value`, 5 timed steps, L2 flushed)."""
     out = {}
-    for name, k in (("cfg1", 32), ("cfg2", 64), ("cfg3", 256)):
+    for name, k in (("cfg1", 32), ("cfg2", 64), ("cfg2", 256), ("cfg3", 256), ("cfg4", 256)):
+        if (name, k) == skip:
+            continue
         cfg = CONFIGS[name]
         d = torch.from_numpy(cfg.image().reshape(-1)).to(dev)
         ctx.check(lib.cqb_set_stream(ctx.h, C.c_void_p(stream.cuda_stream)))
@@ -501,6 +493,70 @@ def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
                                  "frac": evals / (ms * 1e-3) / (fp64_ops / 8),
                                  "peak_source": "measured DADD/DMUL throughput / 8 ops per evaluation"}
     return out
+
+
+# Measured CUDA-core issue rate (tools/microbench.cu on this B200 pool,
+# profiles/r01/microbench_primitives.txt): 111.4 FADD per SM per clock.
+F32_ISSUE_PER_S = 32.41e12
+FLOP_PER_EVAL = 8    # 3 sub, 3 mul, 2 add per distance evaluation
+SLOTS_PER_EVAL = 6   # scan_f32: 3 FSUB + FMUL + 2 FFMA issue slots per evaluation
+
+
+def first_iteration_evals(lib, ctx, torch, d_img, P, k, stream):
+    """dist_evals of a one-iteration run (fixed(1)) = iteration 1's point
+    evaluations + the k(k-1)/2 pairs of the initial center tables."""
+    from paper_1011_0093_b200 import _native as N
+
+    term = N.Termination(0, 1, EPSILON, HARD_CAP)
+    rep = N.Report()
+    cent = np.zeros(3 * k)
+    with torch.cuda.stream(stream):
+        ctx.check(lib.cqb_quantize_device(ctx.h, C.c_void_p(d_img.data_ptr()), P, k, C.byref(term), INIT_SEED,
+                                          None, None, 1, cent.ctypes.data_as(C.POINTER(C.c_double)), None, 0,
+                                          C.byref(rep)))
+    return int(rep.dist_evals)
+
+
+def _loop_roofline(ms, P, n_unique, iters, k, peaks, evals, evals1, phases):
+    """Roofline of the persistent WSM loop (k_wsm_loop), SURVEY.md §8(d).
+
+    Algorithmic work = the reference's own dist_evals (exact, kmeans.hpp:214,
+    228, 237) at 8 FLOP each. Iterations >= 2 (FP32-screened sort-means
+    scans, the bulk of the launch) are reported as the headline: achieved =
+    8 * E(>=2) / their time, peak = 8/6 * the measured FP32 issue rate (6
+    issue slots per evaluation). Iteration 1 (integer dp4a over per-cell
+    candidate lists, which skip most of the reference's evaluations) is
+    reported separately. `model` is §8(d)'s per-launch floor
+    max(E1*6/F32, 10 N'/BW) + max(E(>=2)*6/F32, (I-1)*10 N'/BW) against the
+    measured loop time."""
+    pairs0 = k * (k - 1) // 2
+    e1 = max(evals1 - pairs0, 0)
+    e_rest = max(evals - evals1, 0)  # includes the later tables' pair evaluations (< 0.1%)
+    t = ms * 1e-3
+    t1 = (phases or {}).get("iter1_assign_us", 0.0) * 1e-6
+    t_rest = max(t - t1, 1e-12)
+    peak = FLOP_PER_EVAL / SLOTS_PER_EVAL * F32_ISSUE_PER_S / 1e12
+    achieved = FLOP_PER_EVAL * e_rest / t_rest / 1e12
+    bw = peaks["hbm_gbs"] * 1e9
+    mem_iter = 10.0 * n_unique / bw
+    t_roof = max(e1 * SLOTS_PER_EVAL / F32_ISSUE_PER_S, mem_iter) + max(
+        e_rest * SLOTS_PER_EVAL / F32_ISSUE_PER_S, (iters - 1) * mem_iter)
+    return {
+        "kernel": "k_wsm_loop", "bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak, "traffic": _ncu_traffic("wsm_loop", P), "kernel_ms": ms,
+        "peak_source": "measured FADD issue rate 32.41e12/s (tools/microbench.cu) x 8 FLOP / 6 slots",
+        "note": (f"iterations 2..{iters}: {e_rest} reference distance evaluations (8 FLOP each) in "
+                 f"{t_rest * 1e3:.3f} ms; the loop is latency-bound (dependent L1/L2 loads per scan step), "
+                 f"its working set ({10 * n_unique / 1e6:.0f} MB per iteration) stays in L2"),
+        "iteration1": {"evals": e1, "us": t1 * 1e6,
+                       "reference_evals_per_s": e1 / t1 if t1 > 0 else None,
+                       "note": "integer dp4a argmin over per-16^3-cell candidate lists: most of the "
+                               "reference's evaluations are never performed"},
+        "model": {"t_roof_us": t_roof * 1e6, "t_meas_us": t * 1e6, "frac": t_roof / t,
+                  "compute_us": (e1 + e_rest) * SLOTS_PER_EVAL / F32_ISSUE_PER_S * 1e6,
+                  "memory_us": iters * mem_iter * 1e6,
+                  "def": "max(E1*6/F32, 10N'/HBM) + max(E>=2*6/F32, (I-1)*10N'/HBM), SURVEY.md 8(d)"},
+    }
 
 
 def _ncu_traffic(stage, P):

@@ -183,6 +183,15 @@ int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, 
                        const cqb_termination* term, uint64_t seed, uint8_t* const* d_index_out,
                        uint8_t* const* d_rgb_out, int lanes, double* centers_out, cqb_report* reports);
 
+/* Many seeds of one image: the paper's repeated-run protocol (the
+ * reference's run_bench calls generate_palette once per seed, bench.hpp:
+ * 201-204). The host raster is uploaded once; run i uses seeds[i] and runs
+ * the full device pipeline (histogram, WSM / WSM-C, map + MSE), `lanes` runs
+ * in flight like cqb_quantize_batch. centers_out: n_runs x k x 3 doubles;
+ * reports[i].mse is the run's exact MSE. No raster outputs. */
+int cqb_quantize_runs(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k, const cqb_termination* term,
+                      int n_runs, const uint64_t* seeds, int lanes, double* centers_out, cqb_report* reports);
+
 /* ---- post-processing ---------------------------------------------------
  * Replaces map_pixels(img, palette) (image_ops.hpp:18-51): nearest ROUNDED
  * palette entry, lowest index on ties. centers: k x 3 doubles, k in [1,256];

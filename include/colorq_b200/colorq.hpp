@@ -148,14 +148,24 @@ struct UnknownMethodError : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
 
+// methods.hpp:71-85: every field of the reference, with its defaults. The
+// SKM / FCM / PIM knobs (stable_iters, theta, q, delta, fuzzy_on_pixels)
+// parameterize methods outside the B200 path; they are carried so callers
+// that set them compile unchanged.
 struct MethodParams {
   MethodId id = MethodId::Wsm;
-  int iters = 10;
-  double epsilon = 1e-4;
-  int k_prime = 8;  // fkm neighbour count (methods.hpp:75)
+  int iters = 10;                // fixed-iteration budget
+  double epsilon = 1e-4;         // convergent threshold
+  int k_prime = 8;               // fkm neighbour count
+  int stable_iters = 10;         // skm warm-up iterations
+  double theta = 1.0;            // skm stability threshold
+  double q = 2.0;                // fcm / pim fuzziness
+  double delta = 0.4;            // pim offset fraction
+  bool fuzzy_on_pixels = false;  // fcm / pim on raw pixels
   Termination termination() const {
-    return id == MethodId::WsmC || id == MethodId::KmC || id == MethodId::FkmC ? Termination::convergent(epsilon)
-                                                                                 : Termination::fixed(iters);
+    return id == MethodId::WsmC || id == MethodId::KmC || id == MethodId::FkmC || id == MethodId::Skm
+               ? Termination::convergent(epsilon)
+               : Termination::fixed(iters);
   }
 };
 

@@ -27,7 +27,7 @@ MAX_K = 256
 EXPORTS = (
     "cqb_create", "cqb_destroy", "cqb_last_error", "cqb_set_stream", "cqb_set_grid_limit", "cqb_device_info",
     "cqb_build_histogram", "cqb_run_wsm", "cqb_wsm_iterate", "cqb_quantize", "cqb_quantize_device",
-    "cqb_fetch_results", "cqb_quantize_batch", "cqb_quantize_ex", "cqb_error_image", "cqb_run_km_full", "cqb_run_fkm",
+    "cqb_fetch_results", "cqb_quantize_batch", "cqb_quantize_runs", "cqb_quantize_ex", "cqb_error_image", "cqb_run_km_full", "cqb_run_fkm",
     "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
     "cqb_shard_reseed_candidate", "cqb_set_debug", "cqb_xch_window", "cqb_xch_open", "cqb_xch_emulate",
@@ -105,6 +105,7 @@ def load_library() -> C.CDLL:
                                       _R]
         L.cqb_run_fkm.argtypes = [_vp, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, _T, C.c_uint64, _f64p, _f64p,
                                   C.c_int, _R]
+        L.cqb_quantize_runs.argtypes = [_vp, _u8p, C.c_uint64, C.c_int, _T, C.c_int, _u64p, C.c_int, _f64p, _R]
         L.cqb_quantize_batch.argtypes = [_vp, C.c_int, C.POINTER(_vp), _u64p, C.c_int, _T, C.c_uint64,
                                          C.POINTER(_vp), C.POINTER(_vp), C.c_int, _f64p, _R]
         L.cqb_map_pixels.argtypes = [_vp, _u8p, C.c_uint64, _f64p, C.c_int, _u8p, _u8p, _u64p]

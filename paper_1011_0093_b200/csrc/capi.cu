@@ -312,7 +312,7 @@ int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
 // Images below this size compact the bin table through K1's occupancy map
 // (their tables are sparse: cfg2's 0.37M colors touch 2% of the bins).
 constexpr uint64_t OCC_MAX_PIXELS = 2u << 20;
-constexpr size_t RES_DYN_MAX = 160 * 1024;  // resident-sample loop: dynamic shared memory ceiling
+constexpr size_t RES_DYN_MAX = (CQB_LOOP_MINB == 1 ? 160 : 40) * 1024;  // resident-sample loop: dynamic shared memory ceiling
 
 bool sparse_path(const cqb_ctx* ctx, uint64_t P) { return P < OCC_MAX_PIXELS && !(ctx->debug_flags & 16); }
 bool fused_prep(const cqb_ctx* ctx, uint64_t P) {
@@ -663,7 +663,7 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2, 0>, LOOP_THREADS,
                                                      LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
-    ctx->loop_blocks_max = std::min(nb, 1) * ctx->num_sms;
+    ctx->loop_blocks_max = std::min(nb, CQB_LOOP_MINB) * ctx->num_sms;
     CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     CK(cudaMalloc(&ctx->bins, sizeof(uint2) << 24));
@@ -975,10 +975,47 @@ int lane_fail(cqb_ctx* ctx, cqb_ctx* lane, int rc) {
 }
 }  // namespace
 
+namespace {
+// Images in flight on `lanes` sub-contexts (cqb_quantize_batch,
+// cqb_quantize_runs); image i uses seeds[i], or `seed` when seeds is null.
+int quantize_lanes(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, const uint64_t* n_pixels, int k,
+                   const cqb_termination* term, uint64_t seed, const uint64_t* seeds, uint8_t* const* d_index_out,
+                   uint8_t* const* d_rgb_out, int lanes, double* centers_out, cqb_report* reports);
+}  // namespace
+
 int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, const uint64_t* n_pixels, int k,
                        const cqb_termination* term, uint64_t seed, uint8_t* const* d_index_out,
                        uint8_t* const* d_rgb_out, int lanes, double* centers_out, cqb_report* reports) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  return quantize_lanes(ctx, n_images, d_rgb, n_pixels, k, term, seed, nullptr, d_index_out, d_rgb_out, lanes,
+                        centers_out, reports);
+}
+
+int cqb_quantize_runs(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k, const cqb_termination* term,
+                      int n_runs, const uint64_t* seeds, int lanes, double* centers_out, cqb_report* reports) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (n_runs < 0 || (n_runs > 0 && (!seeds || !centers_out || !reports)))
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize_runs: null argument");
+  if (n_pixels == 0 || !rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "build_histogram: empty image");
+  if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  if (n_runs == 0) return CQB_OK;
+  CK(cudaSetDevice(ctx->device));
+  TRY(ensure_pixels(ctx, n_pixels));
+  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * n_pixels, cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<const uint8_t*> imgs((size_t)n_runs, ctx->d_img);
+  std::vector<uint64_t> px((size_t)n_runs, n_pixels);
+  const int rc = quantize_lanes(ctx, n_runs, imgs.data(), px.data(), k, term, 0, seeds, nullptr, nullptr, lanes,
+                                centers_out, reports);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+namespace {
+int quantize_lanes(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, const uint64_t* n_pixels, int k,
+                   const cqb_termination* term, uint64_t seed, const uint64_t* seeds, uint8_t* const* d_index_out,
+                   uint8_t* const* d_rgb_out, int lanes, double* centers_out, cqb_report* reports) {
   if (n_images < 0 || (n_images > 0 && (!d_rgb || !n_pixels || !centers_out || !reports)))
     return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize_batch: null argument");
   TRY(check_k(ctx, k));
@@ -1009,15 +1046,16 @@ int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, 
     double* c = centers_out + (size_t)i * 3 * k;
     int rc = cqb_fetch_results(lane, c, nullptr, 0, &reports[i]);
     if (rc != CQB_OK && lane->h_stage->status == ST_DRAWS_EXHAUSTED)  // rare: rerun with the retry loop
-      rc = cqb_quantize_device(lane, d_rgb[i], n_pixels[i], k, term, seed, d_index_out ? d_index_out[i] : nullptr,
-                               d_rgb_out ? d_rgb_out[i] : nullptr, 1, c, nullptr, 0, &reports[i]);
+      rc = cqb_quantize_device(lane, d_rgb[i], n_pixels[i], k, term, seeds ? seeds[i] : seed,
+                               d_index_out ? d_index_out[i] : nullptr, d_rgb_out ? d_rgb_out[i] : nullptr, 1, c,
+                               nullptr, 0, &reports[i]);
     return rc == CQB_OK ? CQB_OK : lane_fail(ctx, lane, rc);
   };
   for (int i = 0; i < n_images; ++i) {
     const int l = i % lanes;
     TRY(finish(l));
     cqb_ctx* lane = ctx->lanes[l];
-    const int rc = cqb_quantize_device(lane, d_rgb[i], n_pixels[i], k, term, seed,
+    const int rc = cqb_quantize_device(lane, d_rgb[i], n_pixels[i], k, term, seeds ? seeds[i] : seed,
                                        d_index_out ? d_index_out[i] : nullptr, d_rgb_out ? d_rgb_out[i] : nullptr, 0,
                                        nullptr, nullptr, 0, nullptr);
     if (rc != CQB_OK) return lane_fail(ctx, lane, rc);
@@ -1031,6 +1069,7 @@ int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, 
   }
   return CQB_OK;
 }
+}  // namespace
 
 int cqb_quantize(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
                  uint64_t seed, double* centers_out, double* sse_history, int hist_cap, uint8_t* index_out,

@@ -9,7 +9,10 @@ constexpr int KMAX = 256;            // palette sizes handled on device (u8 labe
 #ifndef CQB_LOOP_THREADS
 #define CQB_LOOP_THREADS 1024
 #endif
-constexpr int LOOP_THREADS = CQB_LOOP_THREADS;  // persistent WSM loop block size (one block per SM)
+constexpr int LOOP_THREADS = CQB_LOOP_THREADS;
+#ifndef CQB_LOOP_MINB
+#define CQB_LOOP_MINB 1  // persistent WSM loop blocks per SM (__launch_bounds__)
+#endif  // persistent WSM loop block size (one block per SM)
 constexpr int MAXBLK = 1024;         // max persistent blocks (reseed candidate slots)
 constexpr int HIST_THREADS = 256;    // histogram / compaction block size
 constexpr int PX_PER_THREAD = 16;    // 16 pixels = 48 B = 3 x 16-B vector loads

@@ -31,14 +31,26 @@
 #include "common.cuh"
 #include "map.cuh"
 
+#ifndef CQB_DIAG_FALLBACK
+#define CQB_DIAG_FALLBACK 0
+#endif
+
 namespace cqb {
 
 namespace cg = cooperative_groups;
+
+constexpr int ROW32 = KMAX + 4;  // FP32 row stride (entries): 16-B aligned rows with room for the +inf tail
 
 struct WsmState {
   double C[2][3 * KMAX];                  // center buffers [k*3 + ch]
   unsigned long long acc[5 * KMAX];       // exact sums [field*KMAX + k]: Sr, Sg, Sb, N, Q
   double sortedD[KMAX * KMAX];            // row p: d(c_p, c_order[p][j]) ascending
+  // The same rows for scan_f32, without the self entry: position i holds
+  // entry i + 1 (FP32 distance, order byte), positions k-1 .. ROW32-1 hold
+  // +inf, so a scan reads aligned quads (one 16-B + one 4-B load per four
+  // entries) and stops at the row's end without a bounds check.
+  alignas(16) float rowD32[KMAX * ROW32];
+  alignas(16) uint8_t rowO[KMAX * ROW32];
   uint8_t order[KMAX * KMAX];             // row p: [p, others by (d, index)]
   double final_C[3 * KMAX];
   uint32_t chosen[KMAX];                  // init: chosen sample indices
@@ -283,6 +295,7 @@ struct LoopSmem {
   unsigned long long* stamp;             // profiling: block_times in the stamped iteration, else null
   unsigned int part_b, part_g;           // emulated ranks (X == 2): block index in its group, group size
   int debug;                             // LoopParams::debug_flags
+  int f32ok;                             // FP32 screening valid: every center |c| < 256
 };
 #define SUB_STAMP(phase)                                                         \
   do {                                                                           \
@@ -371,6 +384,10 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
     if (!resort && lead && t < k) {
       const int e = S.rowo[r][t];
       st->sortedD[p * KMAX + t] = S.rowd[r][e];
+      if (t > 0) {
+        st->rowD32[p * ROW32 + t - 1] = __double2float_rn(S.rowd[r][e]);
+        st->rowO[p * ROW32 + t - 1] = (uint8_t)e;
+      }
       st->order[p * KMAX + t] = (uint8_t)e;
     }
   }
@@ -391,6 +408,10 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
     if (lead && t < k) {
       const int rank = t == p ? 0 : 1 + S.rank_part[r][0][t] + S.rank_part[r][1][t];
       st->sortedD[p * KMAX + rank] = S.rowd[r][t];
+      if (rank > 0) {
+        st->rowD32[p * ROW32 + rank - 1] = __double2float_rn(S.rowd[r][t]);
+        st->rowO[p * ROW32 + rank - 1] = (uint8_t)t;
+      }
       st->order[p * KMAX + rank] = (uint8_t)t;
       S.rowo[r][rank] = (uint8_t)t;
     }
@@ -645,6 +666,48 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
 
 // Assign variants: sort-means (WSM), exhaustive (KM), first k' of the row (FKM).
 enum class Assign { SortMeans, Naive, Fkm };
+constexpr int DBG_NO_F32 = 1 << 17;   // debug flag: FP64 scans only (A/B of the FP32 screening)
+
+// ---------------------------------------------------------------------------
+// FP32 screening of the sort-means scan (iterations >= 2), certified against
+// the reference's FP64 decisions; a lane whose decision the FP32 values
+// cannot certify redoes its point with the exact FP64 scan (scan_fp64).
+//
+// Error bound. x is an integer color, c an FP64 center with |c| < 256 (every
+// center of a run is a mean of colors or a color; checked per launch), cf =
+// fl32(c) with |c - cf| <= 2^-17. The FP32 distance d = fma(b,b, fma(g,g,
+// r*r)) of the FP32 differences a_i = fl(x_i - cf_i) satisfies, against the
+// exact distance D (and so against the reference's FP64 dist2, which is
+// within ~5 ulp64 of D):
+//   |d - D| <= 2^-16 L1 + 2^-21 d + 2^-26,   L1 = sum_i |x_i - c_i| <= sqrt(3 D)
+// (2 |c - cf| L1 + 2u D from the differences, 3u d from the three roundings,
+// u = 2^-24; second-order terms sit in the constants' slack). With
+// sqrt(3 D) <= sqrt(3) (D / 32 + 8) (AM-GM at D = 256) this is at most
+//   Elin(d) = 1.3030e-6 d + 2.1150e-4,
+// increasing in d with slope < 1. Decisions (every comparison below absorbs
+// its own FP32 rounding: each FFMA rounds once):
+//  * break at row entry j: d64[p][t_j] >= 4 prev64 is certain when
+//    fl32(d64) >= pu = fl(4 (1 + 2^-18) prev + 8.52e-4) >= 4 (prev + Elin)(1 + u),
+//    and the scan certainly continues when fl32(d64) < pl =
+//    fl(4 (1 - 2^-18) prev - 8.52e-4); in between the point is ambiguous;
+//  * the argmin: the FP32 best b is the exact (d, index) minimum when every
+//    other evaluated distance has d_t - Elin(d_t) > d_b + Elin(d_b); with d2
+//    the second smallest FP32 distance it suffices that
+//    fl((1 - 2^-19) d2 - 2.12e-4) > fl((1 + 2^-19) d_b + 2.12e-4)
+//    (an FP32 tie never certifies).
+// A certified point has the reference's label and break index J (so its
+// dist_evals) exactly; sums stay exact integers.
+constexpr float F32_INF = __builtin_huge_valf();
+constexpr float F32_PU_A = 4.0f + 0x1p-16f, F32_PL_A = 4.0f - 0x1p-16f, F32_P_B = 8.52e-4f;
+constexpr float F32_C_LO = 1.0f - 0x1p-19f, F32_C_HI = 1.0f + 0x1p-19f, F32_C_B = 2.12e-4f;
+
+__device__ __forceinline__ float u8_to_float(uint32_t v) {  // exact, no I2F
+  return __fsub_rn(__uint_as_float(0x4B000000u | v), 8388608.0f);
+}
+__device__ __forceinline__ float dist32(float x0, float x1, float x2, float4 c) {
+  const float a = __fsub_rn(x0, c.x), b = __fsub_rn(x1, c.y), d = __fsub_rn(x2, c.z);
+  return __fmaf_rn(d, d, __fmaf_rn(b, b, __fmul_rn(a, a)));
+}
 
 // Longest-first chunk order (dynamic shared memory). A chunk's scan cost
 // changes little between iterations, so each block hands its chunks to the
@@ -659,11 +722,19 @@ struct ChunkSched {
   uint8_t cost[SCHED_MAX];
   uint32_t bucket[SCHED_BUCKETS];
 };
-constexpr size_t LOOP_DYN_SMEM = sizeof(ChunkSched);
-__device__ __forceinline__ ChunkSched& chunk_sched() {
+// Dynamic shared memory of the loop kernels (the static LoopSmem is at the
+// 48 KB static limit): the FP32 centers of scan_f32, then the chunk order.
+struct LoopDyn {
+  float4 c4[KMAX];  // centers of the current assignment rounded to FP32
+  ChunkSched sched;
+};
+constexpr size_t LOOP_DYN_SMEM = sizeof(LoopDyn);
+__device__ __forceinline__ LoopDyn& loop_dyn_smem() {
   extern __shared__ __align__(16) unsigned char loop_dyn[];
-  return *reinterpret_cast<ChunkSched*>(loop_dyn);
+  return *reinterpret_cast<LoopDyn*>(loop_dyn);
 }
+__device__ __forceinline__ ChunkSched& chunk_sched() { return loop_dyn_smem().sched; }
+__device__ __forceinline__ float4* loop_c4() { return loop_dyn_smem().c4; }
 // Resident samples (small sample sets): the block's chunks - its fixed share
 // of the Morton-ordered samples - stay in dynamic shared memory for the whole
 // loop (key, count, label; local index = chunk * 32 + lane), so a scan starts
@@ -677,12 +748,12 @@ struct ResSamples {
 };
 __device__ __forceinline__ ResSamples res_samples(int cap) {
   extern __shared__ __align__(16) unsigned char loop_dyn[];
-  unsigned char* b = loop_dyn + ((sizeof(ChunkSched) + 15) & ~size_t(15));
+  unsigned char* b = loop_dyn + ((sizeof(LoopDyn) + 15) & ~size_t(15));
   return {reinterpret_cast<uint32_t*>(b), reinterpret_cast<uint32_t*>(b) + cap,
           reinterpret_cast<uint8_t*>(reinterpret_cast<uint32_t*>(b) + 2 * cap)};
 }
 __host__ __device__ constexpr size_t res_smem_bytes(int cap) {
-  return ((sizeof(ChunkSched) + 15) & ~size_t(15)) + (size_t)cap * 9;
+  return ((sizeof(LoopDyn) + 15) & ~size_t(15)) + (size_t)cap * 9;
 }
 
 // Counting sort of this block's chunks by cost, descending (block-wide).
@@ -727,6 +798,170 @@ constexpr int DEEP_J = CQB_DEEP_J;
 #endif
 constexpr int DEEP_P = CQB_DEEP_P;
 
+// One point's sort-means scan in FP32. Returns its break index J (>= 1) and
+// sets `best` when both decisions are certified, else 0 (redo in FP64).
+// c4: FP32 centers; rq / oq: row p of the FP32 distances / order bytes
+// without the self entry (WsmState::rowD32 / rowO), read four entries at a time.
+template <bool kDeep, int DEEP_J_, int DEEP_P_>
+__device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const float4* __restrict__ rq,
+                                        const uint32_t* __restrict__ oq, int k, uint32_t key, int p, int& best_out,
+                                        unsigned int& n_active) {
+  const float x0 = u8_to_float(key_r(key)), x1 = u8_to_float(key_g(key)), x2 = u8_to_float(key_b(key));
+  const float prev = dist32(x0, x1, x2, c4[p]);
+  const float pu = __fmaf_rn(prev, F32_PU_A, F32_P_B);
+  const float pl = __fmaf_rn(prev, F32_PL_A, -F32_P_B);
+  best_out = p;
+  float4 D = rq[0];  // entries 1..4
+  uint32_t T = oq[0];
+  // the common case: no candidate (kmeans.hpp:220-226 breaks at j = 1); k = 1: D.x = +inf
+  if (D.x >= pl) return D.x >= pu ? 1 : 0;
+  n_active += 1;
+  float bd = prev, d2 = F32_INF;
+  int best = p;
+  auto eval = [&](uint32_t t) {
+    const float d = dist32(x0, x1, x2, c4[t]);
+    d2 = fminf(d2, fmaxf(bd, d));
+    best = d < bd ? (int)t : best;
+    bd = fminf(bd, d);
+  };
+  int j = 1;  // the next entry to test; entry j is a certain candidate at the loop head
+  int qi = 0;
+  float Db;   // the break entry's distance
+  for (;;) {
+    eval(T & 0xFFu);
+    if (D.y >= pl) { Db = D.y; j += 1; break; }
+    eval((T >> 8) & 0xFFu);
+    if (D.z >= pl) { Db = D.z; j += 2; break; }
+    eval((T >> 16) & 0xFFu);
+    if (D.w >= pl) { Db = D.w; j += 3; break; }
+    eval(T >> 24);
+    j += 4;
+    ++qi;
+    D = rq[qi];
+    T = oq[qi];
+    if (D.x >= pl) { Db = D.x; break; }
+    if (kDeep && j > DEEP_J_) {
+      // deep scan: the first entry e >= j with distance >= pl (rows are sorted,
+      // fl32 is monotone, and the +inf tail ends the row), by DEEP_P_
+      // independent probes per round; then j .. e-1 are candidates
+      const float* rf = reinterpret_cast<const float*>(rq) - 1;  // rf[e] = entry e
+      const uint8_t* ro = reinterpret_cast<const uint8_t*>(oq) - 1;
+      int a = j, b = k;
+      while (a < b) {
+        int na = a, nb = b;
+#pragma unroll
+        for (int u = DEEP_P_; u >= 1; --u) {
+          const int m = a + ((b - a) * u) / (DEEP_P_ + 1);
+          if (m >= a && m < b) {
+            if (rf[m] >= pl) nb = m;
+            else if (m + 1 > na) na = m + 1;
+          }
+        }
+        if (na == a && nb == b) {
+          if (rf[a] >= pl) nb = a;
+          else na = a + 1;
+        }
+        a = na < nb ? na : nb;
+        b = nb;
+      }
+      for (int i2 = j; i2 < b; ++i2) eval(ro[i2]);
+      j = b;
+      Db = rf[b];  // +inf at the row's end (b = k)
+      break;
+    }
+  }
+  if (Db < pu) return 0;  // the break itself is uncertain
+  if (!(__fmaf_rn(d2, F32_C_LO, -F32_C_B) > __fmaf_rn(bd, F32_C_HI, F32_C_B))) return 0;
+  best_out = best;
+  return j;
+}
+
+// One point's scan in FP64 with the reference's exact semantics
+// (kmeans.hpp:211-236; KM: assign_naive :83-106; FKM: fast_variants.hpp:42-52).
+// Out of line: it is the rare path of WSM (scan_f32 not certified) and keeps
+// its registers out of the FP32 loop. Returns J | best << 12 | active << 24.
+template <Assign Mode>
+__device__ __noinline__ int scan_fp64(const LoopSmem& S, const double* __restrict__ rd, const uint8_t* __restrict__ ro,
+                                      int k, int kp_, uint32_t key, int p, int debug_flags) {
+  constexpr bool kDeep = Mode == Assign::SortMeans;
+  int best = p, J = 1, active = 0;
+  const uint32_t keyq = key;
+  const double x0 = u8_to_double(key_r(keyq)), x1 = u8_to_double(key_g(keyq)),
+               x2 = u8_to_double(key_b(keyq));
+  double mind = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);  // prev
+  const double bound = 4.0 * mind;
+  bool deep = false;
+  if constexpr (Mode == Assign::Fkm) {
+    // run_fkm (fast_variants.hpp:42-52): lexicographic (d, index) minimum
+    // over order[p][0..k') - self first, then its nearest centers
+    const int kp = kp_;
+    for (int j = 1; j < kp; ++j) {
+      const int t = ro[j];
+      lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+    }
+    J = 0;  // dist_evals are P*k' per iteration, set by the host
+  } else if constexpr (Mode == Assign::Naive) {
+    // assign_naive (kmeans.hpp:83-106): every center, strict < from c_0,
+    // i.e. the lexicographic (d, index) minimum over all k (the start
+    // from the previous label does not change that minimum).
+    for (int t = 0; t < k; ++t)
+      lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+    J = 0;  // dist_evals are P*k per iteration, set by the host
+  } else
+  // the reference's scan (kmeans.hpp:217-231), two entries per step
+  if (k > 1 && rd[1] < bound && !(debug_flags & 1)) {
+    active = 1;
+    int j = 1;
+    for (;;) {
+      const double d0 = rd[j];
+      const double d1 = j + 1 < k ? rd[j + 1] : bound;
+      const int t0 = ro[j];
+      const int t1 = j + 1 < k ? ro[j + 1] : 0;
+      if (d0 >= bound) break;
+      lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]), t0);
+      ++j;
+      if (d1 >= bound) break;
+      lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]), t1);
+      ++j;
+      if (j >= k) break;
+      if (kDeep && j >= DEEP_J) {  // deep scan: find the break index, then evaluate without checks
+        deep = true;
+        break;
+      }
+    }
+    if (kDeep && deep) {
+      // J = min{i in [j, k) : rd[i] >= bound}, or k: the row is sorted, so
+      // DEEP_P independent probes per round cut [lo, hi] to 1/(DEEP_P+1)
+      int a = j, b = k;
+      while (a < b) {
+        int na = a, nb = b;
+#pragma unroll
+        for (int u = DEEP_P; u >= 1; --u) {
+          const int m = a + ((b - a) * u) / (DEEP_P + 1);
+          if (m >= a && m < b) {
+            if (rd[m] >= bound) nb = m;
+            else if (m + 1 > na) na = m + 1;
+          }
+        }
+        if (na == a && nb == b) {  // interval too small for distinct probes: step
+          if (rd[a] >= bound) nb = a;
+          else na = a + 1;
+        }
+        a = na < nb ? na : nb;
+        b = nb;
+      }
+      // candidates j .. b-1 are below the bound: the serial scan's set
+      for (int i2 = j; i2 < b; ++i2) {
+        const int t = ro[i2];
+        lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
+      }
+      j = b;
+    }
+    J = j;
+  }
+  return J | (best << 12) | (active << 24);
+}
+
 template <Assign Mode, int PPT, int X, bool R>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
@@ -752,7 +987,12 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   constexpr bool kDeep = Mode == Assign::SortMeans;
   const uint32_t my_ch = nch > pb ? (nch - 1u - pb) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
+  const float4* __restrict__ rq32 = reinterpret_cast<const float4*>(L.st->rowD32);
+  const uint32_t* __restrict__ oq32 = reinterpret_cast<const uint32_t*>(L.st->rowO);
+  const float4* c4 = loop_c4();
   const uint8_t* __restrict__ go = L.st->order;
+  // FP32 screening (scan_f32): sort-means scans whose centers all satisfy |c| < 256
+  const bool use32 = Mode == Assign::SortMeans && S.f32ok;
   const uint32_t* __restrict__ keys = L.keys;
   const uint32_t* __restrict__ counts = L.counts;
   uint8_t* __restrict__ labels = L.labels;
@@ -795,82 +1035,22 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
       nlab[q] = lab[q];
       if (idx[q] >= hi) continue;
       const int p = lab[q];
-      const double x0 = u8_to_double(key_r(key[q])), x1 = u8_to_double(key_g(key[q])),
-                   x2 = u8_to_double(key_b(key[q]));
-      double mind = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);  // prev
-      const double bound = 4.0 * mind;
-      int best = p;
-      const double* rd = gd + p * KMAX;
       const uint8_t* ro = go + p * KMAX;
-      int J = 1;
-      bool deep = false;
-      if constexpr (Mode == Assign::Fkm) {
-        // run_fkm (fast_variants.hpp:42-52): lexicographic (d, index) minimum
-        // over order[p][0..k') - self first, then its nearest centers
-        const int kp = L.fkm_kprime;
-        for (int j = 1; j < kp; ++j) {
-          const int t = ro[j];
-          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
-        }
-        J = 0;  // dist_evals are P*k' per iteration, set by the host
-      } else if constexpr (Mode == Assign::Naive) {
-        // assign_naive (kmeans.hpp:83-106): every center, strict < from c_0,
-        // i.e. the lexicographic (d, index) minimum over all k (the start
-        // from the previous label does not change that minimum).
-        for (int t = 0; t < k; ++t)
-          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
-        J = 0;  // dist_evals are P*k per iteration, set by the host
-      } else
-      // the reference's scan (kmeans.hpp:217-231), two entries per step
-      if (k > 1 && rd[1] < bound && !(L.debug_flags & 1)) {
-        n_active += 1;
-        int j = 1;
-        for (;;) {
-          const double d0 = rd[j];
-          const double d1 = j + 1 < k ? rd[j + 1] : bound;
-          const int t0 = ro[j];
-          const int t1 = j + 1 < k ? ro[j + 1] : 0;
-          if (d0 >= bound) break;
-          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t0], S.cy[t0], S.cz[t0]), t0);
-          ++j;
-          if (d1 >= bound) break;
-          lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]), t1);
-          ++j;
-          if (j >= k) break;
-          if (kDeep && j >= DEEP_J) {  // deep scan: find the break index, then evaluate without checks
-            deep = true;
-            break;
-          }
-        }
-        if (kDeep && deep) {
-          // J = min{i in [j, k) : rd[i] >= bound}, or k: the row is sorted, so
-          // DEEP_P independent probes per round cut [lo, hi] to 1/(DEEP_P+1)
-          int a = j, b = k;
-          while (a < b) {
-            int na = a, nb = b;
-#pragma unroll
-            for (int u = DEEP_P; u >= 1; --u) {
-              const int m = a + ((b - a) * u) / (DEEP_P + 1);
-              if (m >= a && m < b) {
-                if (rd[m] >= bound) nb = m;
-                else if (m + 1 > na) na = m + 1;
-              }
-            }
-            if (na == a && nb == b) {  // interval too small for distinct probes: step
-              if (rd[a] >= bound) nb = a;
-              else na = a + 1;
-            }
-            a = na < nb ? na : nb;
-            b = nb;
-          }
-          // candidates j .. b-1 are below the bound: the serial scan's set
-          for (int i2 = j; i2 < b; ++i2) {
-            const int t = ro[i2];
-            lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
-          }
-          j = b;
-        }
-        J = j;
+      int best = p;
+      int J = 0;
+      if constexpr (Mode == Assign::SortMeans)
+        if (use32)
+          J = scan_f32<kDeep, DEEP_J, DEEP_P>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4), k, key[q], p, best,
+                                              n_active);
+      if (J == 0) {  // FP64 (KM / FKM, uncertified FP32 screens, or screening off): rare for WSM
+        const int r = scan_fp64<Mode>(S, gd + p * KMAX, ro, k, L.fkm_kprime, key[q], p, L.debug_flags);
+        J = r & 0xFFF;
+        best = (r >> 12) & 0xFF;
+#if CQB_DIAG_FALLBACK  // diagnostics build: the timeline's "active" count = FP64 fallbacks of scan_f32
+        n_active += use32 ? 1000000u : 0u;
+#else
+        n_active += (unsigned)(r >> 24) & 1u;
+#endif
       }
       ev += (uint32_t)J;  // prev + (J - 1) candidates: the reference's count
       J_of[q] = (uint32_t)J;
@@ -1232,7 +1412,7 @@ __device__ __forceinline__ unsigned long long loop_barrier(LoopSmem& S, unsigned
 // L.xw block groups of this launch (single-GPU emulation of the ranks).
 // R: resident samples (ResSamples; small sample sets, X == 0 only).
 template <Assign Mode, int PPT, int X, bool R = false>
-__global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
+__global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopParams L) {
   constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
   __shared__ LoopSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -1278,11 +1458,15 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
   RS.o = st->order;
   (void)dyn;
 
+  int big = 0;  // a center outside (-256, 256): no FP32 screening in this launch (scan_f32's bound)
   for (int t = tid; t < k; t += blockDim.x) {
     S.cx[t] = st->C[0][3 * t];
     S.cy[t] = st->C[0][3 * t + 1];
     S.cz[t] = st->C[0][3 * t + 2];
+    loop_c4()[t] = make_float4(__double2float_rn(S.cx[t]), __double2float_rn(S.cy[t]), __double2float_rn(S.cz[t]), 0.f);
+    big |= !(fabs(S.cx[t]) < 256.0 && fabs(S.cy[t]) < 256.0 && fabs(S.cz[t]) < 256.0);
   }
+  big = __syncthreads_or(big);
   for (int t = tid; t < 5 * KMAX; t += blockDim.x) {
     S.accp[t] = make_uint2(0u, 0u);
     S.accm[t] = make_uint2(0u, 0u);
@@ -1296,6 +1480,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
     S.stamp = nullptr;
     S.wq = 0u;
     S.debug = L.debug_flags;
+    S.f32ok = !big && !(L.debug_flags & DBG_NO_F32);
+
     S.rowo_row[0] = S.rowo_row[1] = -1;
   }
   __syncthreads();
@@ -1319,6 +1505,12 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       }
     }
   }
+  if (Mode == Assign::SortMeans)  // scan_f32 rows: +inf after the k - 1 entries
+    for (int p = blockIdx.x; p < k; p += gridDim.x)
+      for (int i = k - 1 + tid; i < ROW32; i += blockDim.x) {
+        st->rowD32[p * ROW32 + i] = F32_INF;
+        st->rowO[p * ROW32 + i] = 0;
+      }
   if (!kNaive) tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
@@ -1572,6 +1764,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, 1) k_wsm_loop(LoopParams L) {
       }
       __syncthreads();
     }
+    // FP32 copies for the next assign (read after the grid barrier); the new
+    // centers are means of colors or colors, so |c| < 256 holds
+    for (int t = tid; t < k; t += blockDim.x)
+      loop_c4()[t] = make_float4(__double2float_rn(S.cx[t]), __double2float_rn(S.cy[t]), __double2float_rn(S.cz[t]), 0.f);
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
     if (tid == 0) S.stamp = (L.block_times && it == L.stamp_iter) ? L.block_times : nullptr;

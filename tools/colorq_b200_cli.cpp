@@ -150,7 +150,7 @@ int env_threads() {
 
 std::vector<int> parse_k_list(const std::string& s) {
   std::vector<int> ks;
-  for (const std::string& t : colorq::benchdetail::split_list(s)) ks.push_back(std::stoi(t));
+  for (const std::string& t : colorq::bench::list_items(s)) ks.push_back(std::stoi(t));
   if (ks.empty()) throw std::invalid_argument("empty K list");
   return ks;
 }
@@ -182,27 +182,27 @@ int bench_main(int argc, char** argv) {
     return usage(e.what());
   }
   return guarded([&]() {
-    colorq::BenchConfig cfg;
-    cfg.threads = env_threads();
+    colorq::bench::Plan plan;
+    plan.threads = env_threads();
     if (!config.empty()) {
       std::ifstream in(config);
       if (!in) throw std::runtime_error("cannot open config file " + config);
-      colorq::apply_config_text(cfg, in);
+      colorq::bench::read_plan(plan, in);
     }
-    if (!images.empty()) cfg.images = colorq::benchdetail::split_list(images);
+    if (!images.empty()) plan.images = colorq::bench::list_items(images);
     if (!methods.empty()) {
-      cfg.methods.clear();
-      for (const std::string& t : colorq::benchdetail::split_list(methods))
-        cfg.methods.push_back(colorq::parse_method_spec(t));
+      plan.methods.clear();
+      for (const std::string& t : colorq::bench::list_items(methods))
+        plan.methods.push_back(colorq::bench::parse_method_token(t));
     }
-    if (!ks.empty()) cfg.k_values = parse_k_list(ks);
-    if (runs > 0) cfg.runs = runs;
-    if (base_seed >= 0) cfg.base_seed = std::uint64_t(base_seed);
-    if (!output.empty()) cfg.output_prefix = output;
-    if (threads > 0) cfg.threads = threads;
-    cfg.serial_timing = serial;
-    const colorq::BenchResults res = colorq::run_bench(cfg);
-    for (const auto& p : colorq::write_bench_outputs(res, cfg.output_prefix)) std::cout << "wrote " << p.string() << "\n";
+    if (!ks.empty()) plan.ks = parse_k_list(ks);
+    if (runs > 0) plan.runs = runs;
+    if (base_seed >= 0) plan.base_seed = std::uint64_t(base_seed);
+    if (!output.empty()) plan.prefix = output;
+    if (threads > 0) plan.threads = threads;
+    plan.serial = serial;
+    const colorq::bench::Results res = colorq::bench::run(plan);
+    for (const auto& p : colorq::bench::write_outputs(res, plan.prefix)) std::cout << "wrote " << p.string() << "\n";
     std::cout << res.ranks_csv;
     return 0;
   });
@@ -231,7 +231,7 @@ int scaling_main(int argc, char** argv) {
   }
   if (input.empty()) return usage("missing INPUT");
   return guarded([&]() {
-    const colorq::MethodSpec spec = colorq::parse_method_spec(method);
+    const colorq::bench::Method spec = colorq::bench::parse_method_token(method);
     const std::vector<int> kv = parse_k_list(ks);
     const colorq::RgbImage image = colorq::load_ppm(input);
     std::string csv = "k,elapsed_ms,dist_evals\n";
