@@ -433,8 +433,7 @@ def _loop_phases(tl, iters):
     d = lambda x, y: float(np.mean(y - x)) / 1e3  # noqa: E731
     return {
         "iter1_assign_us": float(tl[0, 3] - tl[0, 0]) / 1e3,
-        "stage_rows_us": d(a[:, 0], a[:, 1]),
-        "points_us": d(a[:, 1], a[:, 2]),
+        "points_us": d(a[:, 0], a[:, 2]),
         "flush_us": d(a[:, 2], a[:, 3]),
         "barrier1_us": d(a[:, 3], a[:, 4]),
         "finalize_us": d(a[:, 4], a[:, 5]),

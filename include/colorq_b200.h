@@ -251,6 +251,13 @@ int cqb_shard_reseed_candidate(cqb_ctx* ctx, uint64_t lo, uint64_t hi, const dou
 #define CQB_IPC_HANDLE_BYTES 64
 int cqb_xch_window(cqb_ctx* ctx, int world, int rank, void* ipc_handle_out);
 int cqb_xch_open(cqb_ctx* ctx, const void* handles);
+/* Peer wait limit of the in-kernel exchange (default 5 s; the first exchange
+ * of a launch waits 4x as long). On a timeout the call fails with
+ * CQB_ERR_NCCL and the exchange is reset: every rank must call
+ * cqb_xch_window + cqb_xch_open (or cqb_xch_emulate) again before the next
+ * cqb_quantize_sharded. */
+int cqb_xch_set_timeout(cqb_ctx* ctx, double seconds);
+
 int cqb_xch_emulate(cqb_ctx* ctx, int vranks);
 int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int k, const cqb_termination* term,
                          uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range);

@@ -31,7 +31,7 @@ EXPORTS = (
     "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
     "cqb_shard_reseed_candidate", "cqb_set_debug", "cqb_xch_window", "cqb_xch_open", "cqb_xch_emulate",
-    "cqb_quantize_sharded",
+    "cqb_quantize_sharded", "cqb_xch_set_timeout",
 )
 IPC_HANDLE_BYTES = 64  # CQB_IPC_HANDLE_BYTES (cudaIpcMemHandle_t)
 # cqb_stage_times intervals: memsets | K1 | K2b | init + bitmap scan + rank (+ gather) | loop | map tables+unique | map pixels
@@ -105,7 +105,8 @@ def load_library() -> C.CDLL:
                                       _R]
         L.cqb_run_fkm.argtypes = [_vp, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, _T, C.c_uint64, _f64p, _f64p,
                                   C.c_int, _R]
-        L.cqb_quantize_runs.argtypes = [_vp, _u8p, C.c_uint64, C.c_int, _T, C.c_int, _u64p, C.c_int, _f64p, _R]
+        if hasattr(L, "cqb_quantize_runs"):  # (older builds in A/B runs lack the newest entry points)
+            L.cqb_quantize_runs.argtypes = [_vp, _u8p, C.c_uint64, C.c_int, _T, C.c_int, _u64p, C.c_int, _f64p, _R]
         L.cqb_quantize_batch.argtypes = [_vp, C.c_int, C.POINTER(_vp), _u64p, C.c_int, _T, C.c_uint64,
                                          C.POINTER(_vp), C.POINTER(_vp), C.c_int, _f64p, _R]
         L.cqb_map_pixels.argtypes = [_vp, _u8p, C.c_uint64, _f64p, C.c_int, _u8p, _u8p, _u64p]
@@ -124,6 +125,8 @@ def load_library() -> C.CDLL:
         L.cqb_xch_window.argtypes = [_vp, C.c_int, C.c_int, _vp]
         L.cqb_xch_open.argtypes = [_vp, _vp]
         L.cqb_xch_emulate.argtypes = [_vp, C.c_int]
+        if hasattr(L, "cqb_xch_set_timeout"):
+            L.cqb_xch_set_timeout.argtypes = [_vp, C.c_double]
         L.cqb_quantize_sharded.argtypes = [_vp, _vp, C.c_uint64, C.c_int, _T, C.c_uint64, _vp, _vp, _u64p]
         _lib = L
         return L

@@ -17,6 +17,7 @@
 #include "map.cuh"
 #include "wsm.cuh"
 #include "prep.cuh"
+#include "part.cuh"
 
 using namespace cqb;
 
@@ -81,6 +82,21 @@ struct cqb_ctx {
   uint32_t* d_mcounts = nullptr;
   uint32_t* d_mrank = nullptr;
   unsigned long long* bin_tile_state = nullptr;  // K2b look-back [N_BIN_TILES] + ticket
+  // partitioned large-image histogram (part.cuh)
+  uint32_t* d_entries = nullptr;       // P bucket entries
+  size_t cap_entries = 0;
+  uint32_t* part_cnt = nullptr;        // [source blocks][PB_N]
+  uint32_t* part_off = nullptr;
+  size_t cap_part = 0;                 // source blocks allocated
+  uint32_t* part_start = nullptr;      // [PB_N + 1]
+  unsigned long long* part_tiles = nullptr;  // H4 look-back [PB_N] + ticket
+  uint32_t* first_tab = nullptr;       // 2^24 first pixel per Morton bin (touched bins only)
+  // init_centers by rank selection over first pixels (hist.cuh RS1-RS4)
+  uint32_t* rs_coarse = nullptr;       // [RS_NC]
+  uint16_t* rs_slot_of = nullptr;      // [RS_NC]
+  uint32_t* rs_tgt = nullptr;          // [2 * KMAX] target block, residual
+  uint32_t* rs_slot_bits = nullptr;
+  size_t cap_slot_bits = 0;
   double* d_weights = nullptr;
   unsigned long long* d_n = nullptr;  // N'
 
@@ -114,6 +130,7 @@ struct cqb_ctx {
   unsigned long long* xpeer[8] = {};   // every rank's window as mapped here (own = xwin)
   unsigned long long* xacc = nullptr;  // mode 2: per-group moment sums
   bool xsharded = false;              // set only while cqb_quantize_sharded enqueues
+  unsigned long long xch_timeout_ns = XCH_TIMEOUT_NS;  // cqb_xch_set_timeout
   uint64_t px_lo = 0, px_hi = 0;      // sharded: pixel range mapped by this rank
 
   unsigned long long* d_draws = nullptr;
@@ -216,6 +233,24 @@ int ensure_samples(cqb_ctx* ctx, size_t n) {
   return CQB_OK;
 }
 
+int ensure_part(cqb_ctx* ctx, uint64_t P, uint32_t blocks) {
+  if (P > ctx->cap_entries) {
+    TRY(grow(ctx, &ctx->d_entries, (size_t)P + 64));
+    ctx->cap_entries = (size_t)P + 64;
+  }
+  if (blocks > ctx->cap_part) {
+    TRY(grow(ctx, &ctx->part_cnt, (size_t)blocks * PB_N));
+    TRY(grow(ctx, &ctx->part_off, (size_t)blocks * PB_N));
+    ctx->cap_part = blocks;
+  }
+  if (!ctx->first_tab) {
+    TRY(grow(ctx, &ctx->first_tab, (size_t)1 << 24));
+    TRY(grow(ctx, &ctx->part_start, (size_t)PB_N + 1));
+    TRY(grow(ctx, &ctx->part_tiles, (size_t)PB_N + 1));
+  }
+  return CQB_OK;
+}
+
 int ensure_hist(cqb_ctx* ctx, int n) {
   if (n <= ctx->cap_hist) return CQB_OK;
   TRY(grow(ctx, &ctx->d_hist, (size_t)n));
@@ -290,11 +325,39 @@ int reset_state(cqb_ctx* ctx) {
 // `bitmap`, the bins hold ~first pixel index (K1) and K2b emits first indices
 // + sets the first-occurrence bitmap; without, they hold ranks
 // (k_bins_scatter).
-int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr) {
+int enqueue_morton(cqb_ctx* ctx, uint32_t* bitmap = nullptr, int first_mode = 0) {
   CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_BIN_TILES + 1), ctx->stream));
   k_bins_compact<<<N_BIN_TILES, BC_THREADS, 0, ctx->stream>>>(
       ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
-      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_BIN_TILES), ctx->d_n, bitmap);
+      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_BIN_TILES), ctx->d_n, bitmap,
+      bitmap || first_mode ? 1 : 0);
+  CKL();
+  return CQB_OK;
+}
+
+// init_centers from first pixel indices (hist.cuh RS1-RS4): the samples carry
+// their first pixel in d_mrank; center i = the chosen[i]-th smallest of them.
+int enqueue_rank_select(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, int ndraws) {
+  const int cs = rank_select_shift(P);
+  const int nc = (int)((P + (1ull << cs) - 1) >> cs);
+  const int wps = 1 << (cs - 5);
+  if ((size_t)KMAX * wps > ctx->cap_slot_bits) {
+    TRY(grow(ctx, &ctx->rs_slot_bits, (size_t)KMAX * wps));
+    ctx->cap_slot_bits = (size_t)KMAX * wps;
+  }
+  CK(cudaMemsetAsync(ctx->rs_coarse, 0, sizeof(uint32_t) * RS_NC, ctx->stream));
+  k_first_coarse<<<ctx->num_sms, 1024, 0, ctx->stream>>>(ctx->d_mrank, ctx->d_n, cs, ctx->rs_coarse);
+  CKL();
+  k_init_select<<<1, RS_THREADS, 0, ctx->stream>>>(ctx->d_n, k, ctx->d_draws, ndraws, ctx->st, ctx->rs_coarse, nc,
+                                                   ctx->rs_slot_of, ctx->rs_tgt, ctx->rs_tgt + KMAX,
+                                                   ctx->rs_slot_bits, wps);
+  CKL();
+  k_first_mark<<<ctx->num_sms, 1024, 0, ctx->stream>>>(ctx->d_mrank, ctx->d_n, cs, ctx->rs_slot_of, wps,
+                                                          ctx->rs_slot_bits);
+  CKL();
+  k_rank_pick<<<(k * 32 + 255) / 256, 256, 0, ctx->stream>>>(ctx->rs_slot_bits, wps, cs, ctx->rs_slot_of,
+                                                              ctx->rs_tgt, ctx->rs_tgt + KMAX, d_img,
+                                                              &ctx->st->status, k, ctx->st->C[0]);
   CKL();
   return CQB_OK;
 }
@@ -327,6 +390,46 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   const uint32_t n_words = (uint32_t)((P + 31) / 32);
   const uint32_t ntiles = (n_words + BS_WORDS - 1) / BS_WORDS;
   const bool fused = fused_prep(ctx, P);
+  if (!sparse_path(ctx, P) && (ctx->debug_flags & DBG_PART_HIST)) {
+    // partitioned histogram (part.cuh): H1-H3 partition the pixels into
+    // 2048 Morton buckets, H4 builds each bucket's table in shared memory
+    // and emits the Morton-order samples, H5 flags first occurrences
+    const PartGeom g = part_geom(P, ctx->num_sms);
+    TRY(ensure_part(ctx, P, g.blocks));
+    CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
+    CK(cudaMemsetAsync(ctx->part_tiles, 0, sizeof(unsigned long long) * (PB_N + 1), ctx->stream));
+    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
+    k_part_count<<<g.blocks, PB_THREADS, 0, ctx->stream>>>(d_img, P, g.range, ctx->part_cnt);
+    CKL();
+    k_part_scan<<<1, PB_THREADS, 0, ctx->stream>>>(ctx->part_cnt, g.blocks, ctx->part_off, ctx->part_start);
+    CKL();
+    k_part_scatter<<<g.blocks, PB_THREADS, 0, ctx->stream>>>(d_img, P, g.range, ctx->part_off, ctx->d_entries);
+    CKL();
+    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
+    k_part_build<<<PB_N, PB_BUILD_THREADS, PB_BUILD_SMEM, ctx->stream>>>(
+        ctx->d_entries, ctx->part_off, ctx->part_start, g.blocks, g.range, ctx->d_mkeys, ctx->d_mcounts,
+        ctx->d_mrank, rank_order ? ctx->first_tab : nullptr, ctx->part_tiles,
+        reinterpret_cast<unsigned int*>(ctx->part_tiles + PB_N),
+        ctx->d_n);
+    CKL();
+    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
+    if (!rank_order) {
+      if (init_k > 0) TRY(enqueue_rank_select(ctx, d_img, P, init_k, ndraws));
+      return CQB_OK;
+    }
+    k_first_flags<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(d_img, P, ctx->first_tab, ctx->d_bitmap);
+    CKL();
+    k_bitmap_scan<<<ntiles, BS_THREADS, 0, ctx->stream>>>(ctx->d_bitmap, n_words, ctx->d_bpre, ctx->tile_state,
+                                                          reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles));
+    CKL();
+    if (rank_order) {  // build_histogram API: ranks + the first-occurrence-ordered histogram
+      k_rank_from_bitmap<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+          ctx->d_bitmap, ctx->d_bpre, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n, ctx->d_keys,
+          ctx->d_counts, ctx->d_first, nullptr, &ctx->st->status, 0, nullptr);
+      CKL();
+    }
+    return CQB_OK;
+  }
   if (!(fused && zero_state)) CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
   if (!fused) CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
@@ -385,6 +488,12 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
         ctx->d_occ, ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
         reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_OCC_TILES), ctx->d_n, ctx->d_bitmap);
     CKL();
+  } else if (!rank_order) {
+    // quantize path: samples keep their first pixel; init selects its ranks
+    TRY(enqueue_morton(ctx, nullptr, 1));
+    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
+    if (init_k > 0) TRY(enqueue_rank_select(ctx, d_img, P, init_k, ndraws));
+    return CQB_OK;
   } else {
     TRY(enqueue_morton(ctx, ctx->d_bitmap));
   }
@@ -453,6 +562,7 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
     X = ctx->xmode;
     L.xw = ctx->xw;
     L.xrank = X == 1 ? ctx->xrank : -1;
+    L.xch_timeout_ns = ctx->xch_timeout_ns;
     for (int r = 0; r < ctx->xw; ++r) L.xbox[r] = ctx->xpeer[r];
     if (X == 1) L.labels = reinterpret_cast<uint8_t*>(ctx->xwin) + XB_LAB_OFF;
     if (X == 2) {
@@ -532,7 +642,14 @@ int check_status(cqb_ctx* ctx) {
   if (s == ST_K_EXCEEDS_N)
     return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
   if (s == ST_DRAWS_EXHAUSTED) return fail(ctx, CQB_ERR_INTERNAL, "init_centers: raw draw buffer exhausted");
-  if (s == ST_XCH_TIMEOUT) return fail(ctx, CQB_ERR_NCCL, "sharded loop: a peer rank did not answer within 5 s");
+  if (s == ST_XCH_TIMEOUT) {
+    // the ranks' exchange counters and flags no longer agree: the windows
+    // must be set up again (cqb_xch_window + cqb_xch_open, or cqb_xch_emulate)
+    // before the next sharded call
+    ctx->xmode = 0;
+    return fail(ctx, CQB_ERR_NCCL, "sharded loop: a peer rank did not answer within %.3g s; exchange reset",
+                (double)ctx->xch_timeout_ns * 1e-9);
+  }
   if (s != ST_OK) return fail(ctx, CQB_ERR_INTERNAL, "device status %d", s);
   return CQB_OK;
 }
@@ -660,6 +777,8 @@ int cqb_create(int device, cqb_ctx** out) {
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
     CK(cudaFuncSetAttribute((const void*)k_wsm_loop<Assign::SortMeans, 1, 0, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RES_DYN_MAX));
+    CK(cudaFuncSetAttribute((const void*)k_part_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)PB_BUILD_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2, 0>, LOOP_THREADS,
                                                      LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
@@ -674,6 +793,9 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMalloc(&ctx->d_cand, (size_t)CAND_CELLS * CAND_CAP));
     CK(cudaMalloc(&ctx->d_cand_n, sizeof(uint16_t) * CAND_CELLS));
     CK(cudaMalloc(&ctx->d_wofs, sizeof(uint32_t) << 19));
+    CK(cudaMalloc(&ctx->rs_coarse, sizeof(uint32_t) * RS_NC));
+    CK(cudaMalloc(&ctx->rs_slot_of, sizeof(uint16_t) * RS_NC));
+    CK(cudaMalloc(&ctx->rs_tgt, sizeof(uint32_t) * 2 * KMAX));
     int pb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_prep_small, PREP_THREADS, 0));
     ctx->prep_blocks = std::min(std::max(pb, 0), 1) * ctx->num_sms;
@@ -725,7 +847,8 @@ int cqb_destroy(cqb_ctx* ctx) {
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
-                 ctx->d_draws};
+                 ctx->d_draws, ctx->d_entries, ctx->part_cnt, ctx->part_off, ctx->part_start, ctx->part_tiles,
+                 ctx->first_tab, ctx->rs_coarse, ctx->rs_slot_of, ctx->rs_tgt, ctx->rs_slot_bits};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_draws) cudaFreeHost(ctx->h_draws);
@@ -1086,9 +1209,9 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   TRY(check_k(ctx, k));
   TRY(check_term(ctx, term));
   const uint64_t P = (uint64_t)width * (uint64_t)height;
+  if (P >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
   CK(cudaSetDevice(ctx->device));
   TRY(ensure_pixels(ctx, P));
-  if (P >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
   CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
   // Pinned (mapped) host outputs are written by the map kernel directly over
   // PCIe (zero-copy), overlapping the transfer with the kernel; pageable ones
@@ -1389,14 +1512,28 @@ int cqb_xch_open(cqb_ctx* ctx, const void* handles) {
   if (ctx->xmode != 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_xch_window first");
   CK(cudaSetDevice(ctx->device));
   for (int r = 0; r < ctx->xw; ++r) {
-    if (r == ctx->xrank) continue;
+    if (r == ctx->xrank || ctx->xpeer[r]) continue;  // own window, or mapped by an earlier (partial) call
     cudaIpcMemHandle_t h;
     memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
     void* p = nullptr;
-    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {  // unmap what this call opened: a retry starts clean
+      for (int q = 0; q < r; ++q)
+        if (q != ctx->xrank && ctx->xpeer[q]) {
+          cudaIpcCloseMemHandle(ctx->xpeer[q]);
+          ctx->xpeer[q] = nullptr;
+        }
+      return fail(ctx, CQB_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+    }
     ctx->xpeer[r] = static_cast<unsigned long long*>(p);
   }
   CK(cudaDeviceSynchronize());
+  return CQB_OK;
+}
+
+int cqb_xch_set_timeout(cqb_ctx* ctx, double seconds) {
+  if (!ctx || !(seconds > 0) || seconds > 3600) return CQB_ERR_INVALID_ARGUMENT;
+  ctx->xch_timeout_ns = (unsigned long long)(seconds * 1e9);
   return CQB_OK;
 }
 
@@ -1423,6 +1560,11 @@ int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, 
   if (ctx->xmode == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "cqb_xch_window + cqb_xch_open (or cqb_xch_emulate) first");
   for (int r = 0; r < ctx->xw; ++r)
     if (!ctx->xpeer[r]) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "exchange window of rank %d not mapped (cqb_xch_open)", r);
+  {  // every sending block must exist (cqb_set_grid_limit may have shrunk the grid since)
+    const int g = loop_grid(ctx);
+    if ((ctx->xmode == 2 && g / ctx->xw < ctx->xw) || (ctx->xmode == 1 && g < ctx->xw))
+      return fail(ctx, CQB_ERR_UNSUPPORTED, "grid of %d blocks too small for %d exchanging ranks", g, ctx->xw);
+  }
   TRY(check_k(ctx, k));
   TRY(check_term(ctx, term));
   if (n_pixels == 0 || !d_rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize: empty image");

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
                                                              uint32_t* __restrict__ m_rank,
                                                              unsigned long long* tile_state, unsigned int* ticket,
                                                              unsigned long long* n_unique,
-                                                             uint32_t* __restrict__ bitmap) {
+                                                             uint32_t* __restrict__ bitmap, int first_mode) {
   constexpr int NW = BC_THREADS / 32;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
       if (f0) {
         m_keys[pos] = key_of_morton(bin);
         m_counts[pos] = v[q].x;
-        const uint32_t y = bitmap ? ~v[q].y : v[q].y;
+        const uint32_t y = first_mode ? ~v[q].y : v[q].y;
         m_rank[pos] = y;
         if (bitmap) atomicOr(&bitmap[y >> 5], 1u << (y & 31));
         ++pos;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
       if (f1) {
         m_keys[pos] = key_of_morton(bin + 1);
         m_counts[pos] = v[q].z;
-        const uint32_t y = bitmap ? ~v[q].w : v[q].w;
+        const uint32_t y = first_mode ? ~v[q].w : v[q].w;
         m_rank[pos] = y;
         if (bitmap) atomicOr(&bitmap[y >> 5], 1u << (y & 31));
       }
@@ -488,6 +488,206 @@ __global__ void __launch_bounds__(256) k_rank_from_bitmap(
     });
   } else {
     rank_pass(bitmap, pre, m_keys, m_counts, m_rank, n, r_keys, r_counts, r_first, [](uint32_t, uint32_t) {});
+  }
+}
+
+// ---------------------------------------------------------------------------
+// init_centers' gather (kmeans.hpp:58-68) without first-occurrence ranks.
+// Center i is the sample of first-occurrence rank chosen[i] (k_init_centers),
+// i.e. the sample with the chosen[i]-th smallest first pixel index f. Only
+// the samples' first pixels (m_first) are needed:
+//   RS1 k_first_coarse  histogram of f >> cs (NC <= 4096 coarse pixel blocks)
+//   RS2 k_init_select   init_centers' chosen ranks; prefix of the coarse counts;
+//                       rank r -> (block, residual);
+//                       the distinct target blocks get a slot
+//   RS3 k_first_mark    a bitmap of the first pixels inside the target blocks
+//   RS4 k_rank_pick     the residual-th set bit of the center's block = its
+//                       first pixel; the center is that pixel's color
+// Two coalesced passes over N' first indices plus K bitmaps of 2^cs bits.
+constexpr int RS_NC = 4096;
+__host__ __device__ inline int rank_select_shift(uint64_t P) {  // smallest cs >= 5 with P >> cs <= RS_NC
+  int cs = 5;
+  while ((P + (1ull << cs) - 1) >> cs > (uint64_t)RS_NC) ++cs;
+  return cs;
+}
+
+__global__ void __launch_bounds__(1024) k_first_coarse(const uint32_t* __restrict__ m_first,
+                                                      const unsigned long long* __restrict__ n_unique, int cs,
+                                                      uint32_t* __restrict__ coarse) {
+  __shared__ uint32_t h[RS_NC];
+  for (int i = threadIdx.x; i < RS_NC; i += blockDim.x) h[i] = 0u;
+  __syncthreads();
+  const uint64_t n = *n_unique, n4 = n / 4;
+  const uint4* f4 = reinterpret_cast<const uint4*>(m_first);  // 16-B aligned allocation
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n4; s += 2 * T) {
+    const uint4 v = __ldg(f4 + s);  // two independent 16-B loads in flight per thread
+    const uint4 u = s + T < n4 ? __ldg(f4 + s + T) : make_uint4(0u, 0u, 0u, 0u);
+    atomicAdd(&h[v.x >> cs], 1u);
+    atomicAdd(&h[v.y >> cs], 1u);
+    atomicAdd(&h[v.z >> cs], 1u);
+    atomicAdd(&h[v.w >> cs], 1u);
+    if (s + T < n4) {
+      atomicAdd(&h[u.x >> cs], 1u);
+      atomicAdd(&h[u.y >> cs], 1u);
+      atomicAdd(&h[u.z >> cs], 1u);
+      atomicAdd(&h[u.w >> cs], 1u);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - 4 * n4) atomicAdd(&h[m_first[4 * n4 + threadIdx.x] >> cs], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < RS_NC; i += blockDim.x)
+    if (h[i]) atomicAdd(&coarse[i], h[i]);
+}
+
+// One CTA of RS_THREADS. slot_of[b]: the bitmap slot of target block b (or
+// 0xFFFF); target[i] = slot << 16 | residual... split in two arrays.
+constexpr int RS_THREADS = 1024;
+__device__ __forceinline__ void rank_targets_block(const uint32_t* __restrict__ coarse, int nc,
+                                                   const uint32_t* __restrict__ chosen,
+                                                   const int* __restrict__ status, int k,
+                                                   uint16_t* __restrict__ slot_of, uint32_t* __restrict__ tgt_block,
+                                                   uint32_t* __restrict__ tgt_resid,
+                                                   uint32_t* __restrict__ slot_bits, int words_per_slot) {
+  constexpr int PER = RS_NC / RS_THREADS;  // 4 coarse blocks per thread
+  __shared__ uint32_t pre[RS_NC + 1];
+  __shared__ uint16_t so[RS_NC];
+  __shared__ uint32_t tb[KMAX];
+  __shared__ uint32_t warp_tot[RS_THREADS / 32];
+  __shared__ int n_slots;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  uint32_t c[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    c[q] = t * PER + q < nc ? coarse[t * PER + q] : 0u;
+    sum += c[q];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  if (t == 0) n_slots = 0;
+  __syncthreads();
+  uint32_t run = incl - sum;
+  for (int w = 0; w < wid; ++w) run += warp_tot[w];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    pre[t * PER + q] = run;
+    run += c[q];
+    so[t * PER + q] = 0xFFFFu;
+  }
+  if (t == RS_THREADS - 1) pre[RS_NC] = run;
+  __syncthreads();
+  const bool ok = *status == 0;
+  if (ok && t < k) {  // the block holding rank r: the last b with pre[b] <= r
+    const uint32_t r = chosen[t];
+    int lo = 0, hi = nc;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= r) lo = mid;
+      else hi = mid;
+    }
+    tb[t] = (uint32_t)lo;
+    tgt_block[t] = (uint32_t)lo;
+    tgt_resid[t] = r - pre[lo];
+  }
+  __syncthreads();
+  // distinct target blocks get consecutive slots: flag them, then rank the
+  // flags (thread t owns blocks t*PER .. t*PER+PER-1)
+  if (ok && t < k) so[tb[t]] = 0u;
+  __syncthreads();
+  uint32_t f = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) f += so[t * PER + q] == 0u;
+  uint32_t fi = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, fi, o);
+    if (lane >= o) fi += u;
+  }
+  __syncthreads();
+  if (lane == 31) warp_tot[wid] = fi;
+  __syncthreads();
+  uint32_t slot = fi - f;
+  for (int w = 0; w < wid; ++w) slot += warp_tot[w];
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+    if (so[t * PER + q] == 0u) so[t * PER + q] = (uint16_t)slot++;
+  if (t == RS_THREADS - 1) n_slots = (int)slot;
+  __syncthreads();
+  for (int i = t; i < RS_NC; i += RS_THREADS) slot_of[i] = so[i];
+  for (int i = t; i < n_slots * words_per_slot; i += RS_THREADS) slot_bits[i] = 0u;
+}
+
+__global__ void __launch_bounds__(1024) k_first_mark(const uint32_t* __restrict__ m_first,
+                                                    const unsigned long long* __restrict__ n_unique, int cs,
+                                                    const uint16_t* __restrict__ slot_of, int words_per_slot,
+                                                    uint32_t* __restrict__ slot_bits) {
+  __shared__ uint16_t so[RS_NC];
+  for (int i = threadIdx.x; i < RS_NC; i += blockDim.x) so[i] = slot_of[i];
+  __syncthreads();
+  const uint64_t n = *n_unique, n4 = n / 4;
+  const uint32_t mask = (1u << cs) - 1u;
+  auto mark = [&](uint32_t f) {
+    const uint32_t sl = so[f >> cs];
+    if (sl != 0xFFFFu) atomicOr(&slot_bits[sl * words_per_slot + ((f & mask) >> 5)], 1u << (f & 31));
+  };
+  const uint4* f4 = reinterpret_cast<const uint4*>(m_first);
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n4; s += 2 * T) {
+    const uint4 v = __ldg(f4 + s);
+    const uint4 u = s + T < n4 ? __ldg(f4 + s + T) : make_uint4(0u, 0u, 0u, 0u);
+    mark(v.x);
+    mark(v.y);
+    mark(v.z);
+    mark(v.w);
+    if (s + T < n4) {
+      mark(u.x);
+      mark(u.y);
+      mark(u.z);
+      mark(u.w);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - 4 * n4) mark(m_first[4 * n4 + threadIdx.x]);
+}
+
+// One warp per center.
+__global__ void k_rank_pick(const uint32_t* __restrict__ slot_bits, int words_per_slot, int cs,
+                            const uint16_t* __restrict__ slot_of, const uint32_t* __restrict__ tgt_block,
+                            const uint32_t* __restrict__ tgt_resid, const uint8_t* __restrict__ img,
+                            const int* __restrict__ status, int k, double* __restrict__ centers) {
+  const int i = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (i >= k || *status != 0) return;
+  const uint32_t b = tgt_block[i];
+  const uint32_t* bits = slot_bits + (size_t)slot_of[b] * words_per_slot;
+  uint32_t need = tgt_resid[i];  // set bits to skip before the one we want
+  for (int w0 = 0; w0 < words_per_slot; w0 += 32) {
+    const uint32_t word = w0 + lane < words_per_slot ? bits[w0 + lane] : 0u;
+    const uint32_t pc = __popc(word);
+    uint32_t incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (need < tot) {
+      const unsigned owner = __ballot_sync(0xffffffffu, incl > need && incl - pc <= need);
+      const int src = __ffs(owner) - 1;
+      if (lane == src) {
+        uint32_t wd = word;
+        for (uint32_t d = need - (incl - pc); d; --d) wd &= wd - 1u;
+        const uint64_t px = ((uint64_t)b << cs) + (uint64_t)(w0 + lane) * 32 + (__ffs(wd) - 1);
+        centers[3 * i + 0] = (double)img[3 * px];
+        centers[3 * i + 1] = (double)img[3 * px + 1];
+        centers[3 * i + 2] = (double)img[3 * px + 2];
+      }
+      return;
+    }
+    need -= tot;
   }
 }
 

@@ -35,6 +35,7 @@
 #define CQB_DIAG_FALLBACK 0
 #endif
 
+
 namespace cqb {
 
 namespace cg = cooperative_groups;
@@ -118,6 +119,7 @@ struct LoopParams {
   int res_cap;  // resident-sample kernels: samples per block reserved in dynamic shared memory
   int xw;
   int xrank;
+  unsigned long long xch_timeout_ns;  // peer wait limit of the in-kernel exchange
   unsigned long long* xbox[8];
   unsigned long long* xacc;
 };
@@ -220,6 +222,22 @@ __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restric
   init_centers_block(keys, *n_ptr, k, draws, ndraws, st);
 }
 
+// init_centers' K chosen ranks (above), then RS2 of the rank selection
+// (hist.cuh): one launch for both single-block steps.
+__global__ void __launch_bounds__(RS_THREADS) k_init_select(const unsigned long long* __restrict__ n_ptr, int k,
+                                                           const unsigned long long* __restrict__ draws,
+                                                           int ndraws, WsmState* st,
+                                                           const uint32_t* __restrict__ coarse, int nc,
+                                                           uint16_t* __restrict__ slot_of,
+                                                           uint32_t* __restrict__ tgt_block,
+                                                           uint32_t* __restrict__ tgt_resid,
+                                                           uint32_t* __restrict__ slot_bits, int words_per_slot) {
+  init_centers_block(nullptr, *n_ptr, k, draws, ndraws, st);
+  __syncthreads();
+  rank_targets_block(coarse, nc, st->chosen, &st->status, k, slot_of, tgt_block, tgt_resid, slot_bits,
+                     words_per_slot);
+}
+
 // Initial centers from the Morton-order samples: center i = the sample whose
 // first-occurrence rank is chosen[i] (kmeans.hpp:67-68). Each block sorts the
 // K chosen ranks in shared memory; every sample binary-searches its rank.
@@ -314,15 +332,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-
-// Sorted center rows staged in shared memory, truncated at R entries
-// (R = K for K <= 64); deeper scans continue in the global rows (L2).
-struct RowStage {
-  const double* d;   // row p starts at d + p * stride
-  const uint8_t* o;
-  int R;             // entries available per row (R == k: full rows)
-  int stride;
-};
 
 // Rows pa (and pb, or -1) of the center tables (kmeans.hpp:147-168):
 // d[p][t] = dist2(c_p, c_t) and the order row [p, others sorted by
@@ -667,6 +676,7 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
 // Assign variants: sort-means (WSM), exhaustive (KM), first k' of the row (FKM).
 enum class Assign { SortMeans, Naive, Fkm };
 constexpr int DBG_NO_F32 = 1 << 17;   // debug flag: FP64 scans only (A/B of the FP32 screening)
+constexpr int DBG_PART_HIST = 1 << 18;  // debug flag: large images through the partitioned histogram (part.cuh, A/B)
 
 // ---------------------------------------------------------------------------
 // FP32 screening of the sort-means scan (iterations >= 2), certified against
@@ -963,7 +973,7 @@ __device__ __noinline__ int scan_fp64(const LoopSmem& S, const double* __restric
 }
 
 template <Assign Mode, int PPT, int X, bool R>
-__device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowStage& RS, unsigned long long lo64,
+__device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
   const unsigned int pb = part_block<X>(S), pG = part_size<X>(S);
@@ -997,7 +1007,6 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, const RowSta
   const uint32_t* __restrict__ counts = L.counts;
   uint8_t* __restrict__ labels = L.labels;
   const int k = L.k;
-  (void)RS;
   uint32_t ev = 0;
   (void)W;
   (void)w;
@@ -1198,7 +1207,10 @@ constexpr int XB_SLOT = 5 * KMAX;
 constexpr size_t XB_LAB_OFF = 256 * 1024;
 constexpr size_t XB_BYTES = XB_LAB_OFF + (size_t(1) << 24);
 static_assert((XB_PAY + 2 * XMAX * XB_SLOT) * sizeof(unsigned long long) <= XB_LAB_OFF, "window layout");
-constexpr unsigned long long XCH_TIMEOUT_NS = 5000000000ull;  // a dead peer fails the call instead of hanging
+// A dead peer fails the call instead of hanging: LoopParams::xch_timeout_ns
+// (cqb_xch_set_timeout; default 5 s), and 4x that for the first exchange of
+// a launch, whose peers may still be starting their own launch.
+constexpr unsigned long long XCH_TIMEOUT_NS = 5000000000ull;
 
 __device__ __forceinline__ unsigned long long* xpay(unsigned long long* box, unsigned long long s, int src) {
   return box + XB_PAY + ((size_t)(s & 1) * XMAX + src) * XB_SLOT;
@@ -1209,7 +1221,8 @@ __device__ __forceinline__ void xch_signal(unsigned long long* box, int src, uns
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(box + XB_FLAG + 16 * src), "l"(s) : "memory");
 }
 // Block-wide: wait until all xw sources published exchange s into `box`.
-__device__ __forceinline__ void xch_wait(unsigned long long* box, int xw, unsigned long long s, int* status) {
+__device__ __forceinline__ void xch_wait(unsigned long long* box, int xw, unsigned long long s, int* status,
+                                         unsigned long long timeout_ns) {
   if (threadIdx.x < (unsigned)xw) {
     const unsigned long long* f = box + XB_FLAG + 16 * threadIdx.x;
     const unsigned long long t0 = globaltimer();
@@ -1218,7 +1231,7 @@ __device__ __forceinline__ void xch_wait(unsigned long long* box, int xw, unsign
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
       if (v >= s) break;
       if (*reinterpret_cast<volatile int*>(status) == ST_XCH_TIMEOUT) break;
-      if (globaltimer() - t0 > XCH_TIMEOUT_NS) {
+      if (globaltimer() - t0 > timeout_ns) {
         atomicExch(status, ST_XCH_TIMEOUT);
         break;
       }
@@ -1337,7 +1350,7 @@ __device__ void reseed_empty(LoopSmem& S, const LoopParams& L, cg::grid_group& g
           xch_signal(L.xbox[r], part, s);
         }
       unsigned long long* own = L.xbox[part];
-      xch_wait(own, L.xw, s, &st->status);
+      xch_wait(own, L.xw, s, &st->status, L.xch_timeout_ns);
       if (threadIdx.x == 0) {
         xd = -1.0;
         xi = 0xffffffffu;
@@ -1448,14 +1461,6 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
   if constexpr (X != 0) xs = __ldcg(L.xbox[part] + XB_SEQ);
   unsigned long long* tl = L.timeline;
   const bool rec = tl && blockIdx.x == 0 && tid == 0;
-  // Sorted rows are read straight from the global tables: the warps are
-  // Morton-coherent, so a row access is one L1 transaction shared by the warp
-  // (the grid barrier's gpu-scope fence invalidates L1 between iterations).
-  RowStage RS;
-  RS.R = k;
-  RS.stride = KMAX;
-  RS.d = st->sortedD;
-  RS.o = st->order;
   (void)dyn;
 
   int big = 0;  // a center outside (-256, 256): no FP32 screening in this launch (scan_f32's bound)
@@ -1549,7 +1554,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means<Mode, PPT, X, R>(S, L, RS, lo, hi, it == 1, evals, n_changed, n_deep);
+      assign_sort_means<Mode, PPT, X, R>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -1608,7 +1613,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
         if (tid == 0) xch_signal(L.xbox[pb], part, s);
       }
       unsigned long long* own = L.xbox[part];
-      xch_wait(own, L.xw, s, &st->status);
+      xch_wait(own, L.xw, s, &st->status, it == 1 ? 4 * L.xch_timeout_ns : L.xch_timeout_ns);
       for (int e = tid; e < 5 * KMAX; e += blockDim.x)
         if ((e & (KMAX - 1)) < k) {
           unsigned long long a = 0;
@@ -1776,7 +1781,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     BLOCK_STAMP(5);
     if (CQB_LOOP_BARRIER) {
       bar_target += gridDim.x;
-      const bool stop_here = blockIdx.x == 0 && S.stop_flag;
+      // block 0 also stops the whole grid, on the same iteration, when an
+      // exchange timed out (every block then leaves through this barrier)
+      const bool stop_here =
+          blockIdx.x == 0 && (S.stop_flag || (X != 0 && *reinterpret_cast<volatile int*>(&st->status) != ST_OK));
       if ((loop_barrier(S, &st->bar, bar_target, 1ull + (stop_here ? (1ull << 32) : 0ull)) >> 32) != 0) break;
     } else {
       grid.sync();
@@ -1873,7 +1881,7 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
     const unsigned int pG = X == 2 ? gridDim.x / (unsigned)L.xw : gridDim.x;
     if (tid == 0 && blockIdx.x % pG == 0)
       for (int r = 0; r < L.xw; ++r) xch_signal(L.xbox[r], part, s);
-    xch_wait(L.xbox[part], L.xw, s, &L.st->status);
+    xch_wait(L.xbox[part], L.xw, s, &L.st->status, L.xch_timeout_ns);
   }
   unsigned long long err = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;

@@ -155,13 +155,18 @@ def test_in_kernel_exchange_dead_peer_fails_instead_of_hanging():
     d_img = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
     torch.cuda.synchronize()
     ctx.check(ctx.lib.cqb_set_debug(ctx.h, 32768))
+    ctx.check(ctx.lib.cqb_xch_set_timeout(ctx.h, 1.0))
     t0 = time.time()
     q.enqueue(d_img.data_ptr(), img.shape[0] * img.shape[1], 16, api.Termination.convergent(1e-4, 100), 1)
     with pytest.raises(_native.CqbError) as e:
         q.fetch()
     assert e.value.code == _native.CQB_ERR_NCCL
-    assert time.time() - t0 < 60
+    assert time.time() - t0 < 30
     ctx.check(ctx.lib.cqb_set_debug(ctx.h, 0))
+    # the failed exchange is reset: the same windows are refused until set up again
+    with pytest.raises(_native.CqbInvalidArgument):
+        q.enqueue(d_img.data_ptr(), img.shape[0] * img.shape[1], 16, api.Termination.convergent(1e-4, 100), 1)
+    ctx.check(ctx.lib.cqb_xch_set_timeout(ctx.h, 5.0))
     single = api.quantize(img, 16, api.Termination.convergent(1e-4, 100), seed=1)
     q2 = PeerShardedQuantizer(ctx=ctx, emulate=2)  # fresh windows after a failed exchange
     q2.enqueue(d_img.data_ptr(), img.shape[0] * img.shape[1], 16, api.Termination.convergent(1e-4, 100), 1)
