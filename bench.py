@@ -561,7 +561,7 @@ def _loop_roofline(ms, P, n_unique, iters, k, peaks, evals, evals1, phases):
 def _ncu_traffic(stage, P):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
     ncu --set full capture (profiles/*/traffic.json), for the same image size."""
-    for rnd in ("r02", "r01"):
+    for rnd in ("r02", "r01"):  # newest first
         f = os.path.join(ROOT, "profiles", rnd, "traffic.json")
         try:
             with open(f) as fh:

@@ -192,6 +192,58 @@ int cqb_quantize_batch(cqb_ctx* ctx, int n_images, const uint8_t* const* d_rgb, 
 int cqb_quantize_runs(cqb_ctx* ctx, const uint8_t* rgb, uint64_t n_pixels, int k, const cqb_termination* term,
                       int n_runs, const uint64_t* seeds, int lanes, double* centers_out, cqb_report* reports);
 
+/* ---- generic weighted points (kmeans.hpp's span<const Vec3> API) --------
+ * points: n x 3 doubles (row-major), weights: n doubles, memberships: n
+ * int32, centers: k x 3 doubles, 1 <= k <= 1024 (k > 1024 ->
+ * CQB_ERR_UNSUPPORTED). Distances are FP64 without FMA and the tables are
+ * sorted by (distance, index) with self first, as the reference builds them;
+ * update_centers reproduces the reference's sequential per-cluster sums bit
+ * for bit (stable sort by membership, one thread per cluster). */
+
+/* Replaces init_centers(points, k, seed) (kmeans.hpp:53-70): the chosen point
+ * indices of the partial Fisher-Yates (center i = points[chosen_out[i]]).
+ * k < 1 or k > n -> CQB_ERR_INVALID_ARGUMENT (:54-56). */
+int cqb_init_centers(cqb_ctx* ctx, uint64_t n_points, int k, uint64_t seed, uint32_t* chosen_out);
+
+/* Replaces ClusterState::update_center_tables' full rebuild
+ * (kmeans.hpp:132-184): center_dists k x k (symmetric, zero diagonal),
+ * sorted_order k x k (row i = [i, others by (d, index)]). Outputs nullable. */
+int cqb_points_tables(cqb_ctx* ctx, const double* centers, int k, double* center_dists, int32_t* sorted_order);
+
+/* Replaces assign_sort_means(points, weights, palette, state, audit)
+ * (kmeans.hpp:201-239; mode 0) and assign_naive(points, weights, palette, m)
+ * (kmeans.hpp:83-106; mode 1, exhaustive, lowest index on ties).
+ * memberships: in = previous (mode 0), out = new. With center_dists +
+ * sorted_order (a ClusterState's tables) the scan reads them; with NULL the
+ * tables of `centers` are built first. weighted_sse: fixed-order tree sum of
+ * w * min distance; dist_evals: the reference's count. skip_rank_out /
+ * prev_dist_out (nullable, mode 0): per point the row position where the scan
+ * stopped early (-1 if it ran to the end) and its previous-center distance,
+ * the arguments of the reference's SkipAudit callback. */
+int cqb_points_assign(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n, const double* centers,
+                      int k, const double* center_dists, const int32_t* sorted_order, int mode,
+                      int32_t* memberships, double* weighted_sse, uint64_t* dist_evals, int32_t* skip_rank_out,
+                      double* prev_dist_out);
+
+/* Replaces update_centers(points, weights, memberships, prev)
+ * (kmeans.hpp:245-296), the empty-cluster reseed included. */
+int cqb_points_update(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n,
+                      const int32_t* memberships, const double* prev, int k, double* next_out);
+
+/* Replaces weighted_sse(points, weights, palette, memberships) (kmeans.hpp:306-317). */
+int cqb_points_sse(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n, const double* centers,
+                   int k, const int32_t* memberships, double* sse_out);
+
+/* Replaces run_wsm_points(points, weights, k, term, seed, trajectory)
+ * (kmeans.hpp:379-390); also the device path of run_wsm for histograms whose
+ * colors or weights the integer histogram path cannot take. trajectory:
+ * traj_cap x k x 3 doubles (the palette after every update), nullable;
+ * memberships_out: n int32, nullable. */
+int cqb_run_wsm_points(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n, int k,
+                       const cqb_termination* term, uint64_t seed, double* centers_out, double* sse_history,
+                       int hist_cap, double* trajectory, int traj_cap, int32_t* memberships_out,
+                       cqb_report* report);
+
 /* ---- post-processing ---------------------------------------------------
  * Replaces map_pixels(img, palette) (image_ops.hpp:18-51): nearest ROUNDED
  * palette entry, lowest index on ties. centers: k x 3 doubles, k in [1,256];

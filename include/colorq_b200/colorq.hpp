@@ -23,7 +23,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
+#include <functional>
 #include <memory>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -244,23 +247,203 @@ inline ColorHistogram build_histogram(const RgbImage& img) {
   return h;
 }
 
-// kmeans.hpp:394-404. The device path consumes the integer counts (exact
-// u64 cluster sums); a histogram from build_histogram always carries them.
+// ---------------------------------------------------------------- points
+// kmeans.hpp's span<const Vec3> API over the device point-set kernels
+// (cqb_init_centers / cqb_points_* / cqb_run_wsm_points), k <= 1024.
+using Memberships = std::vector<std::int32_t>;
+
+struct AssignResult {
+  double weighted_sse = 0.0;
+  std::uint64_t dist_evals = 0;
+};
+
+// kmeans.hpp:194-196: called for every point whose sorted scan stopped early.
+using SkipAudit =
+    std::function<void(std::size_t point, int prev_center, int first_skipped_rank, double prev_dist)>;
+
+namespace b200 {
+inline const double* flat(std::span<const Vec3> v) { return v.empty() ? nullptr : v.front().data(); }
+inline std::vector<double> flat(const Palette& p) {
+  std::vector<double> c(3 * p.size());
+  for (std::size_t i = 0; i < p.size(); ++i)
+    for (int d = 0; d < 3; ++d) c[3 * i + std::size_t(d)] = p[i][std::size_t(d)];
+  return c;
+}
+}  // namespace b200
+
+// kmeans.hpp:53-74
+inline Palette init_centers(std::span<const Vec3> points, int k, std::uint64_t seed) {
+  if (k < 1) throw std::invalid_argument("init_centers: k must be >= 1");
+  if (std::size_t(k) > points.size())
+    throw std::invalid_argument("init_centers: k exceeds the number of candidate points");
+  std::vector<std::uint32_t> chosen(std::size_t(k), 0u);
+  b200::check(cqb_init_centers(b200::context(), points.size(), k, seed, chosen.data()));
+  Palette p;
+  for (const std::uint32_t i : chosen) p.centers.push_back(points[i]);
+  return p;
+}
+inline Palette init_centers(const ColorHistogram& hist, int k, std::uint64_t seed) {
+  return init_centers(std::span<const Vec3>(hist.colors), k, seed);
+}
+
+// kmeans.hpp:86-113 (exhaustive; lowest index on ties)
+inline AssignResult assign_naive(std::span<const Vec3> points, std::span<const double> weights,
+                                 const Palette& palette, Memberships& out) {
+  if (palette.empty()) throw std::invalid_argument("assign_naive: empty palette");
+  out.assign(points.size(), 0);
+  const std::vector<double> c = b200::flat(palette);
+  AssignResult r;
+  b200::check(cqb_points_assign(b200::context(), b200::flat(points), weights.data(), points.size(), c.data(),
+                                int(palette.size()), nullptr, nullptr, 1, out.data(), &r.weighted_sse,
+                                &r.dist_evals, nullptr, nullptr));
+  return r;
+}
+inline Memberships assign_naive(const ColorHistogram& hist, const Palette& palette) {
+  Memberships m;
+  assign_naive(hist.colors, hist.weights, palette, m);
+  return m;
+}
+
+// kmeans.hpp:118-189: previous memberships + the K x K center tables.
+struct ClusterState {
+  Memberships memberships;
+  std::vector<double> center_dists;        // k*k, symmetric, zero diagonal
+  std::vector<std::int32_t> sorted_order;  // k*k, row i = [i, others by (d, index)]
+  int k = 0;
+
+  double d(int i, int j) const { return center_dists[std::size_t(i) * std::size_t(k) + std::size_t(j)]; }
+  const std::int32_t* order_row(int i) const { return &sorted_order[std::size_t(i) * std::size_t(k)]; }
+
+  // Rebuilt on the device each call (a full rebuild equals the reference's
+  // incremental one bit for bit); pair_evals counts the pairs the reference
+  // recomputes: all of them first, then those with a moved center.
+  void update_center_tables(const Palette& palette, std::uint64_t* pair_evals = nullptr) {
+    const int nk = int(palette.size());
+    const bool incremental = nk == k && prev_centers_.size() == std::size_t(nk);
+    std::uint64_t still = 0;
+    if (incremental)
+      for (int i = 0; i < nk; ++i) still += palette[std::size_t(i)] == prev_centers_[std::size_t(i)];
+    k = nk;
+    center_dists.resize(std::size_t(k) * std::size_t(k));
+    sorted_order.resize(std::size_t(k) * std::size_t(k));
+    const std::vector<double> c = b200::flat(palette);
+    b200::check(cqb_points_tables(b200::context(), c.data(), k, center_dists.data(), sorted_order.data()));
+    if (pair_evals)
+      *pair_evals += std::uint64_t(k) * std::uint64_t(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0);
+    prev_centers_ = palette.centers;
+  }
+
+ private:
+  std::vector<Vec3> prev_centers_;
+};
+
+// kmeans.hpp:201-239
+inline AssignResult assign_sort_means(std::span<const Vec3> points, std::span<const double> weights,
+                                      const Palette& palette, ClusterState& state,
+                                      const SkipAudit* audit = nullptr) {
+  const int k = int(palette.size());
+  if (state.k != k || state.memberships.size() != points.size())
+    throw std::invalid_argument("assign_sort_means: state does not match inputs");
+  const std::vector<double> c = b200::flat(palette);
+  std::vector<std::int32_t> skip(audit ? points.size() : 0);
+  std::vector<double> prev(audit ? points.size() : 0);
+  const std::vector<std::int32_t> before = audit ? state.memberships : std::vector<std::int32_t>{};
+  AssignResult r;
+  b200::check(cqb_points_assign(b200::context(), b200::flat(points), weights.data(), points.size(), c.data(), k,
+                                state.center_dists.data(), state.sorted_order.data(), 0, state.memberships.data(),
+                                &r.weighted_sse, &r.dist_evals, audit ? skip.data() : nullptr,
+                                audit ? prev.data() : nullptr));
+  if (audit)
+    for (std::size_t i = 0; i < points.size(); ++i)
+      if (skip[i] >= 0) (*audit)(i, before[i], skip[i], prev[i]);
+  return r;
+}
+
+// kmeans.hpp:245-302
+inline Palette update_centers(std::span<const Vec3> points, std::span<const double> weights,
+                              const Memberships& memberships, const Palette& prev) {
+  const std::vector<double> c = b200::flat(prev);
+  std::vector<double> next(c.size());
+  b200::check(cqb_points_update(b200::context(), b200::flat(points), weights.data(), points.size(),
+                                memberships.data(), c.data(), int(prev.size()), next.data()));
+  return b200::palette_from(next.data(), int(prev.size()));
+}
+inline Palette update_centers(const ColorHistogram& hist, const Memberships& memberships, const Palette& prev) {
+  return update_centers(std::span<const Vec3>(hist.colors), std::span<const double>(hist.weights), memberships, prev);
+}
+
+// kmeans.hpp:306-317
+inline double weighted_sse(std::span<const Vec3> points, std::span<const double> weights, const Palette& palette,
+                           const Memberships& memberships) {
+  const std::vector<double> c = b200::flat(palette);
+  double out = 0.0;
+  b200::check(cqb_points_sse(b200::context(), b200::flat(points), weights.data(), points.size(), c.data(),
+                             int(palette.size()), memberships.data(), &out));
+  return out;
+}
+inline double weighted_sse(const ColorHistogram& hist, const Palette& palette, const Memberships& memberships) {
+  return weighted_sse(hist.colors, hist.weights, palette, memberships);
+}
+
+namespace b200 {
+inline KmRunResult run_points(std::span<const Vec3> points, std::span<const double> weights, int k,
+                              const Termination& term, std::uint64_t seed, std::vector<Palette>* trajectory) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (k < 1) throw std::invalid_argument("init_centers: k must be >= 1");
+  if (std::size_t(k) > points.size())
+    throw std::invalid_argument("init_centers: k exceeds the number of candidate points");
+  const cqb_termination t = native(term);
+  const int cap = budget(term);
+  std::vector<double> centers(3 * std::size_t(k)), hist_out(static_cast<std::size_t>(cap));
+  std::vector<double> traj(trajectory ? std::size_t(cap) * 3 * std::size_t(k) : 0);
+  cqb_report rep{};
+  check(cqb_run_wsm_points(context(), flat(points), weights.data(), points.size(), k, &t, seed, centers.data(),
+                           hist_out.data(), cap, trajectory ? traj.data() : nullptr, trajectory ? cap : 0, nullptr,
+                           &rep));
+  KmRunResult out;
+  out.palette = palette_from(centers.data(), k);
+  out.report.method = term.mode == Termination::Mode::Convergent ? "wsm-c" : "wsm";
+  out.report.k = k;
+  out.report.seed = seed;
+  out.report.iterations = rep.iterations;
+  out.report.sse = rep.sse;
+  out.report.dist_evals = rep.dist_evals;
+  out.report.sse_history.assign(hist_out.begin(), hist_out.begin() + rep.iterations);
+  if (trajectory)
+    for (int i = 0; i < rep.iterations; ++i) trajectory->push_back(palette_from(traj.data() + 3 * k * i, k));
+  out.report.elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return out;
+}
+}  // namespace b200
+
+// kmeans.hpp:379-390
+inline KmRunResult run_wsm_points(std::span<const Vec3> points, std::span<const double> weights, int k,
+                                  const Termination& term, std::uint64_t seed,
+                                  std::vector<Palette>* trajectory = nullptr) {
+  return b200::run_points(points, weights, k, term, seed, trajectory);
+}
+
+// kmeans.hpp:394-404. A histogram from build_histogram (8-bit colors, counts,
+// weights = count * (1/total)) takes the integer path: exact u64 cluster sums
+// in one persistent kernel, k <= 256. Any other histogram (real-valued
+// colors or weights, k > 256) runs the point-set path over colors + weights.
 inline KmRunResult run_wsm(const ColorHistogram& hist, int k, const Termination& term, std::uint64_t seed,
                            std::vector<Palette>* trajectory = nullptr) {
   const auto t0 = std::chrono::steady_clock::now();
   if (k < 1) throw std::invalid_argument("init_centers: k must be >= 1");
   if (std::size_t(k) > hist.size())
     throw std::invalid_argument("init_centers: k exceeds the number of candidate points");
-  if (hist.counts.size() != hist.size()) throw std::invalid_argument("run_wsm: histogram has no counts");
-  std::vector<std::uint32_t> keys(hist.size());
-  for (std::size_t i = 0; i < hist.size(); ++i) {
+  bool integer_path = k <= CQB_MAX_K && hist.counts.size() == hist.size() && hist.weights.size() == hist.size() &&
+                      hist.total_pixels > 0;
+  std::vector<std::uint32_t> keys(integer_path ? hist.size() : 0);
+  const double inv_total = integer_path ? 1.0 / double(hist.total_pixels) : 0.0;
+  for (std::size_t i = 0; integer_path && i < hist.size(); ++i) {
     const Vec3& c = hist.colors[i];
-    for (double v : c)
-      if (!(v >= 0 && v <= 255 && v == std::floor(v)))
-        throw std::invalid_argument("run_wsm: histogram colors must be 8-bit integers");
-    keys[i] = pack_rgb(RgbColor{std::uint8_t(c[0]), std::uint8_t(c[1]), std::uint8_t(c[2])});
+    for (double v : c) integer_path &= v >= 0 && v <= 255 && v == std::floor(v);
+    integer_path &= hist.weights[i] == double(hist.counts[i]) * inv_total;  // histogram.hpp:94-97
+    if (integer_path) keys[i] = pack_rgb(RgbColor{std::uint8_t(c[0]), std::uint8_t(c[1]), std::uint8_t(c[2])});
   }
+  if (!integer_path) return b200::run_points(hist.colors, hist.weights, k, term, seed, trajectory);
   const cqb_termination t = b200::native(term);
   const int cap = b200::budget(term);
   std::vector<double> centers(3 * std::size_t(k)), hist_out(static_cast<std::size_t>(cap));

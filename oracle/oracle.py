@@ -117,6 +117,14 @@ class Oracle:
             f("quantize_many").argtypes = [C.POINTER(_u8p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_double, C.c_int, C.c_uint64, C.c_int, _f64p, _i32p]
             f("quantize_many").restype = C.c_double
+            f("init_centers_points").argtypes = [_f64p, C.c_uint64, C.c_int, C.c_uint64, _f64p]
+            f("points_assign").argtypes = [_f64p, _f64p, C.c_uint64, _f64p, C.c_int, C.c_int, _i32p, _f64p, _u64p,
+                                           _u64p]
+            f("points_update").argtypes = [_f64p, _f64p, C.c_uint64, _i32p, _f64p, C.c_int, _f64p]
+            f("points_sse").argtypes = [_f64p, _f64p, C.c_uint64, _f64p, C.c_int, _i32p]
+            f("points_sse").restype = C.c_double
+            f("run_wsm_points").argtypes = [_f64p, _f64p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                            C.c_uint64, _f64p, _f64p, _u64p, _f64p, C.c_int]
             f("write_ppm").argtypes = [_u8p, C.c_int, C.c_int, _u8p, C.c_int64]
             f("write_ppm").restype = C.c_int64
             f("read_ppm").argtypes = [_u8p, C.c_int64, _u8p, C.c_int64, _i32p, _i32p]
@@ -225,6 +233,56 @@ class Oracle:
             self._f("update_centers")(_p(keys, _u32p), _p(counts, _u32p), keys.shape[0], total, _p(lab, _i32p),
                                       _p(P, _f64p), k, _p(out, _f64p))
         return out.reshape(k, 3)
+
+    # -- the point-set API (reference only) --------------------------------
+    def init_centers_points(self, X, k: int, seed: int) -> np.ndarray:
+        X = np.ascontiguousarray(X, np.float64)
+        C_out = np.zeros(3 * k)
+        if self._f("init_centers_points")(_p(X, _f64p), X.shape[0], k, seed, _p(C_out, _f64p)) != 0:
+            raise ValueError("init_centers: invalid k")
+        return C_out.reshape(k, 3)
+
+    def points_assign(self, X, W, centers, memberships, naive: bool = False):
+        X = np.ascontiguousarray(X, np.float64)
+        W = np.ascontiguousarray(W, np.float64)
+        Cc = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        m = np.ascontiguousarray(memberships, np.int32).copy()
+        sse, ev, au = np.zeros(1), np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        rc = self._f("points_assign")(_p(X, _f64p), _p(W, _f64p), X.shape[0], _p(Cc, _f64p), Cc.shape[0] // 3,
+                                      int(naive), _p(m, _i32p), _p(sse, _f64p), _p(ev, _u64p), _p(au, _u64p))
+        if rc != 0:
+            raise ValueError("assign: state does not match inputs")
+        return m, float(sse[0]), int(ev[0]), int(au[0])
+
+    def points_update(self, X, W, memberships, prev):
+        X = np.ascontiguousarray(X, np.float64)
+        W = np.ascontiguousarray(W, np.float64)
+        m = np.ascontiguousarray(memberships, np.int32)
+        P = np.ascontiguousarray(prev, np.float64).reshape(-1)
+        out = np.zeros_like(P)
+        self._f("points_update")(_p(X, _f64p), _p(W, _f64p), X.shape[0], _p(m, _i32p), _p(P, _f64p), P.shape[0] // 3,
+                                 _p(out, _f64p))
+        return out.reshape(-1, 3)
+
+    def points_sse(self, X, W, centers, memberships) -> float:
+        X = np.ascontiguousarray(X, np.float64)
+        W = np.ascontiguousarray(W, np.float64)
+        Cc = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        m = np.ascontiguousarray(memberships, np.int32)
+        return float(self._f("points_sse")(_p(X, _f64p), _p(W, _f64p), X.shape[0], _p(Cc, _f64p), Cc.shape[0] // 3,
+                                           _p(m, _i32p)))
+
+    def run_wsm_points(self, X, W, k: int, mode: int = 1, max_iters: int = 10, eps: float = 1e-4, cap: int = 100,
+                       seed: int = 1) -> WsmResult:
+        X = np.ascontiguousarray(X, np.float64)
+        W = np.ascontiguousarray(W, np.float64)
+        hcap = max(cap if mode == 1 else max_iters, 1)
+        C_out, sse, ev, hist = np.zeros(3 * k), np.zeros(1), np.zeros(1, np.uint64), np.full(hcap, np.nan)
+        it = self._f("run_wsm_points")(_p(X, _f64p), _p(W, _f64p), X.shape[0], k, mode, max_iters, eps, cap, seed,
+                                       _p(C_out, _f64p), _p(sse, _f64p), _p(ev, _u64p), _p(hist, _f64p), hcap)
+        if it < 0:
+            raise ValueError("run_wsm_points: invalid argument")
+        return WsmResult(C_out.reshape(k, 3), it, float(sse[0]), int(ev[0]), hist[:it].copy())
 
     # -- post-processing ---------------------------------------------------
     def map_pixels(self, rgb: np.ndarray, centers: np.ndarray):

@@ -309,6 +309,85 @@ int ref_run_bench(const char* config_text, const char* prefix) {
 
 // write_ppm bytes of a w x h image; returns the byte count (or the needed
 // capacity when cap is too small).
+// ---- the span<const Vec3> point-set API (kmeans.hpp:53-74, 201-317, 379-390)
+namespace {
+std::vector<Vec3> make_points(const double* X, std::uint64_t n) {
+  std::vector<Vec3> v(n);
+  for (std::uint64_t i = 0; i < n; ++i) v[i] = Vec3{X[3 * i], X[3 * i + 1], X[3 * i + 2]};
+  return v;
+}
+}  // namespace
+
+int ref_init_centers_points(const double* X, std::uint64_t n, int k, std::uint64_t seed, double* C) {
+  try {
+    store_palette(init_centers(std::span<const Vec3>(make_points(X, n)), k, seed), C);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// One ClusterState step (update_center_tables + assign_sort_means, or
+// assign_naive with naive = 1) from the given memberships.
+int ref_points_assign(const double* X, const double* W, std::uint64_t n, const double* C, int k, int naive,
+                      std::int32_t* m, double* sse, std::uint64_t* evals, std::uint64_t* audited) {
+  try {
+    const std::vector<Vec3> pts = make_points(X, n);
+    const Palette pal = make_palette(C, k);
+    AssignResult ar;
+    if (naive) {
+      Memberships mm;
+      ar = assign_naive(pts, std::span<const double>(W, n), pal, mm);
+      std::copy(mm.begin(), mm.end(), m);
+    } else {
+      ClusterState st;
+      st.memberships.assign(m, m + n);
+      st.update_center_tables(pal);
+      std::uint64_t cnt = 0;
+      const SkipAudit audit = [&](std::size_t, int, int, double) { ++cnt; };
+      ar = assign_sort_means(pts, std::span<const double>(W, n), pal, st, &audit);
+      std::copy(st.memberships.begin(), st.memberships.end(), m);
+      if (audited) *audited = cnt;
+    }
+    *sse = ar.weighted_sse;
+    *evals = ar.dist_evals;
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+int ref_points_update(const double* X, const double* W, std::uint64_t n, const std::int32_t* m, const double* prev,
+                      int k, double* out) {
+  const std::vector<Vec3> pts = make_points(X, n);
+  const Memberships mm(m, m + n);
+  store_palette(update_centers(pts, std::span<const double>(W, n), mm, make_palette(prev, k)), out);
+  return 0;
+}
+
+double ref_points_sse(const double* X, const double* W, std::uint64_t n, const double* C, int k,
+                      const std::int32_t* m) {
+  const std::vector<Vec3> pts = make_points(X, n);
+  return weighted_sse(pts, std::span<const double>(W, n), make_palette(C, k), Memberships(m, m + n));
+}
+
+int ref_run_wsm_points(const double* X, const double* W, std::uint64_t n, int k, int mode, int max_iters,
+                       double eps, int cap, std::uint64_t seed, double* C_out, double* sse, std::uint64_t* evals,
+                       double* hist, int hist_cap) {
+  try {
+    const std::vector<Vec3> pts = make_points(X, n);
+    const KmRunResult r =
+        run_wsm_points(pts, std::span<const double>(W, n), k, make_term(mode, max_iters, eps, cap), seed);
+    store_palette(r.palette, C_out);
+    *sse = r.report.sse;
+    *evals = r.report.dist_evals;
+    for (int i = 0; i < std::min(hist_cap, r.report.iterations); ++i) hist[i] = r.report.sse_history[std::size_t(i)];
+    return r.report.iterations;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 std::int64_t ref_write_ppm(const std::uint8_t* rgb, int w, int h, std::uint8_t* out, std::int64_t cap) {
   const std::vector<unsigned char> b = write_ppm(make_image(rgb, std::uint64_t(w), std::uint64_t(h)));
   if (std::int64_t(b.size()) <= cap) std::memcpy(out, b.data(), b.size());

@@ -31,7 +31,8 @@ EXPORTS = (
     "cqb_map_pixels", "cqb_mse", "cqb_set_profiling", "cqb_stage_times",
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
     "cqb_shard_reseed_candidate", "cqb_set_debug", "cqb_xch_window", "cqb_xch_open", "cqb_xch_emulate",
-    "cqb_quantize_sharded", "cqb_xch_set_timeout",
+    "cqb_quantize_sharded", "cqb_xch_set_timeout", "cqb_init_centers", "cqb_points_tables", "cqb_points_assign",
+    "cqb_points_update", "cqb_points_sse", "cqb_run_wsm_points",
 )
 IPC_HANDLE_BYTES = 64  # CQB_IPC_HANDLE_BYTES (cudaIpcMemHandle_t)
 # cqb_stage_times intervals: memsets | K1 | K2b | init + bitmap scan + rank (+ gather) | loop | map tables+unique | map pixels
@@ -125,6 +126,16 @@ def load_library() -> C.CDLL:
         L.cqb_xch_window.argtypes = [_vp, C.c_int, C.c_int, _vp]
         L.cqb_xch_open.argtypes = [_vp, _vp]
         L.cqb_xch_emulate.argtypes = [_vp, C.c_int]
+        _i32p = C.POINTER(C.c_int32)
+        if hasattr(L, "cqb_run_wsm_points"):
+            L.cqb_init_centers.argtypes = [_vp, C.c_uint64, C.c_int, C.c_uint64, _u32p]
+            L.cqb_points_tables.argtypes = [_vp, _f64p, C.c_int, _f64p, _i32p]
+            L.cqb_points_assign.argtypes = [_vp, _f64p, _f64p, C.c_uint64, _f64p, C.c_int, _f64p, _i32p, C.c_int,
+                                            _i32p, _f64p, _u64p, _i32p, _f64p]
+            L.cqb_points_update.argtypes = [_vp, _f64p, _f64p, C.c_uint64, _i32p, _f64p, C.c_int, _f64p]
+            L.cqb_points_sse.argtypes = [_vp, _f64p, _f64p, C.c_uint64, _f64p, C.c_int, _i32p, _f64p]
+            L.cqb_run_wsm_points.argtypes = [_vp, _f64p, _f64p, C.c_uint64, C.c_int, _T, C.c_uint64, _f64p, _f64p,
+                                             C.c_int, _f64p, C.c_int, _i32p, _R]
         if hasattr(L, "cqb_xch_set_timeout"):
             L.cqb_xch_set_timeout.argtypes = [_vp, C.c_double]
         L.cqb_quantize_sharded.argtypes = [_vp, _vp, C.c_uint64, C.c_int, _T, C.c_uint64, _vp, _vp, _u64p]

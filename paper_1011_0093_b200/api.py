@@ -296,6 +296,88 @@ def quantize_batch_device(images, k: int, term: Termination | None = None, seed:
             [_report_from(reps[i], name, np.zeros(0)) for i in range(n)])
 
 
+# --------------------------------------------------------------------------- point sets
+# kmeans.hpp's span<const Vec3> API (init_centers, assign_sort_means /
+# assign_naive, update_centers, weighted_sse, run_wsm_points) on the device
+# point-set kernels (points.cuh), k <= 1024.
+_i32p = C.POINTER(C.c_int32)
+
+
+def _pts(points, weights=None):
+    X = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    W = None if weights is None else np.ascontiguousarray(weights, np.float64).reshape(-1)
+    if W is not None and W.shape[0] != X.shape[0]:
+        raise CqbInvalidArgument(N.CQB_ERR_INVALID_ARGUMENT, "points and weights differ in length")
+    return X, W
+
+
+def init_centers(points, k: int, seed: int, device: int = 0) -> np.ndarray:
+    """kmeans.hpp:53-74: k distinct points by the seeded partial Fisher-Yates."""
+    X, _ = _pts(points)
+    ctx = context(device)
+    chosen = np.zeros(max(k, 1), np.uint32)
+    ctx.check(ctx.lib.cqb_init_centers(ctx.h, X.shape[0], k, seed, _p(chosen, _u32p)))
+    return X[chosen[:k]].copy()
+
+
+def assign_points(points, weights, centers, memberships=None, naive: bool = False, device: int = 0):
+    """assign_sort_means from `memberships` (kmeans.hpp:201-239), or
+    assign_naive (:83-106). Returns (memberships, weighted_sse, dist_evals)."""
+    X, W = _pts(points, weights)
+    Cc = np.ascontiguousarray(centers, np.float64).reshape(-1)
+    m = np.zeros(X.shape[0], np.int32) if memberships is None else np.ascontiguousarray(memberships, np.int32).copy()
+    sse, ev = np.zeros(1), np.zeros(1, np.uint64)
+    ctx = context(device)
+    ctx.check(ctx.lib.cqb_points_assign(ctx.h, _p(X, _f64p), _p(W, _f64p), X.shape[0], _p(Cc, _f64p), Cc.size // 3,
+                                        None, None, int(naive), _p(m, _i32p), _p(sse, _f64p), _p(ev, _u64p), None,
+                                        None))
+    return m, float(sse[0]), int(ev[0])
+
+
+def update_centers(points, weights, memberships, prev, device: int = 0) -> np.ndarray:
+    """kmeans.hpp:245-302 (empty clusters re-seeded)."""
+    X, W = _pts(points, weights)
+    m = np.ascontiguousarray(memberships, np.int32)
+    P = np.ascontiguousarray(prev, np.float64).reshape(-1)
+    out = np.zeros_like(P)
+    ctx = context(device)
+    ctx.check(ctx.lib.cqb_points_update(ctx.h, _p(X, _f64p), _p(W, _f64p), X.shape[0], _p(m, _i32p), _p(P, _f64p),
+                                        P.size // 3, _p(out, _f64p)))
+    return out.reshape(-1, 3)
+
+
+def weighted_sse(points, weights, centers, memberships, device: int = 0) -> float:
+    """kmeans.hpp:306-317."""
+    X, W = _pts(points, weights)
+    Cc = np.ascontiguousarray(centers, np.float64).reshape(-1)
+    m = np.ascontiguousarray(memberships, np.int32)
+    out = np.zeros(1)
+    ctx = context(device)
+    ctx.check(ctx.lib.cqb_points_sse(ctx.h, _p(X, _f64p), _p(W, _f64p), X.shape[0], _p(Cc, _f64p), Cc.size // 3,
+                                     _p(m, _i32p), _p(out, _f64p)))
+    return float(out[0])
+
+
+def run_wsm_points(points, weights, k: int, term: Termination | None = None, seed: int = 1, trajectory: bool = False,
+                   device: int = 0) -> KmRunResult:
+    """kmeans.hpp:379-390: Weighted Sort-Means over an arbitrary weighted point set."""
+    X, W = _pts(points, weights)
+    term = term or Termination.convergent()
+    cap = term.iteration_budget
+    centers = np.zeros(3 * max(k, 1))
+    hist = np.zeros(cap)
+    traj = np.zeros((cap, max(k, 1), 3)) if trajectory else None
+    m = np.zeros(X.shape[0], np.int32)
+    rep = N.Report()
+    t = term.native()
+    ctx = context(device)
+    ctx.check(ctx.lib.cqb_run_wsm_points(ctx.h, _p(X, _f64p), _p(W, _f64p), X.shape[0], k, C.byref(t), seed,
+                                         _p(centers, _f64p), _p(hist, _f64p), cap, _p(traj, _f64p),
+                                         cap if trajectory else 0, _p(m, _i32p), C.byref(rep)))
+    r = _report_from(rep, "wsm-c" if term.mode == "convergent" else "wsm", hist)
+    return KmRunResult(centers.reshape(-1, 3)[:k].copy(), r, traj[: rep.iterations].copy() if trajectory else None, m)
+
+
 def generate_palette(img: np.ndarray, mp: MethodParams, k: int, seed: int, device: int = 0) -> QuantizeOutcome:
     """methods.hpp:107-197 — the WSM / WSM-C branch only (the comparator
     quantizers are outside this framework's scope)."""

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,7 @@
 #include "wsm.cuh"
 #include "prep.cuh"
 #include "part.cuh"
+#include "points.cuh"
 
 using namespace cqb;
 
@@ -97,6 +99,32 @@ struct cqb_ctx {
   uint32_t* rs_tgt = nullptr;          // [2 * KMAX] target block, residual
   uint32_t* rs_slot_bits = nullptr;
   size_t cap_slot_bits = 0;
+  // generic weighted points (points.cuh)
+  struct Points {
+    size_t cap_n = 0, cap_tiles = 0;
+    int cap_k = 0;
+    double* X = nullptr;            // 3n
+    double* W = nullptr;            // n
+    int32_t* m = nullptr;           // n memberships
+    uint32_t* perm = nullptr;       // n, stable sort by membership
+    int32_t* skip = nullptr;        // n audit: first skipped rank or -1
+    double* prevd = nullptr;        // n audit: previous distance
+    uint32_t* tcnt = nullptr;       // tiles x k
+    uint32_t* toff = nullptr;
+    double* C = nullptr;            // 3k current centers
+    double* next = nullptr;         // 3k
+    double* taken = nullptr;        // 3k
+    double* dists = nullptr;        // k x k
+    int32_t* order = nullptr;       // k x k
+    double* sortedD = nullptr;      // k x k
+    uint32_t* start = nullptr;      // k + 1
+    int* empty = nullptr;           // k
+    double* part = nullptr;         // block partials
+    unsigned long long* cand_i = nullptr;
+    double* scal = nullptr;         // [0] sse
+    unsigned long long* evals = nullptr;
+    uint32_t* chosen = nullptr;     // k
+  } pts;
   double* d_weights = nullptr;
   unsigned long long* d_n = nullptr;  // N'
 
@@ -848,7 +876,11 @@ int cqb_destroy(cqb_ctx* ctx) {
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
                  ctx->d_draws, ctx->d_entries, ctx->part_cnt, ctx->part_off, ctx->part_start, ctx->part_tiles,
-                 ctx->first_tab, ctx->rs_coarse, ctx->rs_slot_of, ctx->rs_tgt, ctx->rs_slot_bits};
+                 ctx->first_tab, ctx->rs_coarse, ctx->rs_slot_of, ctx->rs_tgt, ctx->rs_slot_bits,
+                 ctx->pts.X, ctx->pts.W, ctx->pts.m, ctx->pts.perm, ctx->pts.skip, ctx->pts.prevd,
+                 ctx->pts.tcnt, ctx->pts.toff, ctx->pts.C, ctx->pts.next, ctx->pts.taken, ctx->pts.dists,
+                 ctx->pts.order, ctx->pts.sortedD, ctx->pts.start, ctx->pts.empty, ctx->pts.part,
+                 ctx->pts.cand_i, ctx->pts.scal, ctx->pts.evals, ctx->pts.chosen};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_draws) cudaFreeHost(ctx->h_draws);
@@ -1352,6 +1384,335 @@ int cqb_mse(cqb_ctx* ctx, const uint8_t* a, const uint8_t* b, uint64_t n_pixels,
   *out = (double)ctx->h_scalar[0] / (double)n_pixels;
   return CQB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Generic weighted points (points.cuh): kmeans.hpp's span<const Vec3> API.
+namespace {
+constexpr int PTS_BLOCKS = 296;  // grid of the point kernels (block partials)
+
+int pts_reserve(cqb_ctx* ctx, uint64_t n, int k) {
+  auto& q = ctx->pts;
+  if (n > q.cap_n) {
+    const size_t c = (size_t)n + 64;
+    TRY(grow(ctx, &q.X, 3 * c));
+    TRY(grow(ctx, &q.W, c));
+    TRY(grow(ctx, &q.m, c));
+    TRY(grow(ctx, &q.perm, c));
+    TRY(grow(ctx, &q.skip, c));
+    TRY(grow(ctx, &q.prevd, c));
+    q.cap_n = c;
+  }
+  const size_t tiles = (size_t)(n + PTS_TILE - 1) / PTS_TILE;
+  if (k > q.cap_k || tiles * (size_t)k > q.cap_tiles) {
+    const int kk = std::max(k, q.cap_k);
+    TRY(grow(ctx, &q.tcnt, tiles * (size_t)kk + 1));
+    TRY(grow(ctx, &q.toff, tiles * (size_t)kk + 1));
+    q.cap_tiles = tiles * (size_t)kk;
+  }
+  if (k > q.cap_k) {
+    TRY(grow(ctx, &q.C, 3 * (size_t)k));
+    TRY(grow(ctx, &q.next, 3 * (size_t)k));
+    TRY(grow(ctx, &q.taken, 3 * (size_t)k));
+    TRY(grow(ctx, &q.dists, (size_t)k * k));
+    TRY(grow(ctx, &q.order, (size_t)k * k));
+    TRY(grow(ctx, &q.sortedD, (size_t)k * k));
+    TRY(grow(ctx, &q.start, (size_t)k + 1));
+    TRY(grow(ctx, &q.empty, (size_t)k));
+    TRY(grow(ctx, &q.chosen, (size_t)k));
+    q.cap_k = k;
+  }
+  if (!q.part) {
+    TRY(grow(ctx, &q.part, (size_t)PTS_BLOCKS));
+    TRY(grow(ctx, &q.cand_i, (size_t)PTS_BLOCKS));
+    TRY(grow(ctx, &q.scal, (size_t)8));
+    TRY(grow(ctx, &q.evals, (size_t)2));
+  }
+  return CQB_OK;
+}
+
+int pts_check(cqb_ctx* ctx, uint64_t n, int k) {
+  if (k < 1) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k must be >= 1");
+  if (k > PTS_KMAX) return fail(ctx, CQB_ERR_UNSUPPORTED, "k = %d exceeds the point-set limit %d", k, PTS_KMAX);
+  if (n >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "point sets above 2^32-1 points");
+  return CQB_OK;
+}
+
+int pts_upload(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n) {
+  CK(cudaMemcpyAsync(ctx->pts.X, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  if (weights) CK(cudaMemcpyAsync(ctx->pts.W, weights, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  return CQB_OK;
+}
+
+// Tables (center_dists, order, sorted rows) of the k centers in pts.C.
+int pts_tables(cqb_ctx* ctx, int k) {
+  k_pts_tables<<<k, PTS_THREADS, 0, ctx->stream>>>(ctx->pts.C, k, ctx->pts.dists, ctx->pts.order, ctx->pts.sortedD);
+  CKL();
+  return CQB_OK;
+}
+
+// assign_sort_means (naive: assign_naive) over pts.X with pts.C and the
+// tables; sse -> pts.scal[0], evals -> pts.evals[0].
+int pts_assign(cqb_ctx* ctx, uint64_t n, int k, int naive = 0, bool audit = false) {
+  CK(cudaMemsetAsync(ctx->pts.evals, 0, sizeof(unsigned long long), ctx->stream));
+  k_pts_assign<<<PTS_BLOCKS, PTS_THREADS, 0, ctx->stream>>>(ctx->pts.X, ctx->pts.W, n, ctx->pts.C, k,
+                                                            ctx->pts.order, ctx->pts.sortedD, ctx->pts.m,
+                                                            ctx->pts.part, ctx->pts.evals, naive,
+                                                            audit ? ctx->pts.skip : nullptr, ctx->pts.prevd);
+  CKL();
+  k_pts_sum<<<1, 32, 0, ctx->stream>>>(ctx->pts.part, PTS_BLOCKS, ctx->pts.scal);
+  CKL();
+  return CQB_OK;
+}
+
+// update_centers: pts.next from pts.C (the centers of the assignment), pts.m.
+int pts_update(cqb_ctx* ctx, uint64_t n, int k, int* n_empty) {
+  auto& q = ctx->pts;
+  const uint32_t tiles = (uint32_t)((n + PTS_TILE - 1) / PTS_TILE);
+  k_pts_tile_count<<<tiles, PTS_THREADS, 0, ctx->stream>>>(q.m, n, k, q.tcnt);
+  CKL();
+  k_pts_offsets<<<1, PTS_KMAX, 0, ctx->stream>>>(q.tcnt, tiles, k, q.toff, q.start);
+  CKL();
+  const int wpb = 4;  // tiles (warps) per block
+  k_pts_tile_scatter<<<(tiles + wpb - 1) / wpb, 32 * wpb, sizeof(uint32_t) * wpb * (size_t)k, ctx->stream>>>(
+      q.m, n, k, q.toff, q.perm);
+  CKL();
+  k_pts_sums<<<(k + 127) / 128, 128, 0, ctx->stream>>>(q.X, q.W, q.perm, q.start, k, q.next, q.empty);
+  CKL();
+  std::vector<int> empty((size_t)k);
+  CK(cudaMemcpyAsync(empty.data(), q.empty, sizeof(int) * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int slot = 0;
+  for (int c = 0; c < k; ++c) {  // empty clusters in increasing order (kmeans.hpp:272-294)
+    if (!empty[(size_t)c]) continue;
+    k_pts_reseed_scan<<<PTS_BLOCKS, PTS_THREADS, 0, ctx->stream>>>(q.X, n, q.C, q.m, q.taken, slot, q.part,
+                                                                   q.cand_i);
+    CKL();
+    k_pts_reseed_pick<<<1, 32, 0, ctx->stream>>>(q.part, q.cand_i, PTS_BLOCKS, q.X, c, q.next, q.taken, slot);
+    CKL();
+    ++slot;
+  }
+  if (n_empty) *n_empty = slot;
+  return CQB_OK;
+}
+
+// init_centers: chosen indices of a partial Fisher-Yates over n points.
+__global__ void __launch_bounds__(PTS_KMAX) k_pts_init(unsigned long long n, int k,
+                                                        const unsigned long long* __restrict__ draws, int ndraws,
+                                                        uint32_t* __restrict__ chosen, int* __restrict__ status) {
+  fisher_yates_block<PTS_KMAX>(n, k, draws, ndraws, chosen, status);
+}
+
+int pts_init(cqb_ctx* ctx, uint64_t n, int k, uint64_t seed) {
+  int ndraws = k + 64;
+  for (int attempt = 0; attempt < 4; ++attempt, ndraws *= 4) {
+    TRY(upload_draws(ctx, seed, ndraws));
+    CK(cudaMemsetAsync(&ctx->st->status, 0, sizeof(int), ctx->stream));
+    k_pts_init<<<1, PTS_KMAX, 0, ctx->stream>>>(n, k, ctx->d_draws, ndraws, ctx->pts.chosen, &ctx->st->status);
+    CKL();
+    int status = 0;
+    CK(cudaMemcpyAsync(&ctx->h_stage->status, &ctx->st->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    status = ctx->h_stage->status;
+    if (status == ST_DRAWS_EXHAUSTED) continue;
+    if (status == ST_K_EXCEEDS_N)
+      return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
+    return CQB_OK;
+  }
+  return fail(ctx, CQB_ERR_INTERNAL, "init_centers: raw draw buffer exhausted");
+}
+}  // namespace
+
+extern "C" {
+
+int cqb_init_centers(cqb_ctx* ctx, uint64_t n_points, int k, uint64_t seed, uint32_t* chosen_out) {
+  if (!ctx || !chosen_out) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(pts_check(ctx, n_points, k));
+  if ((uint64_t)k > n_points)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
+  CK(cudaSetDevice(ctx->device));
+  TRY(pts_reserve(ctx, 1, k));
+  TRY(pts_init(ctx, n_points, k, seed));
+  CK(cudaMemcpy(chosen_out, ctx->pts.chosen, sizeof(uint32_t) * (size_t)k, cudaMemcpyDeviceToHost));
+  return CQB_OK;
+}
+
+int cqb_points_tables(cqb_ctx* ctx, const double* centers, int k, double* center_dists, int32_t* sorted_order) {
+  if (!ctx || !centers) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(pts_check(ctx, 1, k));
+  CK(cudaSetDevice(ctx->device));
+  TRY(pts_reserve(ctx, 1, k));
+  CK(cudaMemcpyAsync(ctx->pts.C, centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  TRY(pts_tables(ctx, k));
+  if (center_dists)
+    CK(cudaMemcpyAsync(center_dists, ctx->pts.dists, sizeof(double) * (size_t)k * k, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  if (sorted_order)
+    CK(cudaMemcpyAsync(sorted_order, ctx->pts.order, sizeof(int32_t) * (size_t)k * k, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CQB_OK;
+}
+
+int cqb_points_assign(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n, const double* centers,
+                      int k, const double* center_dists, const int32_t* sorted_order, int mode,
+                      int32_t* memberships, double* weighted_sse, uint64_t* dist_evals, int32_t* skip_rank_out,
+                      double* prev_dist_out) {
+  if (!ctx || (n && (!points || !weights || !memberships)) || !centers || (mode != 0 && mode != 1))
+    return CQB_ERR_INVALID_ARGUMENT;
+  if (mode == 0)
+    for (uint64_t i = 0; i < n; ++i)
+      if (memberships[i] < 0 || memberships[i] >= k)
+        return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "assign_sort_means: state does not match inputs");
+  TRY(pts_check(ctx, n, k));
+  CK(cudaSetDevice(ctx->device));
+  TRY(pts_reserve(ctx, std::max<uint64_t>(n, 1), k));
+  TRY(pts_upload(ctx, points, weights, n));
+  CK(cudaMemcpyAsync(ctx->pts.C, centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->pts.m, memberships, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  if (mode == 0 && center_dists && sorted_order) {  // the caller's tables (ClusterState), as the reference reads them
+    CK(cudaMemcpyAsync(ctx->pts.dists, center_dists, sizeof(double) * (size_t)k * k, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pts.order, sorted_order, sizeof(int32_t) * (size_t)k * k, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    k_pts_sorted_rows<<<k, PTS_THREADS, 0, ctx->stream>>>(ctx->pts.dists, ctx->pts.order, k, ctx->pts.sortedD);
+    CKL();
+  } else if (mode == 0) {
+    TRY(pts_tables(ctx, k));
+  }
+  const bool audit = mode == 0 && skip_rank_out && prev_dist_out;
+  TRY(pts_assign(ctx, n, k, mode, audit));
+  if (audit) {
+    CK(cudaMemcpyAsync(skip_rank_out, ctx->pts.skip, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(prev_dist_out, ctx->pts.prevd, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  double sse = 0;
+  unsigned long long ev = 0;
+  CK(cudaMemcpyAsync(memberships, ctx->pts.m, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&sse, ctx->pts.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&ev, ctx->pts.evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (weighted_sse) *weighted_sse = sse;
+  if (dist_evals) *dist_evals = ev;
+  return CQB_OK;
+}
+
+int cqb_points_update(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n,
+                      const int32_t* memberships, const double* prev, int k, double* next_out) {
+  if (!ctx || !prev || !next_out || (n && (!points || !weights || !memberships))) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(pts_check(ctx, n, k));
+  if (n == 0) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "update_centers: no points");
+  CK(cudaSetDevice(ctx->device));
+  TRY(pts_reserve(ctx, n, k));
+  TRY(pts_upload(ctx, points, weights, n));
+  CK(cudaMemcpyAsync(ctx->pts.m, memberships, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->pts.C, prev, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  TRY(pts_update(ctx, n, k, nullptr));
+  CK(cudaMemcpyAsync(next_out, ctx->pts.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CQB_OK;
+}
+
+int cqb_points_sse(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n, const double* centers,
+                   int k, const int32_t* memberships, double* sse_out) {
+  if (!ctx || !centers || !sse_out || (n && (!points || !weights || !memberships))) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(pts_check(ctx, n, k));
+  CK(cudaSetDevice(ctx->device));
+  TRY(pts_reserve(ctx, std::max<uint64_t>(n, 1), k));
+  TRY(pts_upload(ctx, points, weights, n));
+  CK(cudaMemcpyAsync(ctx->pts.m, memberships, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->pts.C, centers, sizeof(double) * 3 * (size_t)k, cudaMemcpyHostToDevice, ctx->stream));
+  k_pts_sse<<<PTS_BLOCKS, PTS_THREADS, 0, ctx->stream>>>(ctx->pts.X, ctx->pts.W, n, ctx->pts.C, ctx->pts.m,
+                                                         ctx->pts.part);
+  CKL();
+  k_pts_sum<<<1, 32, 0, ctx->stream>>>(ctx->pts.part, PTS_BLOCKS, ctx->pts.scal);
+  CKL();
+  CK(cudaMemcpyAsync(sse_out, ctx->pts.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CQB_OK;
+}
+
+// run_wsm_points (kmeans.hpp:379-390) = run_weighted_kmeans (:336-376) in
+// SortMeans mode from init_centers(points, k, seed).
+int cqb_run_wsm_points(cqb_ctx* ctx, const double* points, const double* weights, uint64_t n, int k,
+                       const cqb_termination* term, uint64_t seed, double* centers_out, double* sse_history,
+                       int hist_cap, double* trajectory, int traj_cap, int32_t* memberships_out,
+                       cqb_report* report) {
+  if (!ctx || !centers_out || (n && (!points || !weights))) return CQB_ERR_INVALID_ARGUMENT;
+  TRY(pts_check(ctx, n, k));
+  TRY(check_term(ctx, term));
+  if ((uint64_t)k > n)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "init_centers: k exceeds the number of candidate points");
+  CK(cudaSetDevice(ctx->device));
+  TRY(pts_reserve(ctx, n, k));
+  TRY(pts_upload(ctx, points, weights, n));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  TRY(pts_init(ctx, n, k, seed));
+  auto& q = ctx->pts;
+  k_pts_gather<<<(k + 255) / 256, 256, 0, ctx->stream>>>(q.X, q.chosen, k, &ctx->st->status, q.C);
+  CKL();
+  CK(cudaMemsetAsync(q.m, 0, sizeof(int32_t) * n, ctx->stream));  // iteration 1 starts from all-zero memberships
+  std::vector<double> cur((size_t)3 * k), nxt((size_t)3 * k);
+  CK(cudaMemcpyAsync(cur.data(), q.C, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<double> prev_tab;  // the centers the tables were last built from
+  unsigned long long evals = 0;
+  double prev_sse = HUGE_VAL, sse = 0;
+  int iter = 0, empties = 0;
+  const int cap = term->mode == 1 ? term->hard_cap : term->max_iters;
+  for (iter = 1;; ++iter) {
+    // update_center_tables' pair count (kmeans.hpp:137-155): all pairs at
+    // first, then the pairs with at least one moved center
+    unsigned long long pairs = (unsigned long long)k * (k - 1) / 2;
+    if (!prev_tab.empty()) {
+      unsigned long long still = 0;
+      for (int c = 0; c < k; ++c)
+        still += memcmp(&prev_tab[3 * (size_t)c], &cur[3 * (size_t)c], 3 * sizeof(double)) == 0;
+      pairs -= still ? still * (still - 1) / 2 : 0;
+    }
+    evals += pairs;
+    prev_tab = cur;
+    TRY(pts_tables(ctx, k));
+    TRY(pts_assign(ctx, n, k));
+    unsigned long long ev = 0;
+    CK(cudaMemcpyAsync(&sse, q.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&ev, q.evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    int ne = 0;
+    TRY(pts_update(ctx, n, k, &ne));  // synchronizes
+    evals += ev;
+    empties += ne;
+    if (sse_history && iter <= hist_cap) sse_history[iter - 1] = sse;
+    CK(cudaMemcpyAsync(nxt.data(), q.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(q.C, q.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (trajectory && iter <= traj_cap) memcpy(trajectory + (size_t)(iter - 1) * 3 * k, nxt.data(), sizeof(double) * 3 * k);
+    cur.swap(nxt);
+    bool stop;
+    if (term->mode == 0) stop = iter >= term->max_iters;
+    else stop = sse == 0.0 || (prev_sse - sse) / sse <= term->epsilon || iter >= cap;
+    if (stop) break;
+    prev_sse = sse;
+  }
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  memcpy(centers_out, cur.data(), sizeof(double) * 3 * (size_t)k);
+  if (memberships_out) CK(cudaMemcpy(memberships_out, q.m, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  if (report) {
+    cqb_report r{};
+    r.iterations = iter;
+    r.k = k;
+    r.seed = seed;
+    r.sse = sse;
+    r.dist_evals = evals;
+    r.n_unique = n;
+    r.empty_events = empties;
+    float ms = 0.f;
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    r.elapsed_ms = cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess ? ms : 0.0;
+    *report = r;
+  }
+  return CQB_OK;
+}
+
+}  // extern "C"
 
 // ---------------------------------------------------------------------------
 // Sharded WSM (multi-GPU): one step of the same persistent loop over a sample

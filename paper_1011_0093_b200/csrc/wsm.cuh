@@ -131,23 +131,25 @@ struct LoopParams {
 // for all k draws in parallel (a rejection, probability < N'/2^64 per draw,
 // diverts to the exact sequential path); the k swaps then run in one thread
 // with positions >= k held in a small open-addressing map.
-// Body of init_centers for one block (any blockDim >= 1; all threads of the
-// block must call it). Returns early, uniformly, on an error status.
-__device__ void init_centers_block(const uint32_t* __restrict__ keys, unsigned long long n, int k,
-                                   const unsigned long long* __restrict__ draws, int ndraws, WsmState* st) {
+// The chosen indices of init_centers for one block (blockDim >= k <= KM; all
+// threads of the block must call it). Returns early, uniformly, on an error
+// status.
+template <int KM>
+__device__ void fisher_yates_block(unsigned long long n, int k, const unsigned long long* __restrict__ draws,
+                                   int ndraws, uint32_t* __restrict__ chosen_out, int* status) {
   // Partial Fisher-Yates (kmeans.hpp:58-68): for i < k, j_i = i + bounded_rand(N'-i),
   // swap(idx[i], idx[j_i]), center i = colors[idx[i]]. Position i is final
   // after step i (later steps swap positions >= i+1), so with
   //   W(i)  = idx[i] just before step i = W(m) for the last m < i with j_m = i, else i
   //   c_i   = idx[j_i] just before step i = W(m) for the last m < i with j_m = j_i, else j_i
   // every chosen index follows from the j's in parallel (pointer jumping for W).
-  __shared__ unsigned long long jv[KMAX];
-  __shared__ int ptr[2][KMAX];
-  __shared__ uint32_t wv[2][KMAX];
+  __shared__ unsigned long long jv[KM];
+  __shared__ int ptr[2][KM];
+  __shared__ uint32_t wv[2][KM];
   __shared__ int s_rejected;
   const int tid = threadIdx.x;
   if ((unsigned long long)k > n) {
-    if (tid == 0) st->status = ST_K_EXCEEDS_N;
+    if (tid == 0) *status = ST_K_EXCEEDS_N;
     return;
   }
   if (tid == 0) s_rejected = 0;
@@ -168,7 +170,7 @@ __device__ void init_centers_block(const uint32_t* __restrict__ keys, unsigned l
       unsigned long long r;
       do {
         if (di >= ndraws) {
-          st->status = ST_DRAWS_EXHAUSTED;
+          *status = ST_DRAWS_EXHAUSTED;
           s_rejected = 2;
           break;
         }
@@ -194,7 +196,7 @@ __device__ void init_centers_block(const uint32_t* __restrict__ keys, unsigned l
   }
   __syncthreads();
   int cur = 0;
-  for (int round = 0; round < 9; ++round) {  // 2^9 > KMAX: every chain resolved
+  for (int round = 0; (1 << round) <= KM; ++round) {  // 2^rounds > KM: every chain resolved
     if (i < k) {
       const int p = ptr[cur][i];
       ptr[cur ^ 1][i] = p < 0 ? -1 : ptr[cur][p];
@@ -203,17 +205,25 @@ __device__ void init_centers_block(const uint32_t* __restrict__ keys, unsigned l
     __syncthreads();
     cur ^= 1;
   }
-  if (i < k) {
-    const uint32_t chosen = same < 0 ? (uint32_t)jv[i] : wv[cur][same];
-    if (keys) {  // first-occurrence-ordered keys available: gather here
-      const uint32_t key = keys[chosen];
-      st->C[0][3 * i + 0] = (double)key_r(key);
-      st->C[0][3 * i + 1] = (double)key_g(key);
-      st->C[0][3 * i + 2] = (double)key_b(key);
-    }
-    st->chosen[i] = chosen;
+  if (i < k) chosen_out[i] = same < 0 ? (uint32_t)jv[i] : wv[cur][same];
+}
+
+// init_centers for the histogram path: chosen sample ranks into st->chosen,
+// and (with first-occurrence-ordered keys) the centers themselves.
+__device__ void init_centers_block(const uint32_t* __restrict__ keys, unsigned long long n, int k,
+                                   const unsigned long long* __restrict__ draws, int ndraws, WsmState* st) {
+  fisher_yates_block<KMAX>(n, k, draws, ndraws, st->chosen, &st->status);
+  __syncthreads();
+  if (st->status != ST_OK) return;
+  const int i = threadIdx.x;
+  if (keys && i < k) {  // first-occurrence-ordered keys available: gather here
+    const uint32_t key = keys[st->chosen[i]];
+    st->C[0][3 * i + 0] = (double)key_r(key);
+    st->C[0][3 * i + 1] = (double)key_g(key);
+    st->C[0][3 * i + 2] = (double)key_b(key);
   }
 }
+
 
 __global__ void __launch_bounds__(KMAX) k_init_centers(const uint32_t* __restrict__ keys,
                                                       const unsigned long long* __restrict__ n_ptr, int k,
@@ -460,6 +470,30 @@ __device__ __forceinline__ void sadd64(uint2* a, unsigned long long v) {
   const uint32_t old = atomicAdd(&a->x, lo);
   const uint32_t c = (uint32_t)(old + lo) < old ? 1u : 0u;
   if (hi + c) atomicAdd(&a->y, hi + c);
+}
+
+// A sample moving from cluster `from` to cluster `to`: its five moments
+// subtracted (accm) and added (accp). The ten low-word atomics are issued
+// back to back (independent round trips in flight), then the carries and
+// high words follow as fire-and-forget adds.
+__device__ __forceinline__ void acc_move(uint2* accm, uint2* accp, int from, int to, uint32_t key, uint32_t cnt) {
+  const unsigned long long c = cnt;
+  const uint32_t r = key_r(key), g = key_g(key), b = key_b(key);
+  const unsigned long long v[5] = {c * r, c * g, c * b, c, c * (unsigned long long)(r * r + g * g + b * b)};
+  uint32_t om[5], op[5];
+#pragma unroll
+  for (int f = 0; f < 5; ++f) {
+    om[f] = atomicAdd(&accm[f * KMAX + from].x, (uint32_t)v[f]);
+    op[f] = atomicAdd(&accp[f * KMAX + to].x, (uint32_t)v[f]);
+  }
+#pragma unroll
+  for (int f = 0; f < 5; ++f) {
+    const uint32_t lo = (uint32_t)v[f], hi = (uint32_t)(v[f] >> 32);
+    const uint32_t cm = hi + ((uint32_t)(om[f] + lo) < om[f] ? 1u : 0u);
+    const uint32_t cp = hi + ((uint32_t)(op[f] + lo) < op[f] ? 1u : 0u);
+    if (cm) atomicAdd(&accm[f * KMAX + from].y, cm);
+    if (cp) atomicAdd(&accp[f * KMAX + to].y, cp);
+  }
 }
 
 // The five exact moments of one sample: Σc·r, Σc·g, Σc·b, Σc, Σc·|x|².
@@ -1093,8 +1127,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       if (full) {
         acc_point_warp(S.accp, v, nlab[q], key[q], cnt);
       } else if (ch) {
-        acc_point(S.accm, lab[q], key[q], cnt);
-        acc_point(S.accp, nlab[q], key[q], cnt);
+        acc_move(S.accm, S.accp, lab[q], nlab[q], key[q], cnt);
       }
     }
   }

@@ -3,6 +3,7 @@
 // cli_test.cpp:142-151), restated against include/colorq_b200/colorq.hpp and
 // therefore executed on the B200 through the C ABI. Prints one line per case;
 // exit code = number of failures. Run by tests/test_gpu_parity.py.
+#include <cmath>
 #include <cstdio>
 #include <map>
 #include <random>
@@ -157,6 +158,171 @@ int main() {
     const auto rounded = round_palette(fused.palette);
     for (std::size_t i = 0; i < img.size(); ++i) REQUIRE(rounded[fused.index_map[i]] == fused.mapped.pixels[i]);
     std::printf("quantize determinism and fusion\n");
+  }
+  // ---- the point-set API (kmeans_test.cpp:24-240), real-valued points
+  struct Pts {
+    std::vector<Vec3> x;
+    std::vector<double> w;
+  };
+  auto uniform_pts = [](std::size_t n, std::uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(0.0, 255.0), wd(0.05, 1.0);
+    Pts p;
+    double tot = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+      p.x.push_back(Vec3{u(rng), u(rng), u(rng)});
+      p.w.push_back(wd(rng));
+      tot += p.w.back();
+    }
+    for (double& v : p.w) v /= tot;
+    return p;
+  };
+  auto blob_pts = [](std::size_t n, int blobs, std::uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(20.0, 235.0);
+    std::normal_distribution<double> nd(0.0, 6.0);
+    std::vector<Vec3> c;
+    for (int b = 0; b < blobs; ++b) c.push_back(Vec3{u(rng), u(rng), u(rng)});
+    Pts p;
+    for (std::size_t i = 0; i < n; ++i) {
+      const Vec3& m = c[rng() % c.size()];
+      p.x.push_back(Vec3{m[0] + nd(rng), m[1] + nd(rng), m[2] + nd(rng)});
+      p.w.push_back(1.0 / double(n));
+    }
+    return p;
+  };
+  {  // init_centers: k distinct input points, deterministic, k > n throws
+    const Pts p = uniform_pts(10, 7);
+    const Palette all = init_centers(p.x, 10, 123);
+    std::set<Vec3> got(all.centers.begin(), all.centers.end()), src(p.x.begin(), p.x.end());
+    REQUIRE(got.size() == 10 && got == src);
+    REQUIRE(init_centers(p.x, 3, 99).centers == init_centers(p.x, 3, 99).centers);
+    REQUIRE(throws<std::invalid_argument>([&] { init_centers(p.x, 11, 1); }));
+    std::printf("init_centers (points)\n");
+  }
+  {  // assign_naive: one center; own centers; equidistant -> lowest index
+    const Pts p = uniform_pts(50, 3);
+    Palette single;
+    single.centers.push_back(Vec3{1, 2, 3});
+    Memberships m;
+    assign_naive(p.x, p.w, single, m);
+    for (auto v : m) REQUIRE(v == 0);
+    Palette own;
+    own.centers = {Vec3{0, 0, 0}, Vec3{100, 0, 0}, Vec3{0, 100, 0}};
+    std::vector<double> w3(3, 1.0 / 3);
+    assign_naive(own.centers, w3, own, m);
+    REQUIRE((m == Memberships{0, 1, 2}));
+    Palette six;
+    for (int i = 0; i < 6; ++i) six.centers.push_back(Vec3{double(1000 + i * 1000), 0, 0});
+    six.centers[2] = Vec3{10, 0, 0};
+    six.centers[5] = Vec3{30, 0, 0};
+    std::vector<Vec3> probe{Vec3{20, 0, 0}};
+    std::vector<double> pw{1.0};
+    assign_naive(probe, pw, six, m);
+    REQUIRE(m[0] == 2);
+    std::printf("assign_naive ties\n");
+  }
+  {  // sort-means: the break at d == 4 prev evaluates only prev; k = 1
+    std::vector<Vec3> x{Vec3{1, 0, 0}};
+    std::vector<double> w{1.0};
+    Palette pal;
+    pal.centers = {Vec3{0, 0, 0}, Vec3{2, 0, 0}};
+    ClusterState st;
+    st.memberships = {0};
+    st.update_center_tables(pal);
+    REQUIRE(st.d(0, 1) == 4.0);
+    const AssignResult r = assign_sort_means(x, w, pal, st);
+    REQUIRE(st.memberships[0] == 0 && r.dist_evals == 1 && r.weighted_sse == 1.0);
+    const Pts p = uniform_pts(64, 5);
+    Palette one;
+    one.centers.push_back(Vec3{10, 20, 30});
+    ClusterState s1;
+    s1.memberships.assign(p.x.size(), 0);
+    s1.update_center_tables(one);
+    REQUIRE(assign_sort_means(p.x, p.w, one, s1).dist_evals == p.x.size());
+    std::printf("sort-means boundary and k = 1\n");
+  }
+  {  // sort-means = exhaustive through 20 iterations; audited skips are valid
+    const Pts p = blob_pts(1000, 10, 31);
+    const int k = 16;
+    Palette pal = init_centers(p.x, k, 77);
+    ClusterState st;
+    assign_naive(p.x, p.w, pal, st.memberships);
+    std::uint64_t audited = 0;
+    for (int iter = 0; iter < 20; ++iter) {
+      pal = update_centers(p.x, p.w, st.memberships, pal);
+      st.update_center_tables(pal);
+      const SkipAudit audit = [&](std::size_t i, int prev_c, int first_rank, double prev_dist) {
+        const auto* order = st.order_row(prev_c);
+        for (int r = first_rank; r < k; ++r) {
+          REQUIRE(dist2(p.x[i], pal[std::size_t(order[r])]) >= prev_dist * (1.0 - 1e-12));
+          ++audited;
+        }
+      };
+      const AssignResult fast = assign_sort_means(p.x, p.w, pal, st, &audit);
+      Memberships ref;
+      const AssignResult slow = assign_naive(p.x, p.w, pal, ref);
+      REQUIRE(st.memberships == ref);
+      REQUIRE(std::abs(fast.weighted_sse - slow.weighted_sse) <= 1e-12 * slow.weighted_sse);
+      REQUIRE(fast.dist_evals <= slow.dist_evals);
+      REQUIRE(std::abs(weighted_sse(p.x, p.w, pal, st.memberships) - slow.weighted_sse) <= 1e-12 * slow.weighted_sse);
+    }
+    REQUIRE(audited > 0);
+    std::printf("sort-means equals exhaustive (20 iterations, audit)\n");
+  }
+  {  // center tables: symmetric, zero diagonal, self-first sorted permutation rows
+    const Pts p = uniform_pts(40, 8);
+    const Palette pal = init_centers(p.x, 12, 3);
+    ClusterState st;
+    std::uint64_t pairs = 0;
+    st.update_center_tables(pal, &pairs);
+    REQUIRE(pairs == 66);
+    for (int i = 0; i < 12; ++i) {
+      REQUIRE(st.d(i, i) == 0.0);
+      for (int j = 0; j < 12; ++j) REQUIRE(st.d(i, j) == st.d(j, i));
+      const auto* row = st.order_row(i);
+      REQUIRE(row[0] == i);
+      REQUIRE(std::set<int>(row, row + 12).size() == 12);
+      for (int j = 2; j < 12; ++j) REQUIRE(st.d(i, row[j - 1]) <= st.d(i, row[j]));
+    }
+    Palette moved = pal;
+    moved[3] = Vec3{1, 2, 3};
+    st.update_center_tables(moved, &pairs);
+    REQUIRE(pairs == 66 + 11);  // only the pairs of the moved center
+    std::printf("center tables\n");
+  }
+  {  // update_centers: weighted means; an empty cluster re-seeded at the farthest point
+    std::vector<Vec3> x{Vec3{0, 0, 0}, Vec3{255, 255, 255}};
+    Palette prev;
+    prev.centers.push_back(Vec3{1, 1, 1});
+    Memberships m{0, 0};
+    const Palette next = update_centers(x, std::vector<double>{0.75, 0.25}, m, prev);
+    REQUIRE(std::abs(next[0][0] - 63.75) <= 1e-12 * 63.75);
+    REQUIRE((update_centers(x, std::vector<double>{0.5, 0.5}, m, prev)[0] == Vec3{127.5, 127.5, 127.5}));
+    std::vector<Vec3> y{Vec3{0, 0, 0}, Vec3{10, 0, 0}, Vec3{200, 0, 0}};
+    Palette p2;
+    p2.centers = {Vec3{5, 0, 0}, Vec3{999, 999, 999}};
+    const Palette r2 = update_centers(y, std::vector<double>{0.3, 0.3, 0.4}, Memberships{0, 0, 0}, p2);
+    REQUIRE((r2[1] == Vec3{200, 0, 0}));
+    std::printf("update_centers means and reseed\n");
+  }
+  {  // run_wsm_points: deterministic, SSE nonincreasing; run_wsm on a
+     // real-valued histogram takes the same point path
+    const Pts p = blob_pts(3000, 12, 9);
+    const auto a = run_wsm_points(p.x, p.w, 12, Termination::convergent(1e-4, 100), 5);
+    const auto b = run_wsm_points(p.x, p.w, 12, Termination::convergent(1e-4, 100), 5);
+    REQUIRE(a.palette.centers == b.palette.centers && a.report.iterations == b.report.iterations);
+    for (std::size_t i = 1; i < a.report.sse_history.size(); ++i)
+      REQUIRE(a.report.sse_history[i] <= a.report.sse_history[i - 1] * (1 + 1e-12));
+    ColorHistogram h;
+    h.colors = p.x;
+    h.weights = p.w;
+    h.total_pixels = p.x.size();
+    const auto c = run_wsm(h, 12, Termination::convergent(1e-4, 100), 5);
+    REQUIRE(c.palette.centers == a.palette.centers && c.report.dist_evals == a.report.dist_evals);
+    const auto big = run_wsm_points(p.x, p.w, 300, Termination::fixed(3), 2);  // k > 256
+    REQUIRE(big.palette.size() == 300 && big.report.iterations == 3);
+    std::printf("run_wsm_points and the real-valued histogram path\n");
   }
   std::printf("%s (%d failures)\n", g_fail ? "FAIL" : "PASS", g_fail);
   return g_fail;
