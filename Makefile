@@ -10,7 +10,7 @@ IO_TEST   := build/io_test
 
 all: $(LIB) oracle $(SHIM_TEST) $(CLI) $(IO_TEST)
 
-$(LIB): $(CSRC)/capi.cu $(CSRC)/common.cuh $(CSRC)/hist.cuh $(CSRC)/part.cuh $(CSRC)/points.cuh $(CSRC)/wsm.cuh $(CSRC)/map.cuh $(CSRC)/prep.cuh include/colorq_b200.h
+$(LIB): $(CSRC)/capi.cu $(CSRC)/common.cuh $(CSRC)/hist.cuh $(CSRC)/points.cuh $(CSRC)/wsm.cuh $(CSRC)/map.cuh $(CSRC)/prep.cuh include/colorq_b200.h
 	mkdir -p $(dir $@) build
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/capi.cu 2> build/ptxas.log || (cat build/ptxas.log; false)
 

@@ -18,7 +18,6 @@
 #include "map.cuh"
 #include "wsm.cuh"
 #include "prep.cuh"
-#include "part.cuh"
 #include "points.cuh"
 
 using namespace cqb;
@@ -72,9 +71,7 @@ struct cqb_ctx {
   int prep_blocks = 0;                 // k_prep_small cooperative grid
   uint8_t* d_err = nullptr;       // error_image raster (cqb_quantize_ex / cqb_error_image)
   uint8_t* err_target = nullptr;  // set only while cqb_quantize_ex enqueues: fused error_image output
-  int naive_mode = 0;             // set only while cqb_run_km_full enqueues: exhaustive assign (KM)
   bool fuse_map = false;          // set only while enqueue_quantize launches the loop: map epilogue
-  int fkm_kprime = 0;             // set only while cqb_run_fkm enqueues: FKM neighbour count
   uint8_t* d_cand = nullptr;      // iteration-1 candidate centers per 16^3 color cell
   uint16_t* d_cand_n = nullptr;
   uint32_t* d_bpre = nullptr;    // per-word set-bit prefix of d_bitmap
@@ -84,15 +81,6 @@ struct cqb_ctx {
   uint32_t* d_mcounts = nullptr;
   uint32_t* d_mrank = nullptr;
   unsigned long long* bin_tile_state = nullptr;  // K2b look-back [N_BIN_TILES] + ticket
-  // partitioned large-image histogram (part.cuh)
-  uint32_t* d_entries = nullptr;       // P bucket entries
-  size_t cap_entries = 0;
-  uint32_t* part_cnt = nullptr;        // [source blocks][PB_N]
-  uint32_t* part_off = nullptr;
-  size_t cap_part = 0;                 // source blocks allocated
-  uint32_t* part_start = nullptr;      // [PB_N + 1]
-  unsigned long long* part_tiles = nullptr;  // H4 look-back [PB_N] + ticket
-  uint32_t* first_tab = nullptr;       // 2^24 first pixel per Morton bin (touched bins only)
   // init_centers by rank selection over first pixels (hist.cuh RS1-RS4)
   uint32_t* rs_coarse = nullptr;       // [RS_NC]
   uint16_t* rs_slot_of = nullptr;      // [RS_NC]
@@ -261,24 +249,6 @@ int ensure_samples(cqb_ctx* ctx, size_t n) {
   return CQB_OK;
 }
 
-int ensure_part(cqb_ctx* ctx, uint64_t P, uint32_t blocks) {
-  if (P > ctx->cap_entries) {
-    TRY(grow(ctx, &ctx->d_entries, (size_t)P + 64));
-    ctx->cap_entries = (size_t)P + 64;
-  }
-  if (blocks > ctx->cap_part) {
-    TRY(grow(ctx, &ctx->part_cnt, (size_t)blocks * PB_N));
-    TRY(grow(ctx, &ctx->part_off, (size_t)blocks * PB_N));
-    ctx->cap_part = blocks;
-  }
-  if (!ctx->first_tab) {
-    TRY(grow(ctx, &ctx->first_tab, (size_t)1 << 24));
-    TRY(grow(ctx, &ctx->part_start, (size_t)PB_N + 1));
-    TRY(grow(ctx, &ctx->part_tiles, (size_t)PB_N + 1));
-  }
-  return CQB_OK;
-}
-
 int ensure_hist(cqb_ctx* ctx, int n) {
   if (n <= ctx->cap_hist) return CQB_OK;
   TRY(grow(ctx, &ctx->d_hist, (size_t)n));
@@ -418,46 +388,6 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   const uint32_t n_words = (uint32_t)((P + 31) / 32);
   const uint32_t ntiles = (n_words + BS_WORDS - 1) / BS_WORDS;
   const bool fused = fused_prep(ctx, P);
-  if (!sparse_path(ctx, P) && (ctx->debug_flags & DBG_PART_HIST)) {
-    // partitioned histogram (part.cuh): H1-H3 partition the pixels into
-    // 2048 Morton buckets, H4 builds each bucket's table in shared memory
-    // and emits the Morton-order samples, H5 flags first occurrences
-    const PartGeom g = part_geom(P, ctx->num_sms);
-    TRY(ensure_part(ctx, P, g.blocks));
-    CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
-    CK(cudaMemsetAsync(ctx->part_tiles, 0, sizeof(unsigned long long) * (PB_N + 1), ctx->stream));
-    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
-    k_part_count<<<g.blocks, PB_THREADS, 0, ctx->stream>>>(d_img, P, g.range, ctx->part_cnt);
-    CKL();
-    k_part_scan<<<1, PB_THREADS, 0, ctx->stream>>>(ctx->part_cnt, g.blocks, ctx->part_off, ctx->part_start);
-    CKL();
-    k_part_scatter<<<g.blocks, PB_THREADS, 0, ctx->stream>>>(d_img, P, g.range, ctx->part_off, ctx->d_entries);
-    CKL();
-    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));
-    k_part_build<<<PB_N, PB_BUILD_THREADS, PB_BUILD_SMEM, ctx->stream>>>(
-        ctx->d_entries, ctx->part_off, ctx->part_start, g.blocks, g.range, ctx->d_mkeys, ctx->d_mcounts,
-        ctx->d_mrank, rank_order ? ctx->first_tab : nullptr, ctx->part_tiles,
-        reinterpret_cast<unsigned int*>(ctx->part_tiles + PB_N),
-        ctx->d_n);
-    CKL();
-    if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
-    if (!rank_order) {
-      if (init_k > 0) TRY(enqueue_rank_select(ctx, d_img, P, init_k, ndraws));
-      return CQB_OK;
-    }
-    k_first_flags<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(d_img, P, ctx->first_tab, ctx->d_bitmap);
-    CKL();
-    k_bitmap_scan<<<ntiles, BS_THREADS, 0, ctx->stream>>>(ctx->d_bitmap, n_words, ctx->d_bpre, ctx->tile_state,
-                                                          reinterpret_cast<unsigned int*>(ctx->tile_state + ntiles));
-    CKL();
-    if (rank_order) {  // build_histogram API: ranks + the first-occurrence-ordered histogram
-      k_rank_from_bitmap<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
-          ctx->d_bitmap, ctx->d_bpre, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n, ctx->d_keys,
-          ctx->d_counts, ctx->d_first, nullptr, &ctx->st->status, 0, nullptr);
-      CKL();
-    }
-    return CQB_OK;
-  }
   if (!(fused && zero_state)) CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
   if (!fused) CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
@@ -568,7 +498,6 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.block_times = ctx->profiling ? ctx->d_block_times : nullptr;
   L.stamp_iter = ctx->stamp_iter;
   L.debug_flags = ctx->debug_flags;
-  L.naive = ctx->naive_mode;
   if (ctx->fuse_map && !(ctx->debug_flags & 256)) {
     L.map_sortedDr = ctx->d_sortedDr;
     L.map_orderR = ctx->d_orderR;
@@ -581,7 +510,6 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
     L.cand = ctx->d_cand;
     L.cand_n = ctx->d_cand_n;
   }
-  L.fkm_kprime = ctx->fkm_kprime;
   if (ctx->profiling)
     CK(cudaMemsetAsync(ctx->d_timeline, 0, sizeof(unsigned long long) * 8 * (size_t)ctx->cap_hist, ctx->stream));
   int X = 0;
@@ -603,24 +531,17 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   // one point per lane per grab for small sample sets (N' <= P < 2M): finer
   // balance; two for large ones: more ILP (cfg2 +1.2%, cfg4 +8% respectively)
   const bool small = total < OCC_MAX_PIXELS;
-  const void* kern = X == 1 ? (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 1>
-                                     : (const void*)k_wsm_loop<Assign::SortMeans, 2, 1>)
-                     : X == 2 ? (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 2>
-                                       : (const void*)k_wsm_loop<Assign::SortMeans, 2, 2>)
-                     : L.naive ? (small ? (const void*)k_wsm_loop<Assign::Naive, 1, 0>
-                                        : (const void*)k_wsm_loop<Assign::Naive, 2, 0>)
-                     : L.fkm_kprime > 0 ? (small ? (const void*)k_wsm_loop<Assign::Fkm, 1, 0>
-                                                 : (const void*)k_wsm_loop<Assign::Fkm, 2, 0>)
-                                        : (small ? (const void*)k_wsm_loop<Assign::SortMeans, 1, 0>
-                                                 : (const void*)k_wsm_loop<Assign::SortMeans, 2, 0>);
+  const void* kern = X == 1   ? (small ? (const void*)k_wsm_loop<1, 1> : (const void*)k_wsm_loop<2, 1>)
+                     : X == 2 ? (small ? (const void*)k_wsm_loop<1, 2> : (const void*)k_wsm_loop<2, 2>)
+                              : (small ? (const void*)k_wsm_loop<1, 0> : (const void*)k_wsm_loop<2, 0>);
   size_t dyn = LOOP_DYN_SMEM;
-  if (X == 0 && small && !L.naive && L.fkm_kprime == 0 && !(ctx->debug_flags & 512)) {
+  if (X == 0 && small && !(ctx->debug_flags & 512)) {
     // resident samples when the block's share (bounded by P) fits in shared memory
     const uint64_t cap = ((total + 31) / 32 + grid - 1) / grid * 32;
     if (res_smem_bytes((int)std::min<uint64_t>(cap, 1u << 24)) <= RES_DYN_MAX) {
       L.res_cap = (int)cap;
       dyn = res_smem_bytes(L.res_cap);
-      kern = (const void*)k_wsm_loop<Assign::SortMeans, 1, 0, true>;
+      kern = (const void*)k_wsm_loop<1, 0, true>;
     }
   }
   CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(LOOP_THREADS), args, dyn, ctx->stream));
@@ -797,17 +718,12 @@ int cqb_create(int device, cqb_ctx** out) {
     if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
     ctx->num_sms = prop.multiProcessorCount;
     int nb = 0;
-    for (const void* f : {(const void*)k_wsm_loop<Assign::SortMeans, 1, 0>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 0>,
-                          (const void*)k_wsm_loop<Assign::Naive, 1, 0>, (const void*)k_wsm_loop<Assign::Naive, 2, 0>,
-                          (const void*)k_wsm_loop<Assign::Fkm, 1, 0>, (const void*)k_wsm_loop<Assign::Fkm, 2, 0>,
-                          (const void*)k_wsm_loop<Assign::SortMeans, 1, 1>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 1>,
-                          (const void*)k_wsm_loop<Assign::SortMeans, 1, 2>, (const void*)k_wsm_loop<Assign::SortMeans, 2, 2>})
+    for (const void* f : {(const void*)k_wsm_loop<1, 0>, (const void*)k_wsm_loop<2, 0>, (const void*)k_wsm_loop<1, 1>,
+                          (const void*)k_wsm_loop<2, 1>, (const void*)k_wsm_loop<1, 2>, (const void*)k_wsm_loop<2, 2>})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
-    CK(cudaFuncSetAttribute((const void*)k_wsm_loop<Assign::SortMeans, 1, 0, true>,
+    CK(cudaFuncSetAttribute((const void*)k_wsm_loop<1, 0, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RES_DYN_MAX));
-    CK(cudaFuncSetAttribute((const void*)k_part_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)PB_BUILD_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<Assign::SortMeans, 2, 0>, LOOP_THREADS,
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<2, 0>, LOOP_THREADS,
                                                      LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
     ctx->loop_blocks_max = std::min(nb, CQB_LOOP_MINB) * ctx->num_sms;
@@ -875,8 +791,7 @@ int cqb_destroy(cqb_ctx* ctx) {
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,
                  ctx->d_ints, ctx->d_taken, ctx->d_cand_d, ctx->d_cand_r, ctx->d_cand_k, ctx->d_traj, ctx->d_centers_in, ctx->d_sortedDr, ctx->d_orderR, ctx->d_palkey,
-                 ctx->d_draws, ctx->d_entries, ctx->part_cnt, ctx->part_off, ctx->part_start, ctx->part_tiles,
-                 ctx->first_tab, ctx->rs_coarse, ctx->rs_slot_of, ctx->rs_tgt, ctx->rs_slot_bits,
+                 ctx->d_draws, ctx->rs_coarse, ctx->rs_slot_of, ctx->rs_tgt, ctx->rs_slot_bits,
                  ctx->pts.X, ctx->pts.W, ctx->pts.m, ctx->pts.perm, ctx->pts.skip, ctx->pts.prevd,
                  ctx->pts.tcnt, ctx->pts.toff, ctx->pts.C, ctx->pts.next, ctx->pts.taken, ctx->pts.dists,
                  ctx->pts.order, ctx->pts.sortedD, ctx->pts.start, ctx->pts.empty, ctx->pts.part,
@@ -1278,20 +1193,63 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   return CQB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+int pts_reserve(cqb_ctx* ctx, uint64_t n, int k);
+int pts_run(cqb_ctx* ctx, uint64_t n, int k, const cqb_termination* term, int mode, int kprime, uint64_t seed,
+            double* centers_out, double* sse_history, int hist_cap, double* trajectory, int traj_cap,
+            int32_t* memberships_out, cqb_report* report);
+
+// The pixel-space comparators of methods.hpp (run_km_full, kmeans.hpp:
+// 409-426; run_fkm over pixels_as_points, methods.hpp:163-178): initial
+// centers = init_centers(build_histogram(image), k, seed) from the device
+// histogram pipeline, then run_weighted_kmeans over all P pixels (weight
+// 1/P each) on the point-set kernels, so every reported distance evaluation
+// is one the device performs.
+int pixel_kmeans(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
+                 uint64_t seed, int mode, int kprime, double* centers_out, double* sse_history, int hist_cap,
+                 cqb_report* report) {
+  if (width <= 0 || height <= 0 || !rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "image dimensions must be positive");
+  TRY(check_k(ctx, k));
+  TRY(check_term(ctx, term));
+  const uint64_t P = (uint64_t)width * (uint64_t)height;
+  if (P >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  CK(cudaSetDevice(ctx->device));
+  TRY(ensure_pixels(ctx, P));
+  TRY(ensure_samples(ctx, P));
+  TRY(pts_reserve(ctx, P, k));
+  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  int ndraws = k + 64;
+  for (int attempt = 0;; ++attempt) {
+    TRY(upload_draws(ctx, seed, ndraws));
+    const bool fused = fused_prep(ctx, P);
+    if (!fused) TRY(reset_state(ctx));
+    TRY(enqueue_histogram(ctx, ctx->d_img, P, false, false, k, ndraws, fused));
+    CK(cudaMemcpyAsync(&ctx->h_stage->status, &ctx->st->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_stage->status != ST_DRAWS_EXHAUSTED || attempt == 3) break;
+    ndraws *= 4;
+  }
+  TRY(check_status(ctx));
+  k_pts_from_rgb<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->d_img, P, ctx->pts.X, ctx->pts.W);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->pts.C, ctx->st->C[0], sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  TRY(pts_run(ctx, P, k, term, mode, kprime, seed, centers_out, sse_history, hist_cap, nullptr, 0, nullptr, report));
+  if (report) report->mse = 0.0;  // the caller fills mse (methods.hpp:104-106)
+  return CQB_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int cqb_run_km_full(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, const cqb_termination* term,
                     uint64_t seed, double* centers_out, double* sse_history, int hist_cap, cqb_report* report) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
-  cqb_report rep{};
-  ctx->naive_mode = 1;
-  const int rc = cqb_quantize_ex(ctx, rgb, width, height, k, term, seed, centers_out, sse_history, hist_cap, nullptr,
-                                 nullptr, nullptr, &rep);
-  ctx->naive_mode = 0;
-  TRY(rc);
-  // assign_naive counts every (pixel, center) pair (kmeans.hpp:104); no tables
-  rep.dist_evals = (uint64_t)rep.iterations * (uint64_t)width * (uint64_t)height * (uint64_t)k;
-  rep.mse = 0.0;  // run_km_full leaves mse to the caller (methods.hpp:104-106)
-  if (report) *report = rep;
-  return CQB_OK;
+  return pixel_kmeans(ctx, rgb, width, height, k, term, seed, PTS_NAIVE, 0, centers_out, sse_history, hist_cap,
+                      report);
 }
 
 int cqb_run_fkm(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, int k_prime,
@@ -1299,19 +1257,8 @@ int cqb_run_fkm(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int k, 
                 cqb_report* report) {
   if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
   if (k_prime < 1 || k_prime > k) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "run_fkm: need 1 <= k_prime <= k");
-  cqb_report rep{};
-  ctx->fkm_kprime = k_prime;
-  const int rc = cqb_quantize_ex(ctx, rgb, width, height, k, term, seed, centers_out, sse_history, hist_cap, nullptr,
-                                 nullptr, nullptr, &rep);
-  ctx->fkm_kprime = 0;
-  TRY(rc);
-  // iteration 1 is assign_naive (P*k); later ones search k' centers (P*k'),
-  // plus the table pair evaluations already in rep.dist_evals
-  const uint64_t P = (uint64_t)width * (uint64_t)height;
-  rep.dist_evals += P * (uint64_t)k + (uint64_t)(rep.iterations - 1) * P * (uint64_t)k_prime;
-  rep.mse = 0.0;
-  if (report) *report = rep;
-  return CQB_OK;
+  return pixel_kmeans(ctx, rgb, width, height, k, term, seed, PTS_FKM, k_prime, centers_out, sse_history, hist_cap,
+                      report);
 }
 
 int cqb_error_image(cqb_ctx* ctx, const uint8_t* original, const uint8_t* quantized, uint64_t n_pixels,
@@ -1385,6 +1332,8 @@ int cqb_mse(cqb_ctx* ctx, const uint8_t* a, const uint8_t* b, uint64_t n_pixels,
   return CQB_OK;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------------------
 // Generic weighted points (points.cuh): kmeans.hpp's span<const Vec3> API.
 namespace {
@@ -1452,11 +1401,11 @@ int pts_tables(cqb_ctx* ctx, int k) {
 
 // assign_sort_means (naive: assign_naive) over pts.X with pts.C and the
 // tables; sse -> pts.scal[0], evals -> pts.evals[0].
-int pts_assign(cqb_ctx* ctx, uint64_t n, int k, int naive = 0, bool audit = false) {
+int pts_assign(cqb_ctx* ctx, uint64_t n, int k, int mode = PTS_SORT_MEANS, bool audit = false, int kprime = 0) {
   CK(cudaMemsetAsync(ctx->pts.evals, 0, sizeof(unsigned long long), ctx->stream));
   k_pts_assign<<<PTS_BLOCKS, PTS_THREADS, 0, ctx->stream>>>(ctx->pts.X, ctx->pts.W, n, ctx->pts.C, k,
                                                             ctx->pts.order, ctx->pts.sortedD, ctx->pts.m,
-                                                            ctx->pts.part, ctx->pts.evals, naive,
+                                                            ctx->pts.part, ctx->pts.evals, mode, kprime,
                                                             audit ? ctx->pts.skip : nullptr, ctx->pts.prevd);
   CKL();
   k_pts_sum<<<1, 32, 0, ctx->stream>>>(ctx->pts.part, PTS_BLOCKS, ctx->pts.scal);
@@ -1520,6 +1469,79 @@ int pts_init(cqb_ctx* ctx, uint64_t n, int k, uint64_t seed) {
   }
   return fail(ctx, CQB_ERR_INTERNAL, "init_centers: raw draw buffer exhausted");
 }
+// run_weighted_kmeans (kmeans.hpp:336-376) from the centers in pts.C:
+// SortMeans (WSM), Naive (run_km_full, :409-426) or FKM (run_fkm,
+// fast_variants.hpp:20-81: iteration 1 exhaustive, then k' neighbours).
+int pts_run(cqb_ctx* ctx, uint64_t n, int k, const cqb_termination* term, int mode, int kprime, uint64_t seed,
+            double* centers_out, double* sse_history, int hist_cap, double* trajectory, int traj_cap,
+            int32_t* memberships_out, cqb_report* report) {
+  auto& q = ctx->pts;
+  CK(cudaMemsetAsync(q.m, 0, sizeof(int32_t) * n, ctx->stream));  // iteration 1 starts from all-zero memberships
+  std::vector<double> cur((size_t)3 * k), nxt((size_t)3 * k);
+  CK(cudaMemcpyAsync(cur.data(), q.C, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<double> prev_tab;  // the centers the tables were last built from
+  unsigned long long evals = 0;
+  double prev_sse = HUGE_VAL, sse = 0;
+  int iter = 0, empties = 0;
+  const int cap = term->mode == 1 ? term->hard_cap : term->max_iters;
+  for (iter = 1;; ++iter) {
+    // this iteration's assignment: FKM's first one is exhaustive
+    const int am = mode == PTS_FKM && iter == 1 ? PTS_NAIVE : mode;
+    if (am != PTS_NAIVE) {
+      // update_center_tables' pair count (kmeans.hpp:137-155): all pairs at
+      // first, then the pairs with at least one moved center
+      unsigned long long pairs = (unsigned long long)k * (k - 1) / 2;
+      if (!prev_tab.empty()) {
+        unsigned long long still = 0;
+        for (int c = 0; c < k; ++c)
+          still += memcmp(&prev_tab[3 * (size_t)c], &cur[3 * (size_t)c], 3 * sizeof(double)) == 0;
+        pairs -= still ? still * (still - 1) / 2 : 0;
+      }
+      evals += pairs;
+      prev_tab = cur;
+      TRY(pts_tables(ctx, k));
+    }
+    TRY(pts_assign(ctx, n, k, am, false, kprime));
+    unsigned long long ev = 0;
+    CK(cudaMemcpyAsync(&sse, q.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&ev, q.evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    int ne = 0;
+    TRY(pts_update(ctx, n, k, &ne));  // synchronizes
+    evals += ev;
+    empties += ne;
+    if (sse_history && iter <= hist_cap) sse_history[iter - 1] = sse;
+    CK(cudaMemcpyAsync(nxt.data(), q.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(q.C, q.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (trajectory && iter <= traj_cap) memcpy(trajectory + (size_t)(iter - 1) * 3 * k, nxt.data(), sizeof(double) * 3 * k);
+    cur.swap(nxt);
+    bool stop;
+    if (term->mode == 0) stop = iter >= term->max_iters;
+    else stop = sse == 0.0 || (prev_sse - sse) / sse <= term->epsilon || iter >= cap;
+    if (stop) break;
+    prev_sse = sse;
+  }
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  memcpy(centers_out, cur.data(), sizeof(double) * 3 * (size_t)k);
+  if (memberships_out) CK(cudaMemcpy(memberships_out, q.m, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  if (report) {
+    cqb_report r{};
+    r.iterations = iter;
+    r.k = k;
+    r.seed = seed;
+    r.sse = sse;
+    r.dist_evals = evals;
+    r.n_unique = n;
+    r.empty_events = empties;
+    float ms = 0.f;
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    r.elapsed_ms = cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess ? ms : 0.0;
+    *report = r;
+  }
+  return CQB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1647,72 +1669,14 @@ int cqb_run_wsm_points(cqb_ctx* ctx, const double* points, const double* weights
   TRY(pts_upload(ctx, points, weights, n));
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   TRY(pts_init(ctx, n, k, seed));
-  auto& q = ctx->pts;
-  k_pts_gather<<<(k + 255) / 256, 256, 0, ctx->stream>>>(q.X, q.chosen, k, &ctx->st->status, q.C);
+  k_pts_gather<<<(k + 255) / 256, 256, 0, ctx->stream>>>(ctx->pts.X, ctx->pts.chosen, k, &ctx->st->status,
+                                                         ctx->pts.C);
   CKL();
-  CK(cudaMemsetAsync(q.m, 0, sizeof(int32_t) * n, ctx->stream));  // iteration 1 starts from all-zero memberships
-  std::vector<double> cur((size_t)3 * k), nxt((size_t)3 * k);
-  CK(cudaMemcpyAsync(cur.data(), q.C, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  std::vector<double> prev_tab;  // the centers the tables were last built from
-  unsigned long long evals = 0;
-  double prev_sse = HUGE_VAL, sse = 0;
-  int iter = 0, empties = 0;
-  const int cap = term->mode == 1 ? term->hard_cap : term->max_iters;
-  for (iter = 1;; ++iter) {
-    // update_center_tables' pair count (kmeans.hpp:137-155): all pairs at
-    // first, then the pairs with at least one moved center
-    unsigned long long pairs = (unsigned long long)k * (k - 1) / 2;
-    if (!prev_tab.empty()) {
-      unsigned long long still = 0;
-      for (int c = 0; c < k; ++c)
-        still += memcmp(&prev_tab[3 * (size_t)c], &cur[3 * (size_t)c], 3 * sizeof(double)) == 0;
-      pairs -= still ? still * (still - 1) / 2 : 0;
-    }
-    evals += pairs;
-    prev_tab = cur;
-    TRY(pts_tables(ctx, k));
-    TRY(pts_assign(ctx, n, k));
-    unsigned long long ev = 0;
-    CK(cudaMemcpyAsync(&sse, q.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&ev, q.evals, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-    int ne = 0;
-    TRY(pts_update(ctx, n, k, &ne));  // synchronizes
-    evals += ev;
-    empties += ne;
-    if (sse_history && iter <= hist_cap) sse_history[iter - 1] = sse;
-    CK(cudaMemcpyAsync(nxt.data(), q.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(q.C, q.next, sizeof(double) * 3 * (size_t)k, cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    if (trajectory && iter <= traj_cap) memcpy(trajectory + (size_t)(iter - 1) * 3 * k, nxt.data(), sizeof(double) * 3 * k);
-    cur.swap(nxt);
-    bool stop;
-    if (term->mode == 0) stop = iter >= term->max_iters;
-    else stop = sse == 0.0 || (prev_sse - sse) / sse <= term->epsilon || iter >= cap;
-    if (stop) break;
-    prev_sse = sse;
-  }
-  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-  memcpy(centers_out, cur.data(), sizeof(double) * 3 * (size_t)k);
-  if (memberships_out) CK(cudaMemcpy(memberships_out, q.m, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
-  if (report) {
-    cqb_report r{};
-    r.iterations = iter;
-    r.k = k;
-    r.seed = seed;
-    r.sse = sse;
-    r.dist_evals = evals;
-    r.n_unique = n;
-    r.empty_events = empties;
-    float ms = 0.f;
-    CK(cudaEventSynchronize(ctx->ev[1]));
-    r.elapsed_ms = cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess ? ms : 0.0;
-    *report = r;
-  }
-  return CQB_OK;
+  return pts_run(ctx, n, k, term, PTS_SORT_MEANS, 0, seed, centers_out, sse_history, hist_cap, trajectory, traj_cap,
+                 memberships_out, report);
 }
 
-}  // extern "C"
+
 
 // ---------------------------------------------------------------------------
 // Sharded WSM (multi-GPU): one step of the same persistent loop over a sample

@@ -23,6 +23,20 @@ namespace cqb {
 constexpr int PTS_KMAX = 1024;
 constexpr int PTS_THREADS = 256;
 constexpr int PTS_TILE = 1024;  // points per tile of the stable counting sort
+constexpr int PTS_SORT_MEANS = 0, PTS_NAIVE = 1, PTS_FKM = 2;  // k_pts_assign modes
+
+// Pixels as points (methods.hpp pixels_as_points; kmeans.hpp:413-416): the
+// u8x3 raster widened to FP64 points of weight 1/P each.
+__global__ void k_pts_from_rgb(const uint8_t* __restrict__ rgb, uint64_t P, double* __restrict__ X,
+                               double* __restrict__ W) {
+  const double w = 1.0 / (double)P;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (uint64_t)gridDim.x * blockDim.x) {
+    X[3 * i] = (double)rgb[3 * i];
+    X[3 * i + 1] = (double)rgb[3 * i + 1];
+    X[3 * i + 2] = (double)rgb[3 * i + 2];
+    W[i] = w;
+  }
+}
 
 // Row p of the center tables: center_dists[p][t] = dist2(c_p, c_t) (zero
 // diagonal, symmetric), order[p] = [p, others by (d, index)], sortedD[p][j] =
@@ -70,8 +84,8 @@ __global__ void __launch_bounds__(PTS_THREADS) k_pts_assign(const double* __rest
                                                             const int32_t* __restrict__ order,
                                                             const double* __restrict__ sortedD,
                                                             int32_t* __restrict__ m, double* __restrict__ sse_part,
-                                                            unsigned long long* __restrict__ evals, int naive,
-                                                            int32_t* __restrict__ skip_rank,
+                                                            unsigned long long* __restrict__ evals, int mode,
+                                                            int kprime, int32_t* __restrict__ skip_rank,
                                                             double* __restrict__ prev_out) {
   __shared__ double cs[3 * PTS_KMAX];
   __shared__ double red[PTS_THREADS / 32];
@@ -82,7 +96,24 @@ __global__ void __launch_bounds__(PTS_THREADS) k_pts_assign(const double* __rest
   unsigned long long ev = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const double x0 = X[3 * i], x1 = X[3 * i + 1], x2 = X[3 * i + 2];
-    if (naive) {  // assign_naive (kmeans.hpp:89-102): strict '<' from c_0
+    if (mode == PTS_FKM) {  // run_fkm (fast_variants.hpp:42-55): order[m][0..k'), ties to the lowest index
+      const int32_t* row = order + (size_t)m[i] * k;
+      int best = row[0];
+      double best_d = dist2_rn(x0, x1, x2, cs[3 * best], cs[3 * best + 1], cs[3 * best + 2]);
+      for (int j = 1; j < kprime; ++j) {
+        const int t = row[j];
+        const double dist = dist2_rn(x0, x1, x2, cs[3 * t], cs[3 * t + 1], cs[3 * t + 2]);
+        if (dist < best_d || (dist == best_d && t < best)) {
+          best_d = dist;
+          best = t;
+        }
+      }
+      ev += (unsigned long long)kprime;
+      m[i] = best;
+      sse = __dadd_rn(sse, __dmul_rn(W[i], best_d));
+      continue;
+    }
+    if (mode == PTS_NAIVE) {  // assign_naive (kmeans.hpp:89-102): strict '<' from c_0
       double best_d = dist2_rn(x0, x1, x2, cs[0], cs[1], cs[2]);
       int best = 0;
       for (int t = 1; t < k; ++t) {

@@ -97,8 +97,6 @@ struct LoopParams {
   int traj_cap;
   unsigned long long* timeline;  // optional: per-iteration globaltimer stamps (8 per iteration)
   int moments_only;  // sharded step: stop after assign + flush (global sums = this shard's moments)
-  int naive;         // run_km_full (kmeans.hpp:409-426): exhaustive assign, no center tables
-  int fkm_kprime;    // run_fkm (fast_variants.hpp:20-81): search the k' nearest centers of the previous one
   const uint8_t* cand;     // iteration 1: per 16^3 color cell, the centers that can be nearest (null: dense)
   // map epilogue (quantize path; null lut: none): k_map_tables + k_map_unique fused into the loop's tail
   int* map_sortedDr;
@@ -707,10 +705,7 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
   }
 }
 
-// Assign variants: sort-means (WSM), exhaustive (KM), first k' of the row (FKM).
-enum class Assign { SortMeans, Naive, Fkm };
 constexpr int DBG_NO_F32 = 1 << 17;   // debug flag: FP64 scans only (A/B of the FP32 screening)
-constexpr int DBG_PART_HIST = 1 << 18;  // debug flag: large images through the partitioned histogram (part.cuh, A/B)
 
 // ---------------------------------------------------------------------------
 // FP32 screening of the sort-means scan (iterations >= 2), certified against
@@ -920,38 +915,17 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
   return j;
 }
 
-// One point's scan in FP64 with the reference's exact semantics
-// (kmeans.hpp:211-236; KM: assign_naive :83-106; FKM: fast_variants.hpp:42-52).
-// Out of line: it is the rare path of WSM (scan_f32 not certified) and keeps
-// its registers out of the FP32 loop. Returns J | best << 12 | active << 24.
-template <Assign Mode>
+// One point's sort-means scan in FP64 with the reference's exact semantics
+// (kmeans.hpp:211-236). Out of line: it is the rare path (scan_f32 not
+// certified, or centers outside its range) and keeps its registers out of the
+// FP32 loop. Returns J | best << 12 | active << 24.
 __device__ __noinline__ int scan_fp64(const LoopSmem& S, const double* __restrict__ rd, const uint8_t* __restrict__ ro,
-                                      int k, int kp_, uint32_t key, int p, int debug_flags) {
-  constexpr bool kDeep = Mode == Assign::SortMeans;
+                                      int k, uint32_t key, int p, int debug_flags) {
   int best = p, J = 1, active = 0;
-  const uint32_t keyq = key;
-  const double x0 = u8_to_double(key_r(keyq)), x1 = u8_to_double(key_g(keyq)),
-               x2 = u8_to_double(key_b(keyq));
+  const double x0 = u8_to_double(key_r(key)), x1 = u8_to_double(key_g(key)), x2 = u8_to_double(key_b(key));
   double mind = dist2_rn(x0, x1, x2, S.cx[p], S.cy[p], S.cz[p]);  // prev
   const double bound = 4.0 * mind;
   bool deep = false;
-  if constexpr (Mode == Assign::Fkm) {
-    // run_fkm (fast_variants.hpp:42-52): lexicographic (d, index) minimum
-    // over order[p][0..k') - self first, then its nearest centers
-    const int kp = kp_;
-    for (int j = 1; j < kp; ++j) {
-      const int t = ro[j];
-      lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
-    }
-    J = 0;  // dist_evals are P*k' per iteration, set by the host
-  } else if constexpr (Mode == Assign::Naive) {
-    // assign_naive (kmeans.hpp:83-106): every center, strict < from c_0,
-    // i.e. the lexicographic (d, index) minimum over all k (the start
-    // from the previous label does not change that minimum).
-    for (int t = 0; t < k; ++t)
-      lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t], S.cy[t], S.cz[t]), t);
-    J = 0;  // dist_evals are P*k per iteration, set by the host
-  } else
   // the reference's scan (kmeans.hpp:217-231), two entries per step
   if (k > 1 && rd[1] < bound && !(debug_flags & 1)) {
     active = 1;
@@ -968,12 +942,12 @@ __device__ __noinline__ int scan_fp64(const LoopSmem& S, const double* __restric
       lex_min(mind, best, dist2_rn(x0, x1, x2, S.cx[t1], S.cy[t1], S.cz[t1]), t1);
       ++j;
       if (j >= k) break;
-      if (kDeep && j >= DEEP_J) {  // deep scan: find the break index, then evaluate without checks
+      if (j >= DEEP_J) {  // deep scan: find the break index, then evaluate without checks
         deep = true;
         break;
       }
     }
-    if (kDeep && deep) {
+    if (deep) {
       // J = min{i in [j, k) : rd[i] >= bound}, or k: the row is sorted, so
       // DEEP_P independent probes per round cut [lo, hi] to 1/(DEEP_P+1)
       int a = j, b = k;
@@ -1006,7 +980,7 @@ __device__ __noinline__ int scan_fp64(const LoopSmem& S, const double* __restric
   return J | (best << 12) | (active << 24);
 }
 
-template <Assign Mode, int PPT, int X, bool R>
+template <int PPT, int X, bool R>
 __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
@@ -1027,8 +1001,8 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   const uint32_t G = pG, W = blockDim.x >> 5, w = threadIdx.x >> 5;
   const uint32_t nch = (hi - lo + 31u) >> 5;
   // small sample sets: chunk costs recorded for the longest-first order
-  constexpr bool kSched = Mode == Assign::SortMeans && PPT == 1;
-  constexpr bool kDeep = Mode == Assign::SortMeans;
+  constexpr bool kSched = PPT == 1;
+  constexpr bool kDeep = true;
   const uint32_t my_ch = nch > pb ? (nch - 1u - pb) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const float4* __restrict__ rq32 = reinterpret_cast<const float4*>(L.st->rowD32);
@@ -1036,7 +1010,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   const float4* c4 = loop_c4();
   const uint8_t* __restrict__ go = L.st->order;
   // FP32 screening (scan_f32): sort-means scans whose centers all satisfy |c| < 256
-  const bool use32 = Mode == Assign::SortMeans && S.f32ok;
+  const bool use32 = S.f32ok;
   const uint32_t* __restrict__ keys = L.keys;
   const uint32_t* __restrict__ counts = L.counts;
   uint8_t* __restrict__ labels = L.labels;
@@ -1081,12 +1055,11 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       const uint8_t* ro = go + p * KMAX;
       int best = p;
       int J = 0;
-      if constexpr (Mode == Assign::SortMeans)
-        if (use32)
+      if (use32)
           J = scan_f32<kDeep, DEEP_J, DEEP_P>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4), k, key[q], p, best,
                                               n_active);
-      if (J == 0) {  // FP64 (KM / FKM, uncertified FP32 screens, or screening off): rare for WSM
-        const int r = scan_fp64<Mode>(S, gd + p * KMAX, ro, k, L.fkm_kprime, key[q], p, L.debug_flags);
+      if (J == 0) {  // FP64: uncertified FP32 screens, or screening off (rare)
+        const int r = scan_fp64(S, gd + p * KMAX, ro, k, key[q], p, L.debug_flags);
         J = r & 0xFFF;
         best = (r >> 12) & 0xFF;
 #if CQB_DIAG_FALLBACK  // diagnostics build: the timeline's "active" count = FP64 fallbacks of scan_f32
@@ -1457,9 +1430,8 @@ __device__ __forceinline__ unsigned long long loop_barrier(LoopSmem& S, unsigned
 // moments exchanged over NVLink inside the loop; 2 = the same exchange among
 // L.xw block groups of this launch (single-GPU emulation of the ranks).
 // R: resident samples (ResSamples; small sample sets, X == 0 only).
-template <Assign Mode, int PPT, int X, bool R = false>
+template <int PPT, int X, bool R = false>
 __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopParams L) {
-  constexpr bool kNaive = Mode == Assign::Naive, kFkm = Mode == Assign::Fkm;
   __shared__ LoopSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
   cg::grid_group grid = cg::this_grid();
@@ -1509,8 +1481,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     S.accp[t] = make_uint2(0u, 0u);
     S.accm[t] = make_uint2(0u, 0u);
   }
-  if (Mode == Assign::SortMeans)
-    for (int j = tid; j < SCHED_MAX; j += blockDim.x) {  // identity order until costs are known
+  for (int j = tid; j < SCHED_MAX; j += blockDim.x) {  // identity order until costs are known
       chunk_sched().order[j] = (uint16_t)j;
       chunk_sched().cost[j] = 0;
     }
@@ -1543,17 +1514,17 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       }
     }
   }
-  if (Mode == Assign::SortMeans)  // scan_f32 rows: +inf after the k - 1 entries
-    for (int p = blockIdx.x; p < k; p += gridDim.x)
+  // scan_f32 rows: +inf after the k - 1 entries
+  for (int p = blockIdx.x; p < k; p += gridDim.x)
       for (int i = k - 1 + tid; i < ROW32; i += blockDim.x) {
         st->rowD32[p * ROW32 + i] = F32_INF;
         st->rowO[p * ROW32 + i] = 0;
       }
-  if (!kNaive) tables_all(S, st, k, false);
+  tables_all(S, st, k, false);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
   // (sharded over processes: counted by rank 0 only)
-  unsigned long long pair_evals = (kNaive || kFkm || (X == 1 && L.xrank != 0))
+  unsigned long long pair_evals = (X == 1 && L.xrank != 0)
                                       ? 0ull
                                       : (unsigned long long)k * (unsigned long long)(k - 1) / 2;
   if (CQB_LOOP_BARRIER && blockIdx.x == 0 && tid == 0) st->bar = 0ull;  // before the prologue barrier
@@ -1574,12 +1545,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       }
       __syncthreads();
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
-      if constexpr (Mode == Assign::SortMeans) {
-        assign_dense_first<X>(S, L, lo, hi, evals);
-      } else {  // KM / FKM: the host accounts P*k for iteration 1
-        unsigned long long ev_dense = 0;
-        assign_dense_first<X>(S, L, lo, hi, ev_dense);
-      }
+      assign_dense_first<X>(S, L, lo, hi, evals);
     } else {
       // no block barrier here: the grid barrier that ended the previous
       // iteration already ordered everything this assign reads (S.wq was
@@ -1587,7 +1553,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means<Mode, PPT, X, R>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
+      assign_sort_means<PPT, X, R>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -1605,7 +1571,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     // next iteration's longest-first chunk order (this block's chunks are
     // done); small sample sets only (latency-bound), re-sorted at iterations
     // 2, 4, 8, ... (costs drift slowly; the sort is not free)
-    if (Mode == Assign::SortMeans && PPT == 1 && it >= 2 && (it & (it - 1)) == 0) {
+    if (PPT == 1 && it >= 2 && (it & (it - 1)) == 0) {
       const unsigned long long nn = hi - lo, nch = (nn + 31) >> 5;
       const uint32_t pb = part_block<X>(S), pG = part_size<X>(S);
       const uint32_t my_ch = nch > pb ? (uint32_t)((nch - 1 - pb) / pG + 1) : 0u;
@@ -1769,11 +1735,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
         // pair evaluations of the incremental table update (kmeans.hpp:137-155)
         if (!stop) {
           const unsigned long long still = (unsigned long long)(k - moved);
-          // FKM builds its first tables for iteration 2 (fast_variants.hpp:42): all pairs
-          if (kFkm && it == 1)
-            pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2;
-          else if (!kNaive)
-            pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
+          pair_evals += (unsigned long long)k * (unsigned long long)(k - 1) / 2 - (still ? still * (still - 1) / 2 : 0ull);
         }
       }
       if (L.traj && it <= L.traj_cap)
@@ -1809,7 +1771,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
     if (tid == 0) S.stamp = (L.block_times && it == L.stamp_iter) ? L.block_times : nullptr;
-    if (!kNaive) tables_all(S, st, k, true);  // wasted work on the final iteration only
+    tables_all(S, st, k, true);  // wasted work on the final iteration only
     if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
     BLOCK_STAMP(5);
     if (CQB_LOOP_BARRIER) {
