@@ -24,6 +24,9 @@ using namespace cqb;
 
 namespace {
 
+constexpr int XFER_CHUNKS = 8;
+constexpr int DBG_NO_XFER_OVERLAP = 1 << 19;  // debug flag: one H2D / D2H copy each, K1 after the H2D
+
 struct Staging {  // pinned host mirror of the per-call results
   double centers[3 * KMAX];
   unsigned long long evals, mse_err, n_unique;
@@ -47,6 +50,14 @@ struct cqb_ctx {
   int grid_limit = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  // cqb_quantize_ex on large images: host<->device copies in XFER_CHUNKS
+  // slices on a second stream, overlapped with K1 (H2D) and the map (D2H)
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t xev[2 * XFER_CHUNKS + 1] = {};
+  bool k1_done = false;               // set only while cqb_quantize_ex enqueues: bins already counted
+  uint8_t* h_index_dst = nullptr;     // set only while cqb_quantize_ex enqueues: chunked D2H targets
+  uint8_t* h_rgb_dst = nullptr;
+  uint8_t* h_err_dst = nullptr;
 
   uint2* bins = nullptr;  // 2^24 x {count, ~first}; all-zero between calls
   uint8_t* lut = nullptr; // 2^24 key -> palette index
@@ -396,7 +407,8 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   // dense ones by scanning all 128 MiB (k_bins_compact), whose K1 runs in
   // 4 Morton slices so each pass's atomics stay in L2.
   const bool sparse = sparse_path(ctx, P);
-  const int passes = fused ? 0 : (P >= (4u << 20) ? 4 : 1);  // fused: K1 runs inside k_prep_small
+  // fused: K1 runs inside k_prep_small; k1_done: cqb_quantize_ex ran it per H2D slice
+  const int passes = fused || ctx->k1_done ? 0 : (P >= (4u << 20) ? 4 : 1);
   for (int q = 0; q < passes; ++q) {
     const uint32_t span = (1u << 24) / passes;
     k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(
@@ -664,13 +676,38 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   uint8_t* d_err_out = ctx->err_target;
   // sharded: this rank maps its pixel range only (offsets are multiples of 16 pixels: aligned vectors)
   const uint64_t plo = ctx->xsharded ? ctx->px_lo : 0, pn = ctx->xsharded ? ctx->px_hi - ctx->px_lo : P;
+  const bool d2h = ctx->h_index_dst || ctx->h_rgb_dst || ctx->h_err_dst;
   if ((d_index || d_rgb_out || d_err_out) && pn > 0) {
-    const uint64_t nchunk = (pn + PX_PER_THREAD - 1) / PX_PER_THREAD;
-    const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-    k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(
-        d_img + 3 * plo, pn, ctx->lut, ctx->d_palkey, k, d_index ? d_index + plo : nullptr,
-        d_rgb_out ? d_rgb_out + 3 * plo : nullptr, d_err_out ? d_err_out + 3 * plo : nullptr);
-    CKL();
+    // with host targets (cqb_quantize_ex): XFER_CHUNKS map launches, each
+    // slice's D2H copies on ctx->xfer overlapping the next slice's map
+    const uint64_t q16 = (pn + 15) / 16;
+    const int nch = d2h ? XFER_CHUNKS : 1;
+    for (int c = 0; c < nch; ++c) {
+      const uint64_t a = plo + std::min(pn, q16 * c / nch * 16), b = plo + std::min(pn, q16 * (c + 1) / nch * 16);
+      if (b <= a) continue;
+      const uint64_t nchunk = (b - a + PX_PER_THREAD - 1) / PX_PER_THREAD;
+      const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+      k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(
+          d_img + 3 * a, b - a, ctx->lut, ctx->d_palkey, k, d_index ? d_index + a : nullptr,
+          d_rgb_out ? d_rgb_out + 3 * a : nullptr, d_err_out ? d_err_out + 3 * a : nullptr);
+      CKL();
+      if (d2h) {
+        CK(cudaEventRecord(ctx->xev[XFER_CHUNKS + c], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->xfer, ctx->xev[XFER_CHUNKS + c], 0));
+        if (ctx->h_index_dst && d_index)
+          CK(cudaMemcpyAsync(ctx->h_index_dst + a, d_index + a, b - a, cudaMemcpyDeviceToHost, ctx->xfer));
+        if (ctx->h_rgb_dst && d_rgb_out)
+          CK(cudaMemcpyAsync(ctx->h_rgb_dst + 3 * a, d_rgb_out + 3 * a, 3 * (b - a), cudaMemcpyDeviceToHost,
+                             ctx->xfer));
+        if (ctx->h_err_dst && d_err_out)
+          CK(cudaMemcpyAsync(ctx->h_err_dst + 3 * a, d_err_out + 3 * a, 3 * (b - a), cudaMemcpyDeviceToHost,
+                             ctx->xfer));
+      }
+    }
+    if (d2h) {  // the caller's stream synchronisation covers the copies
+      CK(cudaEventRecord(ctx->xev[2 * XFER_CHUNKS], ctx->xfer));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->xev[2 * XFER_CHUNKS], 0));
+    }
   }
   PROF(7);
   CK(cudaEventRecord(ctx->ev[2], ctx->stream));
@@ -678,6 +715,14 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   ctx->last_k = k;
   ctx->last_P = P;
   ctx->last_hist_cap = term_iters(term);
+  return CQB_OK;
+}
+
+// The copy stream and its events (cqb_quantize_ex on large images).
+int ensure_xfer(cqb_ctx* ctx) {
+  if (ctx->xfer) return CQB_OK;
+  CK(cudaStreamCreateWithFlags(&ctx->xfer, cudaStreamNonBlocking));
+  for (auto& e : ctx->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return CQB_OK;
 }
 
@@ -812,6 +857,10 @@ int cqb_destroy(cqb_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pev)
     if (e) cudaEventDestroy(e);
+  if (ctx->xfer) cudaStreamSynchronize(ctx->xfer);
+  for (auto& e : ctx->xev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->xfer) cudaStreamDestroy(ctx->xfer);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   for (cqb_ctx* l : ctx->lanes) cqb_destroy(l);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
@@ -1159,7 +1208,31 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   if (P >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
   CK(cudaSetDevice(ctx->device));
   TRY(ensure_pixels(ctx, P));
-  CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  // Large images: the H2D copy in XFER_CHUNKS slices on ctx->xfer, K1 counting
+  // each slice as it lands (one pass over the whole bin table per slice), and
+  // the outputs copied back per map slice (enqueue_quantize); small ones use
+  // one copy and the fused prep kernel.
+  const bool overlap = !sparse_path(ctx, P) && !(ctx->debug_flags & DBG_NO_XFER_OVERLAP);
+  if (overlap) {
+    TRY(ensure_xfer(ctx));
+    CK(cudaEventRecord(ctx->xev[0], ctx->stream));  // d_img is free once the stream's earlier work is done
+    CK(cudaStreamWaitEvent(ctx->xfer, ctx->xev[0], 0));
+    const uint64_t q16 = (P + 15) / 16;
+    for (int c = 0; c < XFER_CHUNKS; ++c) {
+      const uint64_t a = std::min(P, q16 * c / XFER_CHUNKS * 16), b = std::min(P, q16 * (c + 1) / XFER_CHUNKS * 16);
+      if (b <= a) continue;
+      CK(cudaMemcpyAsync(ctx->d_img + 3 * a, rgb + 3 * a, 3 * (b - a), cudaMemcpyHostToDevice, ctx->xfer));
+      CK(cudaEventRecord(ctx->xev[c], ctx->xfer));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->xev[c], 0));
+      const uint64_t nchunk = (b - a + PX_PER_THREAD - 1) / PX_PER_THREAD;
+      const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+      k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(ctx->d_img + 3 * a, b - a, ctx->bins, 0u,
+                                                                       1u << 24, nullptr, (uint32_t)a);
+      CKL();
+    }
+  } else {
+    CK(cudaMemcpyAsync(ctx->d_img, rgb, 3 * P, cudaMemcpyHostToDevice, ctx->stream));
+  }
   // Pinned (mapped) host outputs are written by the map kernel directly over
   // PCIe (zero-copy), overlapping the transfer with the kernel; pageable ones
   // get the device buffers + one D2H copy each.
@@ -1174,14 +1247,25 @@ int cqb_quantize_ex(cqb_ctx* ctx, const uint8_t* rgb, int width, int height, int
   int ndraws = k + 64;
   for (int attempt = 0; attempt < 4; ++attempt) {
     ctx->err_target = error_out ? (ze ? ze : ctx->d_err) : nullptr;
+    // a retry re-counts the histogram from the resident raster (K2b re-zeroed the bins)
+    ctx->k1_done = overlap && attempt == 0;
+    if (overlap) {
+      ctx->h_index_dst = index_out;
+      ctx->h_rgb_dst = rgb_out;
+      ctx->h_err_dst = error_out;
+    }
     const int rc = enqueue_quantize(ctx, ctx->d_img, P, k, term, seed,
                                     index_out ? (zi ? zi : ctx->d_index) : nullptr,
                                     rgb_out ? (zr ? zr : ctx->d_rgb) : nullptr, ndraws);
     ctx->err_target = nullptr;
+    ctx->k1_done = false;
+    ctx->h_index_dst = ctx->h_rgb_dst = ctx->h_err_dst = nullptr;
     TRY(rc);
-    if (index_out && !zi) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
-    if (rgb_out && !zr) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
-    if (error_out && !ze) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!overlap) {
+      if (index_out && !zi) CK(cudaMemcpyAsync(index_out, ctx->d_index, P, cudaMemcpyDeviceToHost, ctx->stream));
+      if (rgb_out && !zr) CK(cudaMemcpyAsync(rgb_out, ctx->d_rgb, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+      if (error_out && !ze) CK(cudaMemcpyAsync(error_out, ctx->d_err, 3 * P, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->h_stage->status != ST_DRAWS_EXHAUSTED) break;
     ndraws *= 4;

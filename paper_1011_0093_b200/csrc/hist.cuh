@@ -35,14 +35,17 @@ __device__ __forceinline__ void bin_add(uint2* __restrict__ bins, uint32_t key, 
 // 126 MB L2 instead of re-fetching sectors from HBM.
 // With `occ`, K1 also marks every touched bin in a 2^24-bit occupancy map
 // (2 MiB), so small images can compact the table without scanning 128 MiB.
+// px0: index of img's first pixel in the whole image (K1 over one slice of
+// an image whose H2D copy is still in flight, cqb_quantize_ex).
 __device__ __forceinline__ void hist_count_chunks(const uint8_t* __restrict__ img, uint64_t P,
                                                   uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi,
-                                                  uint32_t* __restrict__ occ, uint64_t c0, uint64_t cstride) {
+                                                  uint32_t* __restrict__ occ, uint64_t c0, uint64_t cstride,
+                                                  uint32_t px0 = 0) {
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
   for (uint64_t c = c0; c < nchunk; c += cstride) {
     uint32_t keys[PX_PER_THREAD];
     const int n = load_chunk_keys(img, P, c, keys);
-    const uint32_t base = (uint32_t)(c * PX_PER_THREAD);
+    const uint32_t base = px0 + (uint32_t)(c * PX_PER_THREAD);
     uint32_t cur = keys[0], run = 1, start = base;
 #pragma unroll
     for (int s = 1; s < PX_PER_THREAD; ++s) {
@@ -63,9 +66,9 @@ __device__ __forceinline__ void hist_count_chunks(const uint8_t* __restrict__ im
 
 __global__ void __launch_bounds__(HIST_THREADS) k_hist_count(const uint8_t* __restrict__ img, uint64_t P,
                                                               uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi,
-                                                              uint32_t* __restrict__ occ) {
+                                                              uint32_t* __restrict__ occ, uint32_t px0 = 0) {
   hist_count_chunks(img, P, bins, mlo, mhi, occ, (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x,
-                    (uint64_t)gridDim.x * HIST_THREADS);
+                    (uint64_t)gridDim.x * HIST_THREADS, px0);
 }
 
 // Decoupled look-back state word: flag in the high 32 bits, value low.

@@ -516,3 +516,38 @@ def test_quantize_pinned_outputs_zero_copy(case, k, images, port):
         assert list(q.report.sse_history) == list(ref.report.sse_history)
     mine, my_idx = port.map_pixels(img, q.palette)
     np.testing.assert_array_equal(pin_out, mine)
+
+
+def test_quantize_overlapped_transfers(port):
+    """Large images through cqb_quantize_ex: the H2D copy in 8 slices with K1
+    counting each slice as it lands, and the outputs copied back per map slice
+    on a second stream. Ragged size (not a multiple of 16 x 8 pixels), pinned
+    and pageable outputs, error image; equal to the serial path (debug flag
+    1 << 19) and to the oracle."""
+    import torch
+
+    img = gmm_image(1531, 1373, 64, 77)  # 2.1M pixels: the dense path
+    h, w = img.shape[:2]
+    term = api.Termination.fixed(4)
+    ctx = api.context(0)
+    ctx.lib.cqb_set_debug(ctx.h, 1 << 19)
+    try:
+        ser = api.quantize(img, 64, term, seed=3, error=True)
+    finally:
+        ctx.lib.cqb_set_debug(ctx.h, 0)
+    pin_img = torch.from_numpy(img.reshape(-1).copy()).pin_memory().numpy().reshape(img.shape)
+    pin_out = torch.empty(h * w * 3, dtype=torch.uint8).pin_memory().numpy().reshape(h, w, 3)
+    for src, out in ((img, None), (pin_img, pin_out)):
+        q = api.quantize(src, 64, term, seed=3, error=True, out_mapped=out)
+        np.testing.assert_array_equal(q.palette, ser.palette)
+        np.testing.assert_array_equal(q.index_map, ser.index_map)
+        np.testing.assert_array_equal(q.mapped, ser.mapped)
+        np.testing.assert_array_equal(q.error, ser.error)
+        assert q.report.dist_evals == ser.report.dist_evals and q.report.mse == ser.report.mse
+    hh = port.build_histogram(img)
+    o = port.run_wsm(hh.keys, hh.counts, h * w, 64, mode=0, max_iters=4, seed=3)
+    assert q.report.n_unique == len(hh.keys) and q.report.dist_evals == o.dist_evals
+    np.testing.assert_allclose(q.palette, o.centers, rtol=CENTER_RTOL)
+    mine, my_idx = port.map_pixels(img, q.palette)
+    np.testing.assert_array_equal(q.index_map, my_idx)
+    np.testing.assert_array_equal(q.mapped, mine)
