@@ -1409,17 +1409,19 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
 // loads until every block has arrived; the other threads wait at bar.sync.
 // Same ordering as cooperative_groups' grid.sync, with a payload: block 0
 // adds its stop decision to the high half, so no block needs a separate L2
-// round trip to learn whether the loop ends.
+// round trip to learn whether the loop ends. wait = false: arrive only (the
+// block's writes are published; it does not wait for the others).
 __device__ __forceinline__ unsigned long long loop_barrier(LoopSmem& S, unsigned long long* bar, unsigned int target,
-                                                           unsigned long long add) {
+                                                           unsigned long long add, bool wait = true) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(bar), "l"(add) : "memory");
-    unsigned long long v;
-    do {
+    unsigned long long v = 0;
+    while (wait) {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-    } while ((unsigned int)v < target);
+      if ((unsigned int)v >= target) break;
+    }
     S.barv = v;
   }
   __syncthreads();
@@ -1581,7 +1583,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     BLOCK_STAMP(2);
     if (CQB_LOOP_BARRIER) {
       bar_target += gridDim.x;
-      loop_barrier(S, &st->bar, bar_target, 1ull);
+      // sharded: only the sending blocks need every local flush; the others
+      // read the totals from the exchange (each rank sends after its own
+      // barrier), so they arrive without waiting
+      const bool waits = X == 0 || part_block<X>(S) < (unsigned)L.xw;
+      loop_barrier(S, &st->bar, bar_target, 1ull, waits);
     } else {
       grid.sync();
     }

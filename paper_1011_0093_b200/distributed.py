@@ -279,6 +279,16 @@ class PeerShardedQuantizer:
         return centers.reshape(k, 3), rep, hist[: rep.iterations].copy()
 
 
+def pixel_range(n_pixels: int, world: int, rank: int) -> tuple[int, int]:
+    """The raster slice rank ``rank`` maps in cqb_quantize_sharded (capi.cu):
+    contiguous, 16-pixel aligned starts (16-B vector stores), the last rank
+    takes the tail."""
+    q = (n_pixels + 15) // 16
+    lo = min(n_pixels, q * rank // world * 16)
+    hi = n_pixels if rank == world - 1 else min(n_pixels, q * (rank + 1) // world * 16)
+    return lo, hi
+
+
 def exchange_handles(handle: bytes, group=None) -> list[bytes]:
     """All-gather of the ranks' IPC handles, in rank order (host plumbing)."""
     import torch.distributed as dist

@@ -256,6 +256,123 @@ def test_gloo_world2_ipc_handles_in_rank_order():
         assert hs == [bytes([0]) * 64, bytes([1]) * 64]
 
 
+class _FakeXchLib:
+    """Records PeerShardedQuantizer's C-ABI calls (test infrastructure): the
+    window call writes a rank-tagged handle, the open call keeps what it was
+    given, the sharded quantize returns the rank's pixel range."""
+
+    def __init__(self):
+        self.calls = []
+
+    def cqb_xch_window(self, h, world, rank, buf):
+        for i in range(len(buf)):
+            buf[i] = 0x40 + rank
+        self.calls.append(("window", world, rank))
+        return 0
+
+    def cqb_xch_open(self, h, buf):
+        self.calls.append(("open", bytes(buf.raw)))
+        return 0
+
+    def cqb_quantize_sharded(self, h, d_rgb, n, k, term, seed, d_index, d_rgb_out, rng):
+        from paper_1011_0093_b200.distributed import pixel_range
+
+        world, rank = self.calls[0][1], self.calls[0][2]
+        lo, hi = pixel_range(n, world, rank)
+        rng[0], rng[1] = lo, hi
+        t = term._obj
+        self.calls.append(("quantize", d_rgb, n, k, (t.mode, t.max_iters, t.epsilon, t.hard_cap), seed, d_index, d_rgb_out))
+        return 0
+
+    def cqb_fetch_results(self, h, centers, hist, cap, rep):
+        k = self._k
+        for i in range(3 * k):
+            centers[i] = float(i)
+        for i in range(cap):
+            hist[i] = 1.0 / (i + 1)
+        rep._obj.iterations = 3
+        rep._obj.dist_evals = 1000
+        self.calls.append(("fetch", cap))
+        return 0
+
+
+class _FakeCtx:
+    def __init__(self):
+        self.h = 1234
+        self.lib = _FakeXchLib()
+
+    def check(self, rc):
+        assert rc == 0
+
+
+def _peer_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200 import api
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = _FakeCtx()
+        q = PeerShardedQuantizer(ctx=ctx)
+        term = api.Termination.convergent(1e-4, 100)
+        rng = q.enqueue(0xD000 + rank, 1000003, 256, term, seed=7, d_index=0xE000, d_rgb_out=0xF000)
+        ctx.lib._k = 256
+        centers, rep, hist = q.fetch()
+        out_q.put((rank, q.world, q.rank, rng, ctx.lib.calls, centers.shape, rep.iterations, list(hist)))
+    except Exception as e:  # surface the failure instead of a queue timeout
+        out_q.put((rank, "error", repr(e), None, None, None, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_peer_quantizer_setup_path():
+    """The production setup path of the in-kernel sharded loop on CPU:
+    PeerShardedQuantizer over a world-2 gloo group opens its window with the
+    group's world/rank, all-gathers the IPC handles and passes them to
+    cqb_xch_open in rank order, forwards the launch arguments unchanged, and
+    the ranks' pixel ranges tile the raster (16-pixel aligned starts)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=240) for _ in procs], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 1000003
+    handles = bytes([0x40]) * 64 + bytes([0x41]) * 64
+    ranges = []
+    for r, (rank, world, qrank, rng, calls, cshape, iters, hist) in enumerate(outs):
+        assert world != "error", qrank
+        assert (rank, world, qrank) == (r, 2, r)
+        assert calls[0] == ("window", 2, r)
+        assert calls[1] == ("open", handles)  # every rank: all handles, rank order
+        name, d_rgb, n_px, k, term, seed, d_index, d_out = calls[2]
+        assert (name, d_rgb, n_px, k, seed, d_index, d_out) == ("quantize", 0xD000 + r, n, 256, 7, 0xE000, 0xF000)
+        assert term[0] == 1 and term[3] == 100 and abs(term[2] - 1e-4) < 1e-12
+        assert calls[3] == ("fetch", 100)
+        assert cshape == (256, 3) and iters == 3 and len(hist) == 3
+        ranges.append(rng)
+    assert ranges[0][0] == 0 and ranges[0][1] == ranges[1][0] and ranges[1][1] == n
+    assert all(lo % 16 == 0 for lo, _ in ranges)
+
+
+def test_pixel_ranges_tile_the_raster():
+    from paper_1011_0093_b200.distributed import pixel_range
+
+    for n in (1, 15, 16, 17, 1000003, 4096 * 4096):
+        for w in (1, 2, 3, 8):
+            rs = [pixel_range(n, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert all(lo % 16 == 0 and lo <= hi for lo, hi in rs)
+
+
 def test_exchange_protocol_two_slots_suffice():
     """Model of the in-kernel exchange (wsm.cuh, XB_* windows): each rank
     writes exchange s into slot s&1 of every window, publishes flag = s, waits
