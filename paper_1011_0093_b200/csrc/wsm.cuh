@@ -1193,7 +1193,8 @@ __device__ __forceinline__ bool cand_better(double d, unsigned int i, double bd,
 //   u64 flag[src]   at XB_FLAG + 16*src  (own 128-B line per source)
 //   u64 seq         at XB_SEQ            (this rank's exchange counter, kept across launches)
 //   u64 payload[2][XMAX][5*KMAX] at XB_PAY  (slot parity = exchange number & 1)
-//   u8  labels[2^24] at byte XB_LAB_OFF  (the rank's sample labels; all-gathered at the end)
+//   u8  labels[2^24] at byte XB_LAB_OFF  (the rank's sample labels during the loop; after the
+//                                         map epilogue, every rank's final palette indices)
 // Exchange number s: every source writes its payload into slot s&1 of every
 // rank's window with plain stores, then (one thread, after bar.sync) a
 // sys-scope acq_rel fence and a relaxed store of s into flag[source]; a
@@ -1827,15 +1828,6 @@ template <int X>
 __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
                              unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs) {
   const int k = L.k, tid = threadIdx.x;
-  if constexpr (X == 1) {  // all-gather of the labels: this rank's range into every peer's window
-    const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
-    for (int r = 0; r < L.xw; ++r) {
-      if (r == part) continue;
-      uint8_t* dst = reinterpret_cast<uint8_t*>(L.xbox[r]) + XB_LAB_OFF;
-      for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + tid; i < hi; i += T)
-        dst[i] = L.labels[i];
-    }
-  }
   const double* C = L.st->final_C;
   uint32_t* s_key = S.row0;        // rounded palette keys
   int* s_cc = S.empty_list;        // |R_t|^2
@@ -1877,16 +1869,17 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
     }
   }
   grid.sync();
-  if constexpr (X != 0) {  // every rank's labels are in place (emulated: shared array, the round is kept)
-    const unsigned long long s = ++xs;
-    const unsigned int pG = X == 2 ? gridDim.x / (unsigned)L.xw : gridDim.x;
-    if (tid == 0 && blockIdx.x % pG == 0)
-      for (int r = 0; r < L.xw; ++r) xch_signal(L.xbox[r], part, s);
-    xch_wait(L.xbox[part], L.xw, s, &L.st->status, L.xch_timeout_ns);
-  }
+  // Sharded: each rank (part) maps its own samples [lo, hi). X = 1 sends the
+  // palette indices into every rank's window (its label region, contiguous
+  // stores), exchanges the partial error sums, and every rank then fills its
+  // LUT for all samples from its window; X = 2 (one shared LUT) writes it
+  // directly.
+  const unsigned int pb = X == 2 ? part_block<X>(S) : blockIdx.x;
+  const unsigned int pG = X == 2 ? part_size<X>(S) : gridDim.x;
+  const unsigned long long a = X ? lo : 0ull, b = X ? hi : n;
   unsigned long long err = 0;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
+  for (unsigned long long i = a + (unsigned long long)pb * blockDim.x + tid; i < b;
+       i += (unsigned long long)pG * blockDim.x) {
     const uint32_t x = L.keys[i];
     const int xx = key_dot(x, x);
     const int p = X ? (int)__ldcg(&L.labels[i]) : (int)L.labels[i];
@@ -1904,7 +1897,11 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
         best = t;
       }
     }
-    L.map_lut[x] = (uint8_t)best;
+    if constexpr (X == 1) {
+      for (int r = 0; r < L.xw; ++r) (reinterpret_cast<uint8_t*>(L.xbox[r]) + XB_LAB_OFF)[i] = (uint8_t)best;
+    } else {
+      L.map_lut[x] = (uint8_t)best;
+    }
     err += (unsigned long long)L.counts[i] * (unsigned long long)mind;
   }
   err = warp_sum(err);
@@ -1915,6 +1912,29 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
     unsigned long long tot = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += S.red_u64[w];
     if (tot) atomicAdd(&L.st->mse_err, tot);
+  }
+  if constexpr (X != 0) {
+    grid.sync();  // this rank's indices and error partial are in place
+    const unsigned long long s = ++xs;
+    if (tid == 0 && blockIdx.x % pG == 0) {  // one sender per part
+      if (X == 1) {
+        const unsigned long long e = __ldcg(&L.st->mse_err);
+        for (int r = 0; r < L.xw; ++r) *xpay(L.xbox[r], s, part) = e;
+      }
+      for (int r = 0; r < L.xw; ++r) xch_signal(L.xbox[r], part, s);
+    }
+    xch_wait(L.xbox[part], L.xw, s, &L.st->status, L.xch_timeout_ns);
+    if constexpr (X == 1) {
+      if (blockIdx.x == 0 && tid == 0) {  // the world's error sum (every rank reports the same MSE)
+        unsigned long long e = 0;
+        for (int r = 0; r < L.xw; ++r) e += __ldcg(xpay(L.xbox[part], s, r));
+        L.st->mse_err = e;
+      }
+      const uint8_t* idx = reinterpret_cast<const uint8_t*>(L.xbox[part]) + XB_LAB_OFF;
+      for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;
+           i += (unsigned long long)gridDim.x * blockDim.x)
+        L.map_lut[L.keys[i]] = __ldcg(idx + i);
+    }
   }
 }
 
