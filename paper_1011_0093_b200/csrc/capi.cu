@@ -25,6 +25,7 @@ using namespace cqb;
 namespace {
 
 constexpr int XFER_CHUNKS = 8;
+constexpr int DBG_NO_COARSE = 1 << 21;  // debug flag: k_map_pixels with per-pixel LUT gathers only (A/B)
 constexpr int DBG_NO_XFER_OVERLAP = 1 << 19;  // debug flag: one H2D / D2H copy each, K1 after the H2D
 
 struct Staging {  // pinned host mirror of the per-call results
@@ -61,6 +62,9 @@ struct cqb_ctx {
 
   uint2* bins = nullptr;  // 2^24 x {count, ~first}; all-zero between calls
   uint8_t* lut = nullptr; // 2^24 key -> palette index
+  uint32_t* d_cellw = nullptr;   // coarse map table: per-cell words (map.cuh)
+  uint8_t* d_coarse = nullptr;   // its compact form (labels + MIXED bits)
+  bool coarse_built = false;     // set by launch_loop: the loop's epilogue wrote d_coarse for this call
 
   size_t cap_px = 0;
   uint8_t* d_img = nullptr;
@@ -510,11 +514,18 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   L.block_times = ctx->profiling ? ctx->d_block_times : nullptr;
   L.stamp_iter = ctx->stamp_iter;
   L.debug_flags = ctx->debug_flags;
+  ctx->coarse_built = false;
   if (ctx->fuse_map && !(ctx->debug_flags & 256)) {
     L.map_sortedDr = ctx->d_sortedDr;
     L.map_orderR = ctx->d_orderR;
     L.map_palkey = ctx->d_palkey;
     L.map_lut = ctx->lut;
+    // large images: the coarse map table for k_map_pixels_coarse
+    ctx->coarse_built = total >= OCC_MAX_PIXELS && !(ctx->debug_flags & DBG_NO_COARSE);
+    if (ctx->coarse_built) {
+      L.map_cellw = ctx->d_cellw;
+      L.map_coarse = ctx->d_coarse;
+    }
   }
   if (dense_first && !(ctx->debug_flags & 128)) {  // iteration 1 on per-cell candidate lists
     k_grid_cands<<<CAND_CELLS, KMAX, 0, ctx->stream>>>(ctx->st, k, ctx->d_cand, ctx->d_cand_n);
@@ -686,10 +697,17 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
       const uint64_t a = plo + std::min(pn, q16 * c / nch * 16), b = plo + std::min(pn, q16 * (c + 1) / nch * 16);
       if (b <= a) continue;
       const uint64_t nchunk = (b - a + PX_PER_THREAD - 1) / PX_PER_THREAD;
-      const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
-      k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(
-          d_img + 3 * a, b - a, ctx->lut, ctx->d_palkey, k, d_index ? d_index + a : nullptr,
-          d_rgb_out ? d_rgb_out + 3 * a : nullptr, d_err_out ? d_err_out + 3 * a : nullptr);
+      if (ctx->coarse_built && fused_map) {
+        const int g = (int)std::min<uint64_t>((nchunk + MAPC_THREADS - 1) / MAPC_THREADS, (uint64_t)ctx->num_sms);
+        k_map_pixels_coarse<<<std::max(g, 1), MAPC_THREADS, COARSE_BYTES, ctx->stream>>>(
+            d_img + 3 * a, b - a, ctx->lut, ctx->d_coarse, ctx->d_palkey, k, d_index ? d_index + a : nullptr,
+            d_rgb_out ? d_rgb_out + 3 * a : nullptr, d_err_out ? d_err_out + 3 * a : nullptr);
+      } else {
+        const int g = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+        k_map_pixels<<<std::max(g, 1), HIST_THREADS, 0, ctx->stream>>>(
+            d_img + 3 * a, b - a, ctx->lut, ctx->d_palkey, k, d_index ? d_index + a : nullptr,
+            d_rgb_out ? d_rgb_out + 3 * a : nullptr, d_err_out ? d_err_out + 3 * a : nullptr);
+      }
       CKL();
       if (d2h) {
         CK(cudaEventRecord(ctx->xev[XFER_CHUNKS + c], ctx->stream));
@@ -790,6 +808,10 @@ int cqb_create(int device, cqb_ctx** out) {
     ctx->prep_blocks = std::min(std::max(pb, 0), 1) * ctx->num_sms;
     CK(cudaMemset(ctx->d_occ, 0, sizeof(uint32_t) << 19));
     CK(cudaMalloc(&ctx->lut, (size_t)1 << 24));
+    CK(cudaMalloc(&ctx->d_cellw, sizeof(uint32_t) * COARSE_CELLS));
+    CK(cudaMalloc(&ctx->d_coarse, COARSE_BYTES));
+    CK(cudaFuncSetAttribute((const void*)k_map_pixels_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)COARSE_BYTES));
     CK(cudaMalloc(&ctx->bin_tile_state, sizeof(unsigned long long) * (N_BIN_TILES + 1)));
     CK(cudaMalloc(&ctx->st, sizeof(WsmState)));
     CK(cudaMemset(ctx->st, 0, sizeof(WsmState)));
@@ -831,7 +853,7 @@ int cqb_destroy(cqb_ctx* ctx) {
   if (!ctx) return CQB_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  void* dev[] = {ctx->bins, ctx->lut, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->d_err, ctx->tile_state,
+  void* dev[] = {ctx->bins, ctx->lut, ctx->d_cellw, ctx->d_coarse, ctx->d_img, ctx->d_img2, ctx->d_index, ctx->d_rgb, ctx->d_err, ctx->tile_state,
                  ctx->d_keys, ctx->d_counts, ctx->d_first, ctx->d_bitmap, ctx->d_occ, ctx->d_block_counts, ctx->d_units, ctx->d_wofs, ctx->d_cand, ctx->d_cand_n, ctx->d_bpre, ctx->d_labels, ctx->d_lab_rank, ctx->d_mkeys,
                  ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state, ctx->d_weights, ctx->d_n, ctx->st,
                  ctx->d_hist, ctx->d_timeline, ctx->d_block_times, ctx->d_mom, ctx->d_Cnew, ctx->d_scal,

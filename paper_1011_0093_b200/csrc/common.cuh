@@ -130,12 +130,20 @@ __device__ __forceinline__ uint32_t key_b(uint32_t k) { return k & 255u; }
 // u8x3 raster as packed keys. Full chunks use three 16-B read-only vector
 // loads (the raster base is 16-B aligned by contract); the tail chunk uses
 // byte loads. Returns the number of valid pixels.
+// kStream: read-once loads (evict-first), so the raster does not push other
+// L2-resident tables out.
+template <bool kStream = false>
 __device__ __forceinline__ int load_chunk_keys(const uint8_t* __restrict__ img, uint64_t P, uint64_t c,
                                                uint32_t (&keys)[PX_PER_THREAD]) {
   const uint64_t p0 = c * PX_PER_THREAD;
   if (p0 + PX_PER_THREAD <= P) {
     const uint4* src = reinterpret_cast<const uint4*>(img + p0 * 3);
-    const uint4 a = __ldg(src), b = __ldg(src + 1), d = __ldg(src + 2);
+    uint4 a, b, d;
+    if constexpr (kStream) {
+      a = __ldcs(src), b = __ldcs(src + 1), d = __ldcs(src + 2);
+    } else {
+      a = __ldg(src), b = __ldg(src + 1), d = __ldg(src + 2);
+    }
     const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
 #pragma unroll
     for (int s = 0; s < PX_PER_THREAD; ++s) {

@@ -138,6 +138,72 @@ __global__ void k_error_image(const uint8_t* __restrict__ a, const uint8_t* __re
   }
 }
 
+// Stores of one 16-pixel chunk starting at pixel p0 (n valid): u8 index map,
+// mapped RGB and error_image, 16-B vector stores for full chunks.
+__device__ __forceinline__ void map_store16(const uint8_t* __restrict__ img, uint64_t p0, int n,
+                                            const uint32_t (&idx)[PX_PER_THREAD], const uint32_t* s_pal,
+                                            uint8_t* __restrict__ out_index, uint8_t* __restrict__ out_rgb,
+                                            uint8_t* __restrict__ out_err) {
+  if (n == PX_PER_THREAD) {
+    if (out_index) {
+      uint4 v;
+      v.x = idx[0] | (idx[1] << 8) | (idx[2] << 16) | (idx[3] << 24);
+      v.y = idx[4] | (idx[5] << 8) | (idx[6] << 16) | (idx[7] << 24);
+      v.z = idx[8] | (idx[9] << 8) | (idx[10] << 16) | (idx[11] << 24);
+      v.w = idx[12] | (idx[13] << 8) | (idx[14] << 16) | (idx[15] << 24);
+      __stcs(reinterpret_cast<uint4*>(out_index + p0), v);
+    }
+    if (out_rgb || out_err) {
+      uint32_t pc[PX_PER_THREAD];
+#pragma unroll
+      for (int s = 0; s < PX_PER_THREAD; ++s) pc[s] = s_pal[idx[s]];
+      uint32_t w[12];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {  // 4 pixels -> 3 words
+        const uint32_t a = pc[4 * g], b = pc[4 * g + 1], cc = pc[4 * g + 2], d = pc[4 * g + 3];
+        w[3 * g + 0] = a | (b << 24);
+        w[3 * g + 1] = (b >> 8) | (cc << 16);
+        w[3 * g + 2] = (cc >> 16) | (d << 8);
+      }
+      if (out_rgb) {
+        uint4* dst = reinterpret_cast<uint4*>(out_rgb + p0 * 3);
+        __stcs(dst, make_uint4(w[0], w[1], w[2], w[3]));
+        __stcs(dst + 1, make_uint4(w[4], w[5], w[6], w[7]));
+        __stcs(dst + 2, make_uint4(w[8], w[9], w[10], w[11]));
+      }
+      if (out_err) {  // error_image (image_ops.hpp:55-71): 255 - min(255, 4|o - q|) per byte
+        const uint4* src = reinterpret_cast<const uint4*>(img + p0 * 3);
+        const uint4 a = __ldg(src), b = __ldg(src + 1), d = __ldg(src + 2);
+        const uint32_t o[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+        uint32_t e[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) e[i] = err_bytes(o[i], w[i]);
+        uint4* dst = reinterpret_cast<uint4*>(out_err + p0 * 3);
+        __stcs(dst, make_uint4(e[0], e[1], e[2], e[3]));
+        __stcs(dst + 1, make_uint4(e[4], e[5], e[6], e[7]));
+        __stcs(dst + 2, make_uint4(e[8], e[9], e[10], e[11]));
+      }
+    }
+  } else {
+    for (int s = 0; s < n; ++s) {
+      if (out_index) out_index[p0 + s] = (uint8_t)idx[s];
+      const uint32_t pc = s_pal[idx[s]];
+      if (out_rgb) {
+        out_rgb[3 * (p0 + s)] = (uint8_t)pc;
+        out_rgb[3 * (p0 + s) + 1] = (uint8_t)(pc >> 8);
+        out_rgb[3 * (p0 + s) + 2] = (uint8_t)(pc >> 16);
+      }
+      if (out_err) {
+        const uint32_t o = img[3 * (p0 + s)] | (img[3 * (p0 + s) + 1] << 8) | (img[3 * (p0 + s) + 2] << 16);
+        const uint32_t e = err_bytes(o, pc);
+        out_err[3 * (p0 + s)] = (uint8_t)e;
+        out_err[3 * (p0 + s) + 1] = (uint8_t)(e >> 8);
+        out_err[3 * (p0 + s) + 2] = (uint8_t)(e >> 16);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(HIST_THREADS) k_map_pixels(const uint8_t* __restrict__ img, uint64_t P,
                                                               const uint8_t* __restrict__ lut,
                                                               const uint32_t* __restrict__ pal_key, int k,
@@ -158,65 +224,96 @@ __global__ void __launch_bounds__(HIST_THREADS) k_map_pixels(const uint8_t* __re
     uint32_t idx[PX_PER_THREAD];
 #pragma unroll
     for (int s = 0; s < PX_PER_THREAD; ++s) idx[s] = s < n ? (uint32_t)__ldg(lut + keys[s]) : 0u;
-    const uint64_t p0 = c * PX_PER_THREAD;
-    if (n == PX_PER_THREAD) {
-      if (out_index) {
-        uint4 v;
-        v.x = idx[0] | (idx[1] << 8) | (idx[2] << 16) | (idx[3] << 24);
-        v.y = idx[4] | (idx[5] << 8) | (idx[6] << 16) | (idx[7] << 24);
-        v.z = idx[8] | (idx[9] << 8) | (idx[10] << 16) | (idx[11] << 24);
-        v.w = idx[12] | (idx[13] << 8) | (idx[14] << 16) | (idx[15] << 24);
-        *reinterpret_cast<uint4*>(out_index + p0) = v;
-      }
-      if (out_rgb || out_err) {
-        uint32_t pc[PX_PER_THREAD];
-#pragma unroll
-        for (int s = 0; s < PX_PER_THREAD; ++s) pc[s] = s_pal[idx[s]];
-        uint32_t w[12];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {  // 4 pixels -> 3 words
-          const uint32_t a = pc[4 * g], b = pc[4 * g + 1], cc = pc[4 * g + 2], d = pc[4 * g + 3];
-          w[3 * g + 0] = a | (b << 24);
-          w[3 * g + 1] = (b >> 8) | (cc << 16);
-          w[3 * g + 2] = (cc >> 16) | (d << 8);
-        }
-        if (out_rgb) {
-          uint4* dst = reinterpret_cast<uint4*>(out_rgb + p0 * 3);
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          dst[2] = make_uint4(w[8], w[9], w[10], w[11]);
-        }
-        if (out_err) {  // error_image (image_ops.hpp:55-71): 255 - min(255, 4|o - q|) per byte
-          const uint4* src = reinterpret_cast<const uint4*>(img + p0 * 3);
-          const uint4 a = __ldg(src), b = __ldg(src + 1), d = __ldg(src + 2);
-          const uint32_t o[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
-          uint32_t e[12];
-#pragma unroll
-          for (int i = 0; i < 12; ++i) e[i] = err_bytes(o[i], w[i]);
-          uint4* dst = reinterpret_cast<uint4*>(out_err + p0 * 3);
-          dst[0] = make_uint4(e[0], e[1], e[2], e[3]);
-          dst[1] = make_uint4(e[4], e[5], e[6], e[7]);
-          dst[2] = make_uint4(e[8], e[9], e[10], e[11]);
-        }
-      }
+    map_store16(img, c * PX_PER_THREAD, n, idx, s_pal, out_index, out_rgb, out_err);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coarse map table (large images). The LUT gather is one random 32-B L2
+// sector per pixel; on a 16 M-pixel image that is ~0.5 GB of L2 traffic,
+// and the L1 processes one distinct line per cycle. Most colors, however,
+// share their palette index with every other PRESENT color of their small
+// color cell: the cells are 4 x 4 x 8 colors ((r>>2, g>>2, b>>3), 2^17 cells,
+// each a Morton-aligned run of 128 codes, so its samples are contiguous),
+// and a Voronoi cell of a K = 256 palette is ~40 colors wide (cfg4: 69.5% of
+// the pixels fall in pure cells). The loop's map epilogue records, per cell,
+// the index all its samples map to or MIXED (warp segments of equal cells,
+// one CAS per segment: 0 -> index + 1, any other value -> MIXED); a
+// compaction pass turns the words into one byte per cell (128 KB), which
+// k_map_pixels_coarse holds in shared memory: a pixel of a pure cell reads
+// its index with one LDS, only pixels of MIXED cells gather from the LUT.
+// The byte 255 means "gather": MIXED and empty cells, and (K = 256) the pure
+// cells of index 255, whose LUT value is 255 anyway. The result is identical
+// to the per-pixel LUT gather: a pure cell's index IS the LUT value of every
+// color present in it.
+constexpr int COARSE_CELLS = 1 << 17;
+constexpr uint32_t COARSE_MIXED = 0x200u;
+constexpr size_t COARSE_BYTES = COARSE_CELLS;
+constexpr uint32_t COARSE_GATHER = 255u;
+constexpr int MAPC_THREADS = 1024;
+__host__ __device__ __forceinline__ uint32_t coarse_cell(uint32_t key) {
+  return (((key >> 18) & 63u) << 11) | (((key >> 10) & 63u) << 5) | ((key >> 3) & 31u);
+}
+
+// Records sample color x -> palette index `best` for its cell. Called by the
+// lanes in `am` (warp-converged, consecutive Morton samples).
+__device__ __forceinline__ void coarse_note(uint32_t* __restrict__ cellw, unsigned am, uint32_t x, int best) {
+  const uint32_t c = coarse_cell(x);
+  const unsigned mc = __match_any_sync(am, c);
+  const unsigned ml = __match_any_sync(am, (c << 8) | (uint32_t)best);
+  if ((int)(threadIdx.x & 31) == __ffs(mc) - 1) {
+    const uint32_t v = mc == ml ? (uint32_t)best + 1u : COARSE_MIXED;
+    if (v == COARSE_MIXED) {
+      atomicExch(&cellw[c], COARSE_MIXED);
     } else {
-      for (int s = 0; s < n; ++s) {
-        if (out_index) out_index[p0 + s] = (uint8_t)idx[s];
-        const uint32_t pc = s_pal[idx[s]];
-        if (out_rgb) {
-          out_rgb[3 * (p0 + s)] = (uint8_t)pc;
-          out_rgb[3 * (p0 + s) + 1] = (uint8_t)(pc >> 8);
-          out_rgb[3 * (p0 + s) + 2] = (uint8_t)(pc >> 16);
-        }
-        if (out_err) {
-          const uint32_t o = img[3 * (p0 + s)] | (img[3 * (p0 + s) + 1] << 8) | (img[3 * (p0 + s) + 2] << 16);
-          const uint32_t e = err_bytes(o, pc);
-          out_err[3 * (p0 + s)] = (uint8_t)e;
-          out_err[3 * (p0 + s) + 1] = (uint8_t)(e >> 8);
-          out_err[3 * (p0 + s) + 2] = (uint8_t)(e >> 16);
-        }
-      }
+      const uint32_t old = atomicCAS(&cellw[c], 0u, v);
+      if (old != 0u && old != v) atomicExch(&cellw[c], COARSE_MIXED);
     }
+  }
+}
+
+// Word table -> one byte per cell (grid-stride): the pure cells' index, or
+// COARSE_GATHER (MIXED or empty: no pixel reads an empty cell).
+__device__ __forceinline__ void coarse_compact(const uint32_t* __restrict__ cellw, uint8_t* __restrict__ coarse,
+                                               uint32_t gtid, uint32_t gthreads) {
+  for (uint32_t c = gtid; c < (uint32_t)COARSE_CELLS; c += gthreads) {
+    const uint32_t w = __ldcg(&cellw[c]);
+    coarse[c] = (w == 0u || w == COARSE_MIXED) ? (uint8_t)COARSE_GATHER : (uint8_t)(w - 1u);
+  }
+}
+
+// k_map_pixels with the coarse table in shared memory: one block of 1024
+// threads per SM; 128 KB table + palette.
+__global__ void __launch_bounds__(MAPC_THREADS, 1) k_map_pixels_coarse(
+    const uint8_t* __restrict__ img, uint64_t P, const uint8_t* __restrict__ lut, const uint8_t* __restrict__ coarse,
+    const uint32_t* __restrict__ pal_key, int k, uint8_t* __restrict__ out_index, uint8_t* __restrict__ out_rgb,
+    uint8_t* __restrict__ out_err) {
+  extern __shared__ __align__(16) unsigned char mapc_smem[];
+  __shared__ uint32_t s_pal[KMAX];
+  const uint8_t* s_lab = mapc_smem;
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    const uint32_t key = pal_key[t];
+    s_pal[t] = key_r(key) | (key_g(key) << 8) | (key_b(key) << 16);
+  }
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(coarse);
+    uint4* dst = reinterpret_cast<uint4*>(mapc_smem);
+    for (int i = threadIdx.x; i < (int)(COARSE_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  for (uint64_t c = (uint64_t)blockIdx.x * MAPC_THREADS + threadIdx.x; c < nchunk;
+       c += (uint64_t)gridDim.x * MAPC_THREADS) {
+    uint32_t keys[PX_PER_THREAD];
+    const int n = load_chunk_keys<true>(img, P, c, keys);
+    uint32_t idx[PX_PER_THREAD];
+#pragma unroll
+    for (int s = 0; s < PX_PER_THREAD; ++s) {
+      uint32_t v = s_lab[coarse_cell(keys[s])];
+      if (v == COARSE_GATHER && s < n) v = __ldg(lut + keys[s]);
+      idx[s] = v;
+    }
+    map_store16(img, c * PX_PER_THREAD, n, idx, s_pal, out_index, out_rgb, out_err);
   }
 }
 

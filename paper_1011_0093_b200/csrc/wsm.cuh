@@ -103,6 +103,8 @@ struct LoopParams {
   uint8_t* map_orderR;
   uint32_t* map_palkey;
   uint8_t* map_lut;
+  uint32_t* map_cellw;     // coarse map table (null: none): per-cell words, zeroed in the prologue
+  uint8_t* map_coarse;     // its compact form (labels + MIXED bits) for k_map_pixels_coarse
   const uint16_t* cand_n;  // per cell: count, or CAND_OVERFLOW
   int debug_flags;   // diagnostics only (tools/ablate.py): 1 = skip the candidate scan (results wrong)
   unsigned long long* block_times;  // optional: phase stamps of iteration stamp_iter [phase][block]
@@ -1517,6 +1519,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       }
     }
   }
+  if (L.map_cellw)  // the epilogue's coarse cells start empty (read only after the loop's barriers)
+    for (uint32_t c = blockIdx.x * blockDim.x + tid; c < (uint32_t)COARSE_CELLS; c += gridDim.x * blockDim.x)
+      L.map_cellw[c] = 0u;
   // scan_f32 rows: +inf after the k - 1 entries
   for (int p = blockIdx.x; p < k; p += gridDim.x)
       for (int i = k - 1 + tid; i < ROW32; i += blockDim.x) {
@@ -1878,31 +1883,44 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
   const unsigned int pG = X == 2 ? part_size<X>(S) : gridDim.x;
   const unsigned long long a = X ? lo : 0ull, b = X ? hi : n;
   unsigned long long err = 0;
-  for (unsigned long long i = a + (unsigned long long)pb * blockDim.x + tid; i < b;
-       i += (unsigned long long)pG * blockDim.x) {
-    const uint32_t x = L.keys[i];
-    const int xx = key_dot(x, x);
-    const int p = X ? (int)__ldcg(&L.labels[i]) : (int)L.labels[i];
-    const int prev = xx + s_cc[p] - 2 * key_dot(x, s_key[p]);
-    const int bound = 4 * prev;
-    int mind = prev, best = p;
-    const int* rowd = L.map_sortedDr + p * KMAX;
-    const uint8_t* rowo = L.map_orderR + p * KMAX;
-    for (int j = 1; j < k; ++j) {
-      if (rowd[j] > bound) break;
-      const int t = rowo[j];
-      const int d = xx + s_cc[t] - 2 * key_dot(x, s_key[t]);
-      if (d < mind || (d == mind && t < best)) {
-        mind = d;
-        best = t;
+  // whole warps per step (consecutive Morton samples per warp: the coarse table's cell segments)
+  const int lane = tid & 31;
+  for (unsigned long long base = a + (unsigned long long)pb * blockDim.x + (tid & ~31); base < b;
+       base += (unsigned long long)pG * blockDim.x) {
+    const unsigned long long i = base + lane;
+    const bool v = i < b;
+    uint32_t x = 0;
+    int best = 0;
+    if (v) {
+      x = L.keys[i];
+      const int xx = key_dot(x, x);
+      const int p = X ? (int)__ldcg(&L.labels[i]) : (int)L.labels[i];
+      const int prev = xx + s_cc[p] - 2 * key_dot(x, s_key[p]);
+      const int bound = 4 * prev;
+      int mind = prev;
+      best = p;
+      const int* rowd = L.map_sortedDr + p * KMAX;
+      const uint8_t* rowo = L.map_orderR + p * KMAX;
+      for (int j = 1; j < k; ++j) {
+        if (rowd[j] > bound) break;
+        const int t = rowo[j];
+        const int d = xx + s_cc[t] - 2 * key_dot(x, s_key[t]);
+        if (d < mind || (d == mind && t < best)) {
+          mind = d;
+          best = t;
+        }
       }
+      if constexpr (X == 1) {
+        for (int r = 0; r < L.xw; ++r) (reinterpret_cast<uint8_t*>(L.xbox[r]) + XB_LAB_OFF)[i] = (uint8_t)best;
+      } else {
+        L.map_lut[x] = (uint8_t)best;
+      }
+      err += (unsigned long long)L.counts[i] * (unsigned long long)mind;
     }
-    if constexpr (X == 1) {
-      for (int r = 0; r < L.xw; ++r) (reinterpret_cast<uint8_t*>(L.xbox[r]) + XB_LAB_OFF)[i] = (uint8_t)best;
-    } else {
-      L.map_lut[x] = (uint8_t)best;
+    if (X != 1 && L.map_cellw) {
+      const unsigned am = __ballot_sync(0xffffffffu, v);
+      if (v) coarse_note(L.map_cellw, am, x, best);
     }
-    err += (unsigned long long)L.counts[i] * (unsigned long long)mind;
   }
   err = warp_sum(err);
   __syncthreads();
@@ -1931,10 +1949,27 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
         L.st->mse_err = e;
       }
       const uint8_t* idx = reinterpret_cast<const uint8_t*>(L.xbox[part]) + XB_LAB_OFF;
-      for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + tid; i < n;
-           i += (unsigned long long)gridDim.x * blockDim.x)
-        L.map_lut[L.keys[i]] = __ldcg(idx + i);
+      for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (tid & ~31); base < n;
+           base += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = base + lane;
+        const bool v = i < n;
+        uint32_t x = 0;
+        int best = 0;
+        if (v) {
+          x = L.keys[i];
+          best = __ldcg(idx + i);
+          L.map_lut[x] = (uint8_t)best;
+        }
+        if (L.map_cellw) {
+          const unsigned am = __ballot_sync(0xffffffffu, v);
+          if (v) coarse_note(L.map_cellw, am, x, best);
+        }
+      }
     }
+  }
+  if (L.map_cellw) {  // every cell noted: the compact table for k_map_pixels_coarse
+    grid.sync();
+    coarse_compact(L.map_cellw, L.map_coarse, blockIdx.x * blockDim.x + tid, gridDim.x * blockDim.x);
   }
 }
 
