@@ -25,7 +25,9 @@ using namespace cqb;
 namespace {
 
 constexpr int XFER_CHUNKS = 8;
-constexpr int DBG_NO_COARSE = 1 << 21;  // debug flag: k_map_pixels with per-pixel LUT gathers only (A/B)
+constexpr int DBG_NO_COARSE = 1 << 21;  // (see below)
+constexpr int DBG_K1_2PASS = 1 << 22;   // debug flag: K1 in two half-table passes (A/B)
+constexpr int DBG_K1_1PASS = 1 << 23;   // debug flag: K1 in one pass (A/B)  // debug flag: k_map_pixels with per-pixel LUT gathers only (A/B)
 constexpr int DBG_NO_XFER_OVERLAP = 1 << 19;  // debug flag: one H2D / D2H copy each, K1 after the H2D
 
 struct Staging {  // pinned host mirror of the per-call results
@@ -412,11 +414,16 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   // 4 Morton slices so each pass's atomics stay in L2.
   const bool sparse = sparse_path(ctx, P);
   // fused: K1 runs inside k_prep_small; k1_done: cqb_quantize_ex ran it per H2D slice
-  const int passes = fused || ctx->k1_done ? 0 : (P >= (4u << 20) ? 4 : 1);
+  const int passes = fused || ctx->k1_done ? 0 : (P >= (4u << 20) ? ((ctx->debug_flags & DBG_K1_2PASS) ? 2 : (ctx->debug_flags & DBG_K1_1PASS) ? 1 : 4) : 1);
   for (int q = 0; q < passes; ++q) {
     const uint32_t span = (1u << 24) / passes;
-    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(
-        d_img, P, ctx->bins, q * span, q + 1 == passes ? (1u << 24) : (q + 1) * span, sparse ? ctx->d_occ : nullptr);
+    const uint32_t mlo = q * span, mhi = q + 1 == passes ? (1u << 24) : (q + 1) * span;
+    if (passes <= 2 && !sparse)  // half-table passes: the raster streams (evict-first) so the slice stays in L2
+      k_hist_count<true><<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins, mlo, mhi,
+                                                                           sparse ? ctx->d_occ : nullptr);
+    else
+      k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_img, P, ctx->bins, mlo, mhi,
+                                                                      sparse ? ctx->d_occ : nullptr);
     CKL();
   }
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[2], ctx->stream));

@@ -37,6 +37,7 @@ __device__ __forceinline__ void bin_add(uint2* __restrict__ bins, uint32_t key, 
 // (2 MiB), so small images can compact the table without scanning 128 MiB.
 // px0: index of img's first pixel in the whole image (K1 over one slice of
 // an image whose H2D copy is still in flight, cqb_quantize_ex).
+template <bool kStream = false>
 __device__ __forceinline__ void hist_count_chunks(const uint8_t* __restrict__ img, uint64_t P,
                                                   uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi,
                                                   uint32_t* __restrict__ occ, uint64_t c0, uint64_t cstride,
@@ -44,7 +45,7 @@ __device__ __forceinline__ void hist_count_chunks(const uint8_t* __restrict__ im
   const uint64_t nchunk = (P + PX_PER_THREAD - 1) / PX_PER_THREAD;
   for (uint64_t c = c0; c < nchunk; c += cstride) {
     uint32_t keys[PX_PER_THREAD];
-    const int n = load_chunk_keys(img, P, c, keys);
+    const int n = load_chunk_keys<kStream>(img, P, c, keys);
     const uint32_t base = px0 + (uint32_t)(c * PX_PER_THREAD);
     uint32_t cur = keys[0], run = 1, start = base;
 #pragma unroll
@@ -64,10 +65,11 @@ __device__ __forceinline__ void hist_count_chunks(const uint8_t* __restrict__ im
   }
 }
 
+template <bool kStream = false>
 __global__ void __launch_bounds__(HIST_THREADS) k_hist_count(const uint8_t* __restrict__ img, uint64_t P,
                                                               uint2* __restrict__ bins, uint32_t mlo, uint32_t mhi,
                                                               uint32_t* __restrict__ occ, uint32_t px0 = 0) {
-  hist_count_chunks(img, P, bins, mlo, mhi, occ, (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x,
+  hist_count_chunks<kStream>(img, P, bins, mlo, mhi, occ, (uint64_t)blockIdx.x * HIST_THREADS + threadIdx.x,
                     (uint64_t)gridDim.x * HIST_THREADS, px0);
 }
 
