@@ -109,11 +109,11 @@ class Config:
 
 
 CONFIGS = {
-    "cfg1": Config("cfg1", 512, 512, (32,), "512x512 GMM-64, K=32"),
-    "cfg2": Config("cfg2", 768, 512, (64, 256), "768x512 GMM-256, K in {64,256}"),
-    "cfg3": Config("cfg3", 4096, 4096, (256,), "4096x4096 value noise + N(0,8), K=256"),
-    "cfg4": Config("cfg4", 4096, 4096, (256,), "4096x4096 uniform 24-bit, K=256"),
-    "cfg5": Config("cfg5", 1024, 1024, (64, 256), "64 x 1024x1024 GMM-256 images, K in {64,256}", images=64),
+    "cfg1": Config("cfg1", 512, 512, (32,), "GMM-64"),
+    "cfg2": Config("cfg2", 768, 512, (64, 256), "GMM-256"),
+    "cfg3": Config("cfg3", 4096, 4096, (256,), "4-octave value noise + N(0,8)"),
+    "cfg4": Config("cfg4", 4096, 4096, (256,), "uniform 24-bit"),
+    "cfg5": Config("cfg5", 1024, 1024, (64, 256), "64 GMM-256 images", images=64),
 }
 
 # BASELINE.json termination: relative SSE change <= 1e-4 or 100 iterations.

@@ -1728,7 +1728,9 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
           part = dd_add(part, term);
         }
       }
+      if (L.block_times && it == L.stamp_iter && tid == 0) L.block_times[15 * gridDim.x + 0] = globaltimer();
       block_sum3(S, part, moved, unused);
+      if (L.block_times && it == L.stamp_iter && tid == 0) L.block_times[15 * gridDim.x + 1] = globaltimer();
       const double sse = fmax(__dadd_rn(part.hi, part.lo) * inv_P, 0.0);
       bool stop;
       if (L.mode == 0) {
@@ -1764,6 +1766,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
           st->final_C[3 * t + 2] = S.nz[t];
         }
     }
+    if (L.block_times && it == L.stamp_iter && tid == 0 && blockIdx.x == 0) L.block_times[15 * gridDim.x + 2] = globaltimer();
     if (!direct) __syncthreads();  // (direct: the new centers were written before the count barrier)
     BLOCK_STAMP(9);
     if constexpr (X != 0)  // the delta accumulators again
