@@ -34,6 +34,12 @@
 #ifndef CQB_DIAG_FALLBACK
 #define CQB_DIAG_FALLBACK 0
 #endif
+#ifndef CQB_Q0
+#define CQB_Q0 1  // large path: first row quads staged in shared memory
+#endif
+#ifndef CQB_NQ
+#define CQB_NQ 4  // ... how many (entries 1..4*NQ)
+#endif
 
 
 namespace cqb {
@@ -767,6 +773,8 @@ struct ChunkSched {
 // 48 KB static limit): the FP32 centers of scan_f32, then the chunk order.
 struct LoopDyn {
   float4 c4[KMAX];  // centers of the current assignment rounded to FP32
+  float4 q0[CQB_NQ][KMAX];  // large path: entries 1..4*NQ of every FP32 row (staged per pass)
+  uint32_t o0[CQB_NQ][KMAX];
   ChunkSched sched;
 };
 constexpr size_t LOOP_DYN_SMEM = sizeof(LoopDyn);
@@ -843,7 +851,7 @@ constexpr int DEEP_P = CQB_DEEP_P;
 // sets `best` when both decisions are certified, else 0 (redo in FP64).
 // c4: FP32 centers; rq / oq: row p of the FP32 distances / order bytes
 // without the self entry (WsmState::rowD32 / rowO), read four entries at a time.
-template <bool kDeep, int DEEP_J_, int DEEP_P_>
+template <bool kDeep, int DEEP_J_, int DEEP_P_, bool kQ0 = false>
 __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const float4* __restrict__ rq,
                                         const uint32_t* __restrict__ oq, int k, uint32_t key, int p, int& best_out,
                                         unsigned int& n_active) {
@@ -852,8 +860,15 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
   const float pu = __fmaf_rn(prev, F32_PU_A, F32_P_B);
   const float pl = __fmaf_rn(prev, F32_PL_A, -F32_P_B);
   best_out = p;
-  float4 D = rq[0];  // entries 1..4
-  uint32_t T = oq[0];
+  float4 D;  // entries 1..4
+  uint32_t T;
+  if constexpr (kQ0) {  // staged in shared memory
+    D = loop_dyn_smem().q0[0][p];
+    T = loop_dyn_smem().o0[0][p];
+  } else {
+    D = rq[0];
+    T = oq[0];
+  }
   // the common case: no candidate (kmeans.hpp:220-226 breaks at j = 1); k = 1: D.x = +inf
   if (D.x >= pl) return D.x >= pu ? 1 : 0;
   n_active += 1;
@@ -878,8 +893,13 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
     eval(T >> 24);
     j += 4;
     ++qi;
-    D = rq[qi];
-    T = oq[qi];
+    if (kQ0 && qi < CQB_NQ) {
+      D = loop_dyn_smem().q0[qi][p];
+      T = loop_dyn_smem().o0[qi][p];
+    } else {
+      D = rq[qi];
+      T = oq[qi];
+    }
     if (D.x >= pl) { Db = D.x; break; }
     if (kDeep && j > DEEP_J_) {
       // deep scan: the first entry e >= j with distance >= pl (rows are sorted,
@@ -1005,6 +1025,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   // small sample sets: chunk costs recorded for the longest-first order
   constexpr bool kSched = PPT == 1;
   constexpr bool kDeep = true;
+  constexpr bool kQ0 = PPT == 2 && CQB_Q0;
   const uint32_t my_ch = nch > pb ? (nch - 1u - pb) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const float4* __restrict__ rq32 = reinterpret_cast<const float4*>(L.st->rowD32);
@@ -1013,6 +1034,14 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   const uint8_t* __restrict__ go = L.st->order;
   // FP32 screening (scan_f32): sort-means scans whose centers all satisfy |c| < 256
   const bool use32 = S.f32ok;
+  if constexpr (kQ0) {  // the rows' first quads into shared memory (the rows are final: grid barrier)
+    for (int u = threadIdx.x; u < CQB_NQ * L.k; u += blockDim.x) {
+      const int t = u % L.k, qq = u / L.k;
+      loop_dyn_smem().q0[qq][t] = __ldcg(rq32 + t * (ROW32 / 4) + qq);
+      loop_dyn_smem().o0[qq][t] = __ldcg(oq32 + t * (ROW32 / 4) + qq);
+    }
+    __syncthreads();
+  }
   const uint32_t* __restrict__ keys = L.keys;
   const uint32_t* __restrict__ counts = L.counts;
   uint8_t* __restrict__ labels = L.labels;
@@ -1058,8 +1087,8 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       int best = p;
       int J = 0;
       if (use32)
-          J = scan_f32<kDeep, DEEP_J, DEEP_P>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4), k, key[q], p, best,
-                                              n_active);
+          J = scan_f32<kDeep, DEEP_J, DEEP_P, kQ0>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4), k, key[q], p,
+                                                   best, n_active);
       if (J == 0) {  // FP64: uncertified FP32 screens, or screening off (rare)
         const int r = scan_fp64(S, gd + p * KMAX, ro, k, key[q], p, L.debug_flags);
         J = r & 0xFFF;

@@ -52,6 +52,10 @@ for a, b, n in [(3, 8, "fin: centers"), (8, 9, "fin: block0"), (9, 4, "fin: copy
     print(f"sub {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f}")
 for a, b, n in [(3, 8, "block0 centers"), (8, 9, "block0 SSE/term"), (9, 4, "block0 copy")]:
     print(f"sub {n:16s} {dur(a, b)[0]:6.2f}")
+b0 = bt[15 * g: 15 * g + 3].astype(np.int64)
+t8 = int(bt[8 * g])
+print(f"block0 SSE: terms {(b0[0] - t8) / 1e3:6.2f}  block_sum3 {(b0[1] - b0[0]) / 1e3:6.2f}  "
+      f"decision+stores {(b0[2] - b0[1]) / 1e3:6.2f}  trailing sync {(int(bt[9 * g]) - b0[2]) / 1e3:6.2f}")
 for a, b, n in []:
     v = dur(a, b)
     print(f"dur {n:14s} min {v.min():6.2f} p50 {np.median(v):6.2f} max {v.max():6.2f} block0 {v[0]:6.2f}")
