@@ -551,3 +551,55 @@ def test_quantize_overlapped_transfers(port):
     mine, my_idx = port.map_pixels(img, q.palette)
     np.testing.assert_array_equal(q.index_map, my_idx)
     np.testing.assert_array_equal(q.mapped, mine)
+
+
+def test_quantize_concurrent_callers(port):
+    """Host threads streaming images through the C ABI concurrently (one
+    context each): a call that starts while another is in flight skips the
+    sliced H2D/K1 overlap (one copy, 4-pass K1). Every caller's outputs equal
+    the single-caller run and the oracle's map of its palette."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    imgs = [gmm_image(1531, 1373, 64, 90 + i) for i in range(3)]  # dense path, ragged
+    term = api.Termination.fixed(3)
+    solo = [api.quantize(im, 64, term, seed=5, error=True) for im in imgs]
+
+    def run(j):
+        return [api.quantize(imgs[j], 64, term, seed=5, error=True) for _ in range(2)]
+
+    with ThreadPoolExecutor(3) as ex:
+        outs = list(ex.map(run, range(3)))
+    for j, rs in enumerate(outs):
+        for q in rs:
+            np.testing.assert_array_equal(q.palette, solo[j].palette)
+            np.testing.assert_array_equal(q.index_map, solo[j].index_map)
+            np.testing.assert_array_equal(q.mapped, solo[j].mapped)
+            np.testing.assert_array_equal(q.error, solo[j].error)
+            assert q.report.dist_evals == solo[j].report.dist_evals and q.report.mse == solo[j].report.mse
+    mine, my_idx = port.map_pixels(imgs[0], solo[0].palette)
+    np.testing.assert_array_equal(solo[0].index_map, my_idx)
+
+
+@pytest.mark.parametrize("k", [7, 255, 256])
+def test_coarse_map_table_matches_lut_path(k, port):
+    """Large images map through the coarse 4x4x8-cell table (pure cells from
+    shared memory, byte 255 = gather from the LUT; with K = 256 the pure cells
+    of index 255 gather too). Index map, mapped raster and error image equal
+    the per-pixel LUT path (debug flag 1 << 21) and the oracle's map."""
+    img = value_noise_image(2048, 1024, 11)
+    term = api.Termination.fixed(2)
+    ctx = api.context(0)
+    ctx.lib.cqb_set_debug(ctx.h, 1 << 21)
+    try:
+        lut = api.quantize(img, k, term, seed=4, error=True)
+    finally:
+        ctx.lib.cqb_set_debug(ctx.h, 0)
+    q = api.quantize(img, k, term, seed=4, error=True)
+    np.testing.assert_array_equal(q.palette, lut.palette)
+    np.testing.assert_array_equal(q.index_map, lut.index_map)
+    np.testing.assert_array_equal(q.mapped, lut.mapped)
+    np.testing.assert_array_equal(q.error, lut.error)
+    assert q.report.mse == lut.report.mse
+    mine, my_idx = port.map_pixels(img, q.palette)
+    np.testing.assert_array_equal(q.index_map, my_idx)
+    np.testing.assert_array_equal(q.mapped, mine)
