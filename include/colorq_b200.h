@@ -314,6 +314,31 @@ int cqb_xch_emulate(cqb_ctx* ctx, int vranks);
 int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int k, const cqb_termination* term,
                          uint64_t seed, uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range);
 
+/* ---- pixel-row sharded histogram (config 4 across GPUs) -----------------
+ * build_histogram (histogram.hpp:65-99) split over the W ranks of
+ * cqb_quantize_sharded, so no rank counts the whole image:
+ *  1. cqb_hist_rows: rank r counts the pixel rows it maps (pixel_range: 16-
+ *     pixel aligned, the last rank takes the tail; global pixel indices) into
+ *     its own bin table and compacts the touched bins in Morton order into
+ *     d_out as u32 triplets {key, count, first pixel} (cap >= its pixels).
+ *     owner_counts[o] = how many of them fall in rank o's Morton range
+ *     [o 2^24 / W, (o + 1) 2^24 / W); they are contiguous, in owner order.
+ *  2. the host moves each run to its owner (all-to-all; NCCL over NVLink).
+ *  3. cqb_hist_merge: the owner merges what it received (count sum, first
+ *     pixel min) and compacts its range (Morton order) into d_out.
+ *  4. the host all-gathers the owners' lists; concatenated in rank order they
+ *     are the whole image's histogram in Morton order, which
+ *     cqb_quantize_sharded_samples takes instead of counting the image
+ *     (with no exchange set up: the single-GPU pipeline from that histogram).
+ * The result is identical to the unsharded histogram, entry for entry. */
+int cqb_hist_rows(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int world, int rank, uint32_t* d_out,
+                  uint64_t cap, uint64_t* n_out, uint64_t* owner_counts);
+int cqb_hist_merge(cqb_ctx* ctx, const uint32_t* d_in, uint64_t n_in, uint32_t* d_out, uint64_t cap,
+                   uint64_t* n_out);
+int cqb_quantize_sharded_samples(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, const uint32_t* d_samples,
+                                 uint64_t n_unique, int k, const cqb_termination* term, uint64_t seed,
+                                 uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,8 @@ struct cqb_ctx {
   uint32_t* d_cellw = nullptr;   // coarse map table: per-cell words (map.cuh)
   uint8_t* d_coarse = nullptr;   // its compact form (labels + MIXED bits)
   bool coarse_built = false;     // set by launch_loop: the loop's epilogue wrote d_coarse for this call
+  const uint32_t* ext_samples = nullptr;  // set only while cqb_quantize_sharded_samples enqueues: the
+  uint64_t ext_n = 0;                     // whole image's Morton-ordered {key, count, first} triplets
 
   size_t cap_px = 0;
   uint8_t* d_img = nullptr;
@@ -563,9 +565,9 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   // one point per lane per grab for small sample sets (N' <= P < 2M): finer
   // balance; two for large ones: more ILP (cfg2 +1.2%, cfg4 +8% respectively)
   const bool small = total < OCC_MAX_PIXELS;
-  const void* kern = X == 1   ? (small ? (const void*)k_wsm_loop<1, 1> : (const void*)k_wsm_loop<2, 1>)
-                     : X == 2 ? (small ? (const void*)k_wsm_loop<1, 2> : (const void*)k_wsm_loop<2, 2>)
-                              : (small ? (const void*)k_wsm_loop<1, 0> : (const void*)k_wsm_loop<2, 0>);
+  const void* kern = X == 1   ? (small ? (const void*)k_wsm_loop<1, 1> : (const void*)k_wsm_loop<CQB_PPT_LARGE, 1>)
+                     : X == 2 ? (small ? (const void*)k_wsm_loop<1, 2> : (const void*)k_wsm_loop<CQB_PPT_LARGE, 2>)
+                              : (small ? (const void*)k_wsm_loop<1, 0> : (const void*)k_wsm_loop<CQB_PPT_LARGE, 0>);
   size_t dyn = LOOP_DYN_SMEM;
   if (X == 0 && small && !(ctx->debug_flags & 512)) {
     // resident samples when the block's share (bounded by P) fits in shared memory
@@ -672,9 +674,21 @@ int enqueue_quantize(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, int k, cons
   TRY(upload_draws(ctx, seed, ndraws));
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   PROF(0);
-  const bool fused = fused_prep(ctx, P);
-  if (!fused) TRY(reset_state(ctx));  // else zeroed inside k_prep_small
-  TRY(enqueue_histogram(ctx, d_img, P, true, false, k, ndraws, fused));  // records PROF(1..3)
+  if (ctx->ext_samples) {  // the histogram came from the pixel-row shards (cqb_hist_rows / cqb_hist_merge)
+    TRY(reset_state(ctx));
+    const int gu = (int)std::min<uint64_t>((ctx->ext_n + 255) / 256, (uint64_t)ctx->num_sms * 8);
+    k_unpack_triplets<<<std::max(gu, 1), 256, 0, ctx->stream>>>(ctx->ext_samples, ctx->ext_n, ctx->d_mkeys,
+                                                                ctx->d_mcounts, ctx->d_mrank, ctx->d_n);
+    CKL();
+    PROF(1);
+    PROF(2);
+    PROF(3);
+    TRY(enqueue_rank_select(ctx, d_img, P, k, ndraws));
+  } else {
+    const bool fused = fused_prep(ctx, P);
+    if (!fused) TRY(reset_state(ctx));  // else zeroed inside k_prep_small
+    TRY(enqueue_histogram(ctx, d_img, P, true, false, k, ndraws, fused));  // records PROF(1..3)
+  }
   PROF(4);
   ctx->fuse_map = true;  // k_map_tables + k_map_unique run in the loop kernel's tail
   const int lrc = launch_loop(ctx, k, term, 1, P, nullptr, 0);
@@ -790,12 +804,12 @@ int cqb_create(int device, cqb_ctx** out) {
     if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
     ctx->num_sms = prop.multiProcessorCount;
     int nb = 0;
-    for (const void* f : {(const void*)k_wsm_loop<1, 0>, (const void*)k_wsm_loop<2, 0>, (const void*)k_wsm_loop<1, 1>,
-                          (const void*)k_wsm_loop<2, 1>, (const void*)k_wsm_loop<1, 2>, (const void*)k_wsm_loop<2, 2>})
+    for (const void* f : {(const void*)k_wsm_loop<1, 0>, (const void*)k_wsm_loop<CQB_PPT_LARGE, 0>, (const void*)k_wsm_loop<1, 1>,
+                          (const void*)k_wsm_loop<CQB_PPT_LARGE, 1>, (const void*)k_wsm_loop<1, 2>, (const void*)k_wsm_loop<CQB_PPT_LARGE, 2>})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
     CK(cudaFuncSetAttribute((const void*)k_wsm_loop<1, 0, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RES_DYN_MAX));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<2, 0>, LOOP_THREADS,
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<CQB_PPT_LARGE, 0>, LOOP_THREADS,
                                                      LOOP_DYN_SMEM));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
     ctx->loop_blocks_max = std::min(nb, CQB_LOOP_MINB) * ctx->num_sms;
@@ -830,7 +844,7 @@ int cqb_create(int device, cqb_ctx** out) {
     CK(cudaMalloc(&ctx->d_mom, sizeof(unsigned long long) * 5 * KMAX));
     CK(cudaMallocHost(&ctx->h_mom, sizeof(unsigned long long) * (5 * KMAX + 1)));
     CK(cudaMalloc(&ctx->d_Cnew, sizeof(double) * 3 * KMAX));
-    CK(cudaMalloc(&ctx->d_scal, sizeof(double) * 8));
+    CK(cudaMalloc(&ctx->d_scal, sizeof(double) * 24));  // [0..7] sse + reseed, [8..16] cqb_hist_rows owner bounds
     CK(cudaMalloc(&ctx->d_ints, sizeof(int) * (KMAX + 8)));
     CK(cudaMalloc(&ctx->d_taken, sizeof(uint32_t) * KMAX));
     CK(cudaMalloc(&ctx->d_cand_d, sizeof(double) * MAXBLK));
@@ -2036,6 +2050,122 @@ int cqb_quantize_sharded(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, 
   ctx->xsharded = true;
   const int rc = enqueue_quantize(ctx, d_rgb, n_pixels, k, term, seed, d_index_out, d_rgb_out, k + 64);
   ctx->xsharded = false;
+  return rc;
+}
+
+// ---- pixel-row sharded histogram (config 4 across GPUs) --------------------
+int cqb_hist_rows(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int world, int rank, uint32_t* d_out,
+                  uint64_t cap, uint64_t* n_out, uint64_t* owner_counts) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (world < 1 || world > XMAX || rank < 0 || rank >= world)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_rows: rank %d of world %d (1..%d ranks)", rank, world, XMAX);
+  if (!d_rgb || !d_out || !n_out || !owner_counts) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_rows: null buffer");
+  if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+  if (!aligned16(d_rgb)) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_rows: the raster must be 16-B aligned");
+  CK(cudaSetDevice(ctx->device));
+  // this rank's rows: the pixel range it also maps (16-pixel aligned starts)
+  const uint64_t q = (n_pixels + 15) / 16;
+  const uint64_t lo = std::min(n_pixels, q * (uint64_t)rank / (uint64_t)world * 16);
+  const uint64_t hi = rank == world - 1 ? n_pixels : std::min(n_pixels, q * (uint64_t)(rank + 1) / (uint64_t)world * 16);
+  const uint64_t n = hi - lo;
+  if (cap < n) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_rows: capacity %llu < %llu rows' pixels",
+                           (unsigned long long)cap, (unsigned long long)n);
+  TRY(ensure_pixels(ctx, std::max<uint64_t>(n, 1)));
+  TRY(ensure_samples(ctx, std::max<uint64_t>(n, 1)));
+  // K1 over the rows (global pixel indices), occupancy map for the compaction;
+  // large row sets in 4 Morton-slice passes (each pass's atomics in L2)
+  const uint64_t nchunk = (n + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+  const int passes = n >= (4u << 20) ? 4 : 1;
+  for (int p = 0; p < passes && n > 0; ++p) {
+    const uint32_t span = (1u << 24) / passes;
+    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(
+        d_rgb + 3 * lo, n, ctx->bins, p * span, p + 1 == passes ? (1u << 24) : (p + 1) * span, ctx->d_occ,
+        (uint32_t)lo);
+    CKL();
+  }
+  CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_OCC_TILES + 1), ctx->stream));
+  k_occ_compact<<<N_OCC_TILES, OC_THREADS, 0, ctx->stream>>>(
+      ctx->d_occ, ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
+      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_OCC_TILES), ctx->d_n, nullptr);
+  CKL();
+  unsigned long long* d_bounds = reinterpret_cast<unsigned long long*>(ctx->d_scal) + 8;
+  const int gp = (int)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)ctx->num_sms * 8);
+  k_pack_triplets<<<std::max(gp, 1), 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n,
+                                                            d_out, world, d_bounds);
+  CKL();
+  unsigned long long b[XMAX + 1];
+  CK(cudaMemcpyAsync(b, d_bounds, sizeof(unsigned long long) * (world + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n_out = b[world];
+  for (int o = 0; o < world; ++o) owner_counts[o] = b[o + 1] - b[o];
+  return CQB_OK;
+}
+
+int cqb_hist_merge(cqb_ctx* ctx, const uint32_t* d_in, uint64_t n_in, uint32_t* d_out, uint64_t cap,
+                   uint64_t* n_out) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if ((!d_in && n_in) || !d_out || !n_out) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_merge: null buffer");
+  if (n_in >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "hist_merge: above 2^32-1 entries");
+  CK(cudaSetDevice(ctx->device));
+  TRY(ensure_samples(ctx, std::max<uint64_t>(std::min<uint64_t>(n_in, 1u << 24), 1)));
+  if (n_in) {
+    const int g = (int)std::min<uint64_t>((n_in + 255) / 256, (uint64_t)ctx->num_sms * 16);
+    k_merge_triplets<<<g, 256, 0, ctx->stream>>>(d_in, n_in, ctx->bins, ctx->d_occ);
+    CKL();
+  }
+  CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (N_OCC_TILES + 1), ctx->stream));
+  k_occ_compact<<<N_OCC_TILES, OC_THREADS, 0, ctx->stream>>>(
+      ctx->d_occ, ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
+      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + N_OCC_TILES), ctx->d_n, nullptr);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const uint64_t n = ctx->h_scalar[0];
+  if (n > cap) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_merge: capacity %llu < %llu merged samples",
+                           (unsigned long long)cap, (unsigned long long)n);
+  if (n) {
+    const int gp = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->num_sms * 8);
+    k_pack_triplets<<<gp, 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n, d_out, 0,
+                                                 nullptr);
+    CKL();
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  *n_out = n;
+  return CQB_OK;
+}
+
+int cqb_quantize_sharded_samples(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, const uint32_t* d_samples,
+                                 uint64_t n_unique, int k, const cqb_termination* term, uint64_t seed,
+                                 uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (!d_samples || n_unique == 0 || n_unique > n_pixels)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "sharded samples: %llu samples for %llu pixels",
+                (unsigned long long)n_unique, (unsigned long long)n_pixels);
+  ctx->ext_samples = d_samples;
+  ctx->ext_n = n_unique;
+  int rc;
+  if (ctx->xmode == 0) {  // one rank: the single-GPU pipeline from the given histogram
+    rc = [&]() -> int {
+      TRY(check_k(ctx, k));
+      TRY(check_term(ctx, term));
+      if (!d_rgb) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "quantize: empty image");
+      if (n_pixels >= 0xffffffffull) return fail(ctx, CQB_ERR_UNSUPPORTED, "images above 2^32-1 pixels");
+      if (!aligned16(d_rgb) || (d_index_out && !aligned16(d_index_out)) || (d_rgb_out && !aligned16(d_rgb_out)))
+        return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "sharded quantize: device buffers must be 16-B aligned");
+      CK(cudaSetDevice(ctx->device));
+      TRY(ensure_pixels(ctx, n_pixels));
+      if (px_range) {
+        px_range[0] = 0;
+        px_range[1] = n_pixels;
+      }
+      return enqueue_quantize(ctx, d_rgb, n_pixels, k, term, seed, d_index_out, d_rgb_out, k + 64);
+    }();
+  } else {
+    rc = cqb_quantize_sharded(ctx, d_rgb, n_pixels, k, term, seed, d_index_out, d_rgb_out, px_range);
+  }
+  ctx->ext_samples = nullptr;
+  ctx->ext_n = 0;
   return rc;
 }
 

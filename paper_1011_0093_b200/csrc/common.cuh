@@ -13,6 +13,9 @@ constexpr int LOOP_THREADS = CQB_LOOP_THREADS;
 #ifndef CQB_LOOP_MINB
 #define CQB_LOOP_MINB 1  // persistent WSM loop blocks per SM (__launch_bounds__)
 #endif  // persistent WSM loop block size (one block per SM)
+#ifndef CQB_PPT_LARGE
+#define CQB_PPT_LARGE 2  // WSM loop: 32-sample chunks per warp grab for large sample sets
+#endif
 constexpr int MAXBLK = 1024;         // max persistent blocks (reseed candidate slots)
 constexpr int HIST_THREADS = 256;    // histogram / compaction block size
 constexpr int PX_PER_THREAD = 16;    // 16 pixels = 48 B = 3 x 16-B vector loads

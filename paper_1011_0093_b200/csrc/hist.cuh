@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(OC_THREADS) k_occ_compact(uint32_t* __restrict
           m_keys[pos] = key_of_morton(ms[e]);
           m_counts[pos] = v[e].x;
           m_first[pos] = f;
-          asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bitmap + (f >> 5)), "r"(1u << (f & 31)) : "memory");
+          if (bitmap)
+            asm volatile("red.global.or.b32 [%0], %1;" ::"l"(bitmap + (f >> 5)), "r"(1u << (f & 31)) : "memory");
           bins[ms[e]] = make_uint2(0u, 0u);
           ++pos;
         }
@@ -703,6 +704,73 @@ __global__ void k_hist_weights(const uint32_t* __restrict__ counts, const unsign
   const double inv_total = 1.0 / (double)P;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     weights[i] = __dmul_rn((double)counts[i], inv_total);
+}
+
+// ---------------------------------------------------------------------------
+// Pixel-row sharded histogram (config 4 across GPUs; capi.cu cqb_hist_rows /
+// cqb_hist_merge). Samples travel between ranks as {key, count, first pixel}
+// u32 triplets; rank o owns the bins of Morton range [o 2^24 / W, (o+1) 2^24 / W).
+
+__host__ __device__ __forceinline__ uint32_t owner_morton_lo(int o, int world) {
+  return (uint32_t)(((unsigned long long)o << 24) / (unsigned long long)world);
+}
+
+// Morton-ordered SoA samples -> triplets, and the W + 1 owner boundaries
+// (first sample index of each owner's Morton range; bounds[W] = n).
+__global__ void k_pack_triplets(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ counts,
+                                const uint32_t* __restrict__ first, const unsigned long long* __restrict__ n_ptr,
+                                uint32_t* __restrict__ out, int world, unsigned long long* __restrict__ bounds) {
+  const unsigned long long n = *n_ptr;
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (unsigned long long i = tid; i < n; i += (unsigned long long)gridDim.x * blockDim.x) {
+    out[3 * i] = keys[i];
+    out[3 * i + 1] = counts[i];
+    out[3 * i + 2] = first[i];
+  }
+  if (bounds && tid <= (unsigned long long)world) {
+    const int o = (int)tid;
+    unsigned long long a = 0, b = n;  // first i with morton(keys[i]) >= lo(o)
+    if (o == world) {
+      a = n;
+    } else {
+      const uint32_t m = owner_morton_lo(o, world);
+      while (a < b) {
+        const unsigned long long mid = (a + b) >> 1;
+        if (morton_of_key(keys[mid]) < m) a = mid + 1;
+        else b = mid;
+      }
+    }
+    bounds[o] = a;
+  }
+}
+
+// Received triplets (any order, keys may repeat across source ranks) into the
+// bin table: count sum, first-pixel min, occupancy bit (k_occ_compact then
+// emits them in Morton order).
+__global__ void k_merge_triplets(const uint32_t* __restrict__ in, unsigned long long n, uint2* __restrict__ bins,
+                                 uint32_t* __restrict__ occ) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t key = in[3 * i], cnt = in[3 * i + 1], f = in[3 * i + 2];
+    const uint32_t m = morton_of_key(key);
+    uint32_t* b = reinterpret_cast<uint32_t*>(bins + m);
+    atomicAdd(b, cnt);
+    atomicMax(b + 1, ~f);
+    atomicOr(&occ[m >> 5], 1u << (m & 31));
+  }
+}
+
+// The whole image's triplets (owners' lists concatenated) -> SoA samples.
+__global__ void k_unpack_triplets(const uint32_t* __restrict__ in, unsigned long long n, uint32_t* __restrict__ keys,
+                                  uint32_t* __restrict__ counts, uint32_t* __restrict__ first,
+                                  unsigned long long* __restrict__ n_ptr) {
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0) *n_ptr = n;
+  for (unsigned long long i = tid; i < n; i += (unsigned long long)gridDim.x * blockDim.x) {
+    keys[i] = in[3 * i];
+    counts[i] = in[3 * i + 1];
+    first[i] = in[3 * i + 2];
+  }
 }
 
 }  // namespace cqb

@@ -37,6 +37,9 @@
 #ifndef CQB_Q0
 #define CQB_Q0 1  // large path: first row quads staged in shared memory
 #endif
+#ifndef CQB_Q0_SMALL
+#define CQB_Q0_SMALL 0  // ... also on the small path
+#endif
 #ifndef CQB_NQ
 #define CQB_NQ 4  // ... how many (entries 1..4*NQ)
 #endif
@@ -1025,7 +1028,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   // small sample sets: chunk costs recorded for the longest-first order
   constexpr bool kSched = PPT == 1;
   constexpr bool kDeep = true;
-  constexpr bool kQ0 = PPT == 2 && CQB_Q0;
+  constexpr bool kQ0 = (PPT >= 2 || CQB_Q0_SMALL) && CQB_Q0;
   const uint32_t my_ch = nch > pb ? (nch - 1u - pb) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const float4* __restrict__ rq32 = reinterpret_cast<const float4*>(L.st->rowD32);

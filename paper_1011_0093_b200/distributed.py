@@ -265,6 +265,31 @@ class PeerShardedQuantizer:
         self._k, self._cap = k, term.iteration_budget
         return int(rng[0]), int(rng[1])
 
+    def enqueue_rows(self, img, n_pixels: int, k: int, term, seed: int = 1, d_index: int | None = None,
+                     d_rgb_out: int | None = None, group=None) -> tuple[int, int]:
+        """cqb_quantize_sharded with the histogram sharded by pixel rows too
+        (``img``: the raster as a CUDA uint8 tensor on every rank): this rank
+        counts only its rows, the owners merge, the whole histogram is
+        all-gathered (NCCL), then the loop and the map run as in enqueue."""
+        backend = DeviceHistBackend(self.ctx)
+        if self.emulated:
+            samples = sharded_histogram_emulated(backend, img, n_pixels, self.world)
+        else:
+            import torch.distributed as dist
+
+            if dist.is_available() and dist.is_initialized():
+                samples = sharded_histogram(backend, img, n_pixels, TensorExchange(group))
+            else:
+                samples = sharded_histogram_emulated(backend, img, n_pixels, 1)
+        self._samples = samples  # alive until the enqueued work has read it (fetch)
+        rng = np.zeros(2, np.uint64)
+        t = term.native()
+        self.ctx.check(self.lib.cqb_quantize_sharded_samples(self.ctx.h, img.data_ptr(), n_pixels, samples.data_ptr(),
+                                                             samples.shape[0], k, C.byref(t), seed, d_index,
+                                                             d_rgb_out, rng.ctypes.data_as(_u64p)))
+        self._k, self._cap = k, term.iteration_budget
+        return int(rng[0]), int(rng[1])
+
     def fetch(self):
         """Wait; return (centers [k,3], report, sse_history). report.dist_evals
         is this rank's share (sum over ranks for the reference's count)."""
@@ -296,4 +321,118 @@ def exchange_handles(handle: bytes, group=None) -> list[bytes]:
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, handle, group=group)
     assert all(isinstance(h, bytes) and len(h) == len(handle) for h in out)
+    return out
+
+
+# --------------------------------------------------------------------------- sharded histogram
+# build_histogram (histogram.hpp:65-99) split over the ranks by pixel rows,
+# with bin ownership by Morton range (include/colorq_b200.h, cqb_hist_rows):
+# rank r counts the rows it maps, sends each owner its run of touched bins,
+# owners merge and compact, and the owners' lists are all-gathered — the
+# whole image's Morton-ordered histogram, identical to the unsharded one,
+# without any rank counting every pixel.
+class DeviceHistBackend:
+    """cqb_hist_rows / cqb_hist_merge on one context (tensors on its GPU)."""
+
+    def __init__(self, ctx):
+        self.ctx, self.lib = ctx, ctx.lib
+
+    def rows(self, img, n_pixels: int, world: int, rank: int):
+        import torch
+
+        lo, hi = pixel_range(n_pixels, world, rank)
+        out = torch.empty((max(hi - lo, 1), 3), dtype=torch.int32, device=img.device)
+        n = C.c_uint64()
+        counts = np.zeros(world, np.uint64)
+        self.ctx.check(self.lib.cqb_hist_rows(self.ctx.h, img.data_ptr(), n_pixels, world, rank, out.data_ptr(),
+                                              out.shape[0], C.byref(n), counts.ctypes.data_as(_u64p)))
+        return out[: n.value], [int(c) for c in counts]
+
+    def merge(self, recv, world: int):
+        import torch
+
+        cap = max(1, min(recv.shape[0], ((1 << 24) + world - 1) // world + 1))
+        out = torch.empty((cap, 3), dtype=torch.int32, device=recv.device)
+        n = C.c_uint64()
+        self.ctx.check(self.lib.cqb_hist_merge(self.ctx.h, recv.data_ptr() if recv.shape[0] else None,
+                                               recv.shape[0], out.data_ptr(), cap, C.byref(n)))
+        return out[: n.value]
+
+
+class TensorExchange:
+    """All-to-all and all-gather of [n, 3] int32 sample triplets over a
+    torch.distributed group (NCCL for CUDA tensors, gloo for CPU ones)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def alltoallv(self, send, send_counts: list):
+        import torch
+        import torch.distributed as dist
+
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=send.device)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = [int(v) for v in rc.tolist()]
+        recv = torch.empty((sum(recv_counts), 3), dtype=send.dtype, device=send.device)
+        dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=recv_counts,
+                               input_split_sizes=list(send_counts), group=self.group)
+        return recv
+
+    def allgatherv(self, t):
+        import torch
+        import torch.distributed as dist
+
+        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        ns = torch.empty(self.world, dtype=torch.int64, device=t.device)
+        dist.all_gather_into_tensor(ns, n, group=self.group)
+        sizes = [int(v) for v in ns.tolist()]
+        m = max(sizes)
+        pad = torch.zeros((m, 3), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        out = torch.empty((self.world * m, 3), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, pad, group=self.group)
+        return torch.cat([out[r * m: r * m + sizes[r]] for r in range(self.world)])
+
+
+def sharded_histogram(backend, img, n_pixels: int, exchange):
+    """This rank's share of the pixel-row sharded histogram; returns the whole
+    image's Morton-ordered {key, count, first pixel} triplets (every rank)."""
+    _sync(img)
+    local, counts = backend.rows(img, n_pixels, exchange.world, exchange.rank)
+    recv = exchange.alltoallv(local, counts)
+    _sync(recv)
+    own = backend.merge(recv, exchange.world)
+    out = exchange.allgatherv(own)
+    _sync(out)
+    return out
+
+
+def _sync(t):
+    """The library's stream reads what torch's stream produced (and back)."""
+    if getattr(t, "is_cuda", False):
+        import torch
+
+        torch.cuda.current_stream(t.device).synchronize()
+
+
+def sharded_histogram_emulated(backend, img, n_pixels: int, world: int):
+    """The same data path in one process: the W ranks' row counts in
+    sequence, the all-to-all and all-gather as slicing (single-GPU check)."""
+    import torch
+
+    _sync(img)
+    runs = [backend.rows(img, n_pixels, world, r) for r in range(world)]
+    owners = []
+    for o in range(world):
+        parts = [loc[sum(c[:o]): sum(c[: o + 1])] for loc, c in runs]
+        recv = torch.cat(parts)
+        _sync(recv)
+        owners.append(backend.merge(recv, world))
+    out = torch.cat(owners)
+    _sync(out)
     return out

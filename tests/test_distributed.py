@@ -409,3 +409,102 @@ def test_exchange_protocol_two_slots_suffice():
     for t in th:
         t.join()
     assert not errors, errors[:3]
+
+
+# --------------------------------------------------------------------------- sharded histogram
+class FakeHistBackend:
+    """CPU stand-in for DeviceHistBackend (cqb_hist_rows / cqb_hist_merge
+    semantics, test infrastructure): CPU int32 tensors of {key, count, first}."""
+
+    @staticmethod
+    def _emit(keys, counts, first):
+        import torch
+
+        o = np.argsort(_morton(keys), kind="stable")
+        t = np.stack([keys[o], counts[o], first[o]], 1).astype(np.int64)
+        return torch.from_numpy(t.astype(np.uint32).view(np.int32).reshape(-1, 3).copy())
+
+    def rows(self, img, n_pixels, world, rank):
+        from paper_1011_0093_b200.distributed import pixel_range
+
+        lo, hi = pixel_range(n_pixels, world, rank)
+        px = img.numpy().reshape(-1, 3)[lo:hi].astype(np.uint32)
+        keys = (px[:, 0] << 16) | (px[:, 1] << 8) | px[:, 2]
+        u, first, counts = np.unique(keys, return_index=True, return_counts=True)
+        t = self._emit(u, counts, first + lo)
+        m = _morton(t.numpy().view(np.uint32)[:, 0])
+        bounds = [int(np.searchsorted(m, ((o << 24) // world))) for o in range(world)] + [len(m)]
+        return t, [bounds[o + 1] - bounds[o] for o in range(world)]
+
+    def merge(self, recv, world):
+        a = recv.numpy().view(np.uint32).astype(np.int64)
+        if len(a) == 0:
+            return self._emit(np.zeros(0, np.uint32), np.zeros(0, np.int64), np.zeros(0, np.int64))
+        u, inv = np.unique(a[:, 0], return_inverse=True)
+        counts = np.bincount(inv, weights=a[:, 1], minlength=len(u)).astype(np.int64)
+        first = np.full(len(u), np.iinfo(np.int64).max)
+        np.minimum.at(first, inv, a[:, 2])
+        return self._emit(u.astype(np.uint32), counts, first)
+
+
+def _full_histogram(img):
+    px = img.reshape(-1, 3).astype(np.uint32)
+    keys = (px[:, 0] << 16) | (px[:, 1] << 8) | px[:, 2]
+    u, first, counts = np.unique(keys, return_index=True, return_counts=True)
+    return FakeHistBackend._emit(u, counts, first).numpy()
+
+
+def _hist_worker(rank, world, port, img, out_q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1011_0093_b200.distributed import TensorExchange, sharded_histogram
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = torch.from_numpy(img.reshape(-1).copy())
+        out = sharded_histogram(FakeHistBackend(), t, img.shape[0] * img.shape[1], TensorExchange())
+        out_q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_histogram_matches_full(world):
+    """Pixel-row sharded histogram through the real exchange code
+    (TensorExchange: all-to-all of the owners' runs, all-gather of the owner
+    lists) over gloo: every rank ends with the whole image's Morton-ordered
+    histogram, entry for entry (counts summed across row shards, first pixel =
+    global minimum), although no rank counted every pixel."""
+    img = gmm_image(97, 61, 12, 5)
+    img[::7, ::3] = img[0, 0]  # a color repeated across every row shard
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hist_worker, args=(r, world, port, img, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=240) for _ in procs], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = _full_histogram(img)
+    for _, got in outs:
+        np.testing.assert_array_equal(got, ref)
+
+
+def test_sharded_histogram_emulated_matches_full():
+    """The one-process emulation (the single-GPU check's data path) with the
+    CPU stand-in: W = 1..5 row shards give the full histogram."""
+    import torch
+
+    from paper_1011_0093_b200.distributed import sharded_histogram_emulated
+
+    img = gmm_image(64, 50, 9, 8)
+    ref = _full_histogram(img)
+    t = torch.from_numpy(img.reshape(-1).copy())
+    for w in (1, 2, 3, 5):
+        got = sharded_histogram_emulated(FakeHistBackend(), t, img.shape[0] * img.shape[1], w).numpy()
+        np.testing.assert_array_equal(got, ref)

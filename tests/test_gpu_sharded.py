@@ -269,3 +269,123 @@ def test_exchange_argument_errors():
     rc = lib.cqb_quantize_sharded(ctx.h, d.data_ptr(), 16, 4, C.byref(t), 1, None, None, None)
     assert rc == _native.CQB_ERR_INVALID_ARGUMENT and b"not mapped" in lib.cqb_last_error(ctx.h)
     ctx.close()
+
+
+# --------------------------------------------------------------------------- pixel-row sharded histogram
+def _morton_np(keys):
+    def spread(v):
+        v = v.astype(np.uint64) & 0xFF
+        v = (v | (v << 8)) & 0x0000F00F
+        v = (v | (v << 4)) & 0x000C30C3
+        v = (v | (v << 2)) & 0x00249249
+        return v
+    k = keys.astype(np.uint64)
+    return (spread(k >> 16) << 2) | (spread(k >> 8) << 1) | spread(k)
+
+
+def _full_triplets(img):
+    px = img.reshape(-1, 3).astype(np.uint32)
+    keys = (px[:, 0] << 16) | (px[:, 1] << 8) | px[:, 2]
+    u, first, counts = np.unique(keys, return_index=True, return_counts=True)
+    o = np.argsort(_morton_np(u), kind="stable")
+    return np.stack([u[o], counts[o], first[o]], 1).astype(np.uint32)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("case", ["gmm", "uniform", "ragged"])
+def test_row_sharded_histogram_matches_full(world, case):
+    """cqb_hist_rows (K1 over one rank's pixel rows with global pixel indices,
+    occupancy compaction, owner split) + cqb_hist_merge (count sum, first-pixel
+    min, owner-range compaction), W ranks emulated in one process: the owners'
+    lists concatenated are the whole image's Morton-ordered histogram, entry
+    for entry."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import DeviceHistBackend, sharded_histogram_emulated
+
+    img = {"gmm": lambda: gmm_image(384, 256, 48, 5), "uniform": lambda: uniform_image(2048, 2048, 9),
+           "ragged": lambda: gmm_image(1531, 1373, 64, 77)}[case]()
+    P = img.shape[0] * img.shape[1]
+    ctx = _native.Context(0)
+    try:
+        d = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+        got = sharded_histogram_emulated(DeviceHistBackend(ctx), d, P, world).cpu().numpy().view(np.uint32)
+    finally:
+        ctx.close()
+    np.testing.assert_array_equal(got, _full_triplets(img))
+
+
+@pytest.mark.parametrize("world", [0, 2, 8])
+def test_quantize_from_row_sharded_histogram(world):
+    """cqb_quantize_sharded_samples after the row-sharded histogram (world 0:
+    no exchange, the single-GPU pipeline from the given histogram; W: the
+    emulated in-kernel exchange) gives the single-GPU quantize bit for bit:
+    palette, iterations, dist_evals, MSE, index map and mapped raster."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import (DeviceHistBackend, PeerShardedQuantizer,
+                                                  sharded_histogram_emulated)
+
+    img = uniform_image(1024, 2048, 12)
+    k = 256
+    term = api.Termination.convergent(1e-4, 100)
+    single = api.quantize(img, k, term, seed=1)
+    P = img.shape[0] * img.shape[1]
+    ctx = _native.Context(0)
+    try:
+        d_img = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+        d_idx = torch.empty(P, dtype=torch.uint8, device="cuda")
+        d_rgb = torch.empty(3 * P, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        if world:
+            q = PeerShardedQuantizer(ctx=ctx, emulate=world)
+            lo, hi = q.enqueue_rows(d_img, P, k, term, 1, d_idx.data_ptr(), d_rgb.data_ptr())
+            centers, rep, hist = q.fetch()
+        else:
+            import ctypes as C
+
+            samples = sharded_histogram_emulated(DeviceHistBackend(ctx), d_img, P, 4)
+            rng = np.zeros(2, np.uint64)
+            t = term.native()
+            ctx.check(ctx.lib.cqb_quantize_sharded_samples(ctx.h, d_img.data_ptr(), P, samples.data_ptr(),
+                                                           samples.shape[0], k, C.byref(t), 1, d_idx.data_ptr(),
+                                                           d_rgb.data_ptr(), rng.ctypes.data_as(C.POINTER(C.c_uint64))))
+            centers = np.zeros(3 * k)
+            hist = np.zeros(term.iteration_budget)
+            rep = _native.Report()
+            ctx.check(ctx.lib.cqb_fetch_results(ctx.h, centers.ctypes.data_as(C.POINTER(C.c_double)),
+                                                hist.ctypes.data_as(C.POINTER(C.c_double)), term.iteration_budget,
+                                                C.byref(rep)))
+            centers = centers.reshape(k, 3)
+            lo, hi = int(rng[0]), int(rng[1])
+        assert (lo, hi) == (0, P)
+        np.testing.assert_array_equal(centers, single.palette)
+        assert rep.iterations == single.report.iterations and rep.dist_evals == single.report.dist_evals
+        assert rep.mse == single.report.mse and rep.n_unique == single.report.n_unique
+        np.testing.assert_array_equal(d_idx.cpu().numpy().reshape(img.shape[:2]), single.index_map)
+        np.testing.assert_array_equal(d_rgb.cpu().numpy().reshape(img.shape), single.mapped)
+    finally:
+        ctx.close()
+
+
+def test_hist_rows_argument_errors():
+    import torch
+
+    from paper_1011_0093_b200 import _native
+
+    ctx = _native.Context(0)
+    try:
+        d = torch.zeros(3 * 64, dtype=torch.uint8, device="cuda")
+        out = torch.empty((64, 3), dtype=torch.int32, device="cuda")
+        n = np.zeros(1, np.uint64)
+        cnt = np.zeros(16, np.uint64)
+        u64 = lambda a: a.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_uint64))  # noqa: E731
+        for world, rank, cap in ((0, 0, 64), (2, 2, 64), (9, 0, 64), (1, 0, 63)):
+            rc = ctx.lib.cqb_hist_rows(ctx.h, d.data_ptr(), 64, world, rank, out.data_ptr(), cap, u64(n), u64(cnt))
+            assert rc == _native.CQB_ERR_INVALID_ARGUMENT, (world, rank, cap)
+        assert ctx.lib.cqb_hist_rows(ctx.h, d.data_ptr(), 64, 1, 0, out.data_ptr(), 64, u64(n), u64(cnt)) == 0
+        assert int(n[0]) == 1 and int(cnt[0]) == 1
+    finally:
+        ctx.close()
