@@ -1775,7 +1775,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
         if (it <= L.hist_cap) L.sse_hist[it - 1] = sse;
         st->iterations = it;
         st->sse = sse;
-        st->n_empty_events += empt;
+        if (empt) st->n_empty_events += empt;  // (rare: no global read-modify-write on the critical path)
         if (stop) st->stop_it = it;
         S.stop_flag = stop;
         // pair evaluations of the incremental table update (kmeans.hpp:137-155)
