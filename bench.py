@@ -70,6 +70,7 @@ def _dist():
 
 
 E2E_INFLIGHT = 3  # concurrent host callers of the e2e measurement
+RED_PAIRS_PEAK = 106.3e9  # random RED pairs/s on a 32 MiB bin slice (profiles/r02/microbench_mem.txt)
 
 
 def _workload(cfg, k):
@@ -619,6 +620,17 @@ def _hbm_stages(stage_ms, P, n_unique, peaks):
             r = _roofline(st, stage_ms[st], P, n_unique, 1, 0, peaks, 0)
             out[st] = {"achieved_gbs": round(r["achieved"], 1), "frac": round(r["frac"], 4),
                        "algorithmic_bytes": r["algorithmic_bytes"], "ms": round(stage_ms[st], 4)}
+    if "hist_count" in out:
+        # K1's bound is the L2 atomic unit, not HBM: one RED pair (count add +
+        # first-pixel max on one 8-B bin) per pixel run, counted here as one
+        # per pixel (exact for uniform data), against the measured ceiling of
+        # random RED pairs on a 32 MiB table slice (tools/microbench_mem.cu)
+        ach = P / (stage_ms["hist_count"] * 1e-3)
+        out["hist_count"]["l2_atomic_roofline"] = {
+            "achieved_gpairs_s": round(ach / 1e9, 1), "peak_gpairs_s": RED_PAIRS_PEAK / 1e9,
+            "frac": round(ach / RED_PAIRS_PEAK, 4),
+            "peak_source": "measured: random RED.ADD+RED.MAX pairs over a 32 MiB slice, "
+                           "profiles/r02/microbench_mem.txt"}
     return out
 
 
