@@ -1245,9 +1245,18 @@ constexpr int XB_FLAG = 0;
 constexpr int XB_SEQ = XMAX * 16;
 constexpr int XB_PAY = XB_SEQ + 128;
 constexpr int XB_SLOT = 5 * KMAX;
-constexpr size_t XB_LAB_OFF = 256 * 1024;
+// the per-iteration moment exchange in "LL" words: each u64 sum travels as
+// two words {32 data bits, the exchange number's low 32 bits}, so a receiver
+// polls the data itself (8-B stores are single-copy atomic) — no sender
+// fence, no flag round trip
+constexpr int XB_LL_SLOT = 2 * 5 * KMAX;
+constexpr int XB_LL = XB_PAY + 2 * XMAX * XB_SLOT;
+constexpr size_t XB_LAB_OFF = 512 * 1024;
 constexpr size_t XB_BYTES = XB_LAB_OFF + (size_t(1) << 24);
-static_assert((XB_PAY + 2 * XMAX * XB_SLOT) * sizeof(unsigned long long) <= XB_LAB_OFF, "window layout");
+static_assert((XB_LL + 2 * XMAX * XB_LL_SLOT) * sizeof(unsigned long long) <= XB_LAB_OFF, "window layout");
+#ifndef CQB_XLL
+#define CQB_XLL 1
+#endif
 // A dead peer fails the call instead of hanging: LoopParams::xch_timeout_ns
 // (cqb_xch_set_timeout; default 5 s), and 4x that for the first exchange of
 // a launch, whose peers may still be starting their own launch.
@@ -1257,10 +1266,76 @@ __device__ __forceinline__ unsigned long long* xpay(unsigned long long* box, uns
   return box + XB_PAY + ((size_t)(s & 1) * XMAX + src) * XB_SLOT;
 }
 // Thread 0 only, after the payload stores are ordered by bar.sync: publish s.
+__device__ __forceinline__ unsigned long long* xll(unsigned long long* box, unsigned long long s, int src) {
+  return box + XB_LL + ((size_t)(s & 1) * XMAX + src) * XB_LL_SLOT;
+}
+// two LL words in one 16-B store (each 8-B half is single-copy atomic, which
+// is all the protocol needs)
+__device__ __forceinline__ void ll_store2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+// Spin until word p carries exchange tag `tag` (or the exchange failed).
+__device__ __forceinline__ unsigned long long ll_wait(const unsigned long long* p, uint32_t tag, int* status,
+                                                      unsigned long long t0, unsigned long long limit) {
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if ((uint32_t)(v >> 32) == tag) return v;
+    if (*reinterpret_cast<volatile int*>(status) == ST_XCH_TIMEOUT) return 0ull;
+    if (globaltimer() - t0 > limit) {
+      atomicExch(status, ST_XCH_TIMEOUT);
+      return 0ull;
+    }
+  }
+}
+
 __device__ __forceinline__ void xch_signal(unsigned long long* box, int src, unsigned long long s) {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(box + XB_FLAG + 16 * src), "l"(s) : "memory");
 }
+// The per-iteration K x 5 moment all-reduce in LL words (block-wide; inline:
+// out of line, the call's register save spills into the points loop): block pb < xw of every
+// part sends its part's sums to part pb; every block sums the xw sources.
+__device__ __forceinline__ void xch_moments_ll(unsigned long long* dst_box, unsigned long long* own, int part,
+                                            unsigned int pb, int xw,
+                                            unsigned long long s, int k, const unsigned long long* gacc,
+                                            unsigned long long* tot, bool silent, int* status,
+                                            unsigned long long limit) {
+  const int tid = threadIdx.x;
+  const uint32_t tag = (uint32_t)s;
+  if (pb < (unsigned)xw && !silent) {
+    unsigned long long* dst = xll(dst_box, s, part);
+    const unsigned long long hi = (unsigned long long)tag << 32;
+    for (int e = tid; e < 5 * KMAX; e += blockDim.x)
+      if ((e & (KMAX - 1)) < k) {
+        const unsigned long long v = __ldcg(&gacc[e]);
+        ll_store2(dst + 2 * e, (v & 0xffffffffull) | hi, (v >> 32) | hi);
+      }
+  }
+  const unsigned long long t0 = globaltimer();
+  for (int e = tid; e < 5 * KMAX; e += blockDim.x)
+    if ((e & (KMAX - 1)) < k) {
+      // two sources' words in flight at a time; only late words are polled
+      unsigned long long a = 0;
+      for (int r = 0; r < xw; r += 2) {
+        const unsigned long long* s0 = xll(own, s, r) + 2 * e;
+        const unsigned long long* s1 = xll(own, s, r + 1) + 2 * e;
+        ulonglong2 v0 = __ldcg(reinterpret_cast<const ulonglong2*>(s0));
+        ulonglong2 v1 = r + 1 < xw ? __ldcg(reinterpret_cast<const ulonglong2*>(s1)) : make_ulonglong2(0ull, 0ull);
+        if ((uint32_t)(v0.x >> 32) != tag) v0.x = ll_wait(s0, tag, status, t0, limit);
+        if ((uint32_t)(v0.y >> 32) != tag) v0.y = ll_wait(s0 + 1, tag, status, t0, limit);
+        a += (v0.x & 0xffffffffull) | ((v0.y & 0xffffffffull) << 32);
+        if (r + 1 < xw) {
+          if ((uint32_t)(v1.x >> 32) != tag) v1.x = ll_wait(s1, tag, status, t0, limit);
+          if ((uint32_t)(v1.y >> 32) != tag) v1.y = ll_wait(s1 + 1, tag, status, t0, limit);
+          a += (v1.x & 0xffffffffull) | ((v1.y & 0xffffffffull) << 32);
+        }
+      }
+      tot[e] = a;
+    }
+  __syncthreads();
+}
+
 // Block-wide: wait until all xw sources published exchange s into `box`.
 __device__ __forceinline__ void xch_wait(unsigned long long* box, int xw, unsigned long long s, int* status,
                                          unsigned long long timeout_ns) {
@@ -1648,22 +1723,28 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       const unsigned int pb = part_block<X>(S);
       // (debug flag 32768, tests only: part 1 goes silent at iteration 3 - a dead peer)
       const bool silent = (L.debug_flags & 32768) && part == 1 && it >= 3;
-      if (pb < (unsigned)L.xw && !silent) {  // block pb of every part sends to rank pb
-        unsigned long long* dst = xpay(L.xbox[pb], s, part);
-        for (int e = tid; e < 5 * KMAX; e += blockDim.x)
-          if ((e & (KMAX - 1)) < k) dst[e] = __ldcg(&gacc[e]);
-        __syncthreads();
-        if (tid == 0) xch_signal(L.xbox[pb], part, s);
-      }
-      unsigned long long* own = L.xbox[part];
-      xch_wait(own, L.xw, s, &st->status, it == 1 ? 4 * L.xch_timeout_ns : L.xch_timeout_ns);
-      for (int e = tid; e < 5 * KMAX; e += blockDim.x)
-        if ((e & (KMAX - 1)) < k) {
-          unsigned long long a = 0;
-          for (int r = 0; r < L.xw; ++r) a += __ldcg(xpay(own, s, r) + e);
-          tot[e] = a;
+      const unsigned long long limit = it == 1 ? 4 * L.xch_timeout_ns : L.xch_timeout_ns;
+      if (CQB_XLL) {
+        xch_moments_ll(pb < (unsigned)L.xw ? L.xbox[pb] : nullptr, L.xbox[part], part, pb, L.xw, s, k, gacc, tot,
+                       silent, &st->status, limit);
+      } else {
+        if (pb < (unsigned)L.xw && !silent) {  // block pb of every part sends to rank pb
+          unsigned long long* dst = xpay(L.xbox[pb], s, part);
+          for (int e = tid; e < 5 * KMAX; e += blockDim.x)
+            if ((e & (KMAX - 1)) < k) dst[e] = __ldcg(&gacc[e]);
+          __syncthreads();
+          if (tid == 0) xch_signal(L.xbox[pb], part, s);
         }
-      __syncthreads();
+        unsigned long long* own = L.xbox[part];
+        xch_wait(own, L.xw, s, &st->status, limit);
+        for (int e = tid; e < 5 * KMAX; e += blockDim.x)
+          if ((e & (KMAX - 1)) < k) {
+            unsigned long long a = 0;
+            for (int r = 0; r < L.xw; ++r) a += __ldcg(xpay(own, s, r) + e);
+            tot[e] = a;
+          }
+        __syncthreads();
+      }
     }
 
     // ---------------- finalize(it) ----------------
