@@ -54,9 +54,10 @@ def _args():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--shard", action="store_true",
                     help="shard the unique samples over the ranks (in-kernel NVLink exchange); default for cfg4 at N>1")
-    ap.add_argument("--hist", choices=["replicated", "rows"], default=None,
-                    help="sharded path: histogram replicated on every rank (default), or sharded by pixel "
-                         "rows with a Morton-range bin ownership exchange (cqb_hist_rows / cqb_hist_merge + NCCL)")
+    ap.add_argument("--hist", choices=["replicated", "rows", "morton"], default=None,
+                    help="sharded path: histogram replicated on every rank (default at N=1), sharded by pixel rows "
+                         "with a Morton-range bin ownership exchange (cqb_hist_rows / cqb_hist_merge + NCCL), or "
+                         "by Morton range over every pixel (cqb_hist_range + NCCL all-gather; default at N>1)")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="single GPU: W block groups of the loop act as W sharded ranks (exchange overhead)")
     return ap.parse_args()
@@ -750,11 +751,12 @@ def run_sharded(a, cfg, world, rank, local):
     d_out = torch.empty(3 * P, dtype=torch.uint8, device=dev)
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    rows = a.hist == "rows"
+    hist = a.hist or ("morton" if world > 1 else "replicated")
+    rows = hist in ("rows", "morton")
 
     def one():
-        if rows:  # histogram sharded by pixel rows too (cqb_hist_rows / cqb_hist_merge + NCCL all-to-all)
-            return q.enqueue_rows(d_img, P, k, term, INIT_SEED, d_idx.data_ptr(), d_out.data_ptr())
+        if rows:  # histogram sharded too (pixel rows + all-to-all, or Morton ranges), then all-gathered
+            return q.enqueue_rows(d_img, P, k, term, INIT_SEED, d_idx.data_ptr(), d_out.data_ptr(), split=hist)
         return q.enqueue(d_img.data_ptr(), P, k, term, INIT_SEED, d_idx.data_ptr(), d_out.data_ptr())
 
     def tmax(v):
@@ -847,8 +849,9 @@ def run_sharded(a, cfg, world, rank, local):
             "config": {"workload": _workload(cfg, k), "pixels": P, "n_unique": n_unique, "iterations": iters,
                        "k": k, "parallelism": (f"sample shards x{world}, in-kernel NVLink exchange" if world > 1 else
                                                f"sample shards x{ranks} emulated as block groups on one GPU"),
-                       "histogram": ("pixel-row shards, Morton-range bin owners, NCCL all-to-all + all-gather"
-                                     if rows else "replicated on every rank"),
+                       "histogram": {"rows": "pixel-row shards, Morton-range bin owners, NCCL all-to-all + all-gather",
+                                     "morton": "Morton-range shards over every pixel, NCCL all-gather"}.get(
+                                         hist, "replicated on every rank"),
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
                        "timed": "per-step CUDA events on the library stream; value = P*steps / max-rank sum"},
             "e2e": {"value": P * a.steps / e2e_s / 1e6, "unit": "Mpixel/s", "h2d_bytes_per_step": 3 * P,

@@ -335,6 +335,15 @@ int cqb_hist_rows(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int wor
                   uint64_t cap, uint64_t* n_out, uint64_t* owner_counts);
 int cqb_hist_merge(cqb_ctx* ctx, const uint32_t* d_in, uint64_t n_in, uint32_t* d_out, uint64_t cap,
                    uint64_t* n_out);
+/* Morton-range sharded histogram (the cheaper split when every rank holds the
+ * raster): rank r counts EVERY pixel but only into the bins of its Morton
+ * range (whole compaction tiles: [r T / W, (r+1) T / W) of T = 2048 tiles of
+ * 8192 bins), in L2-sized passes, and compacts that range into d_out
+ * (triplets as above, cap >= min(n_pixels, range bins)). No exchange is
+ * needed to finish the owners' lists; concatenated in rank order they are the
+ * whole histogram. */
+int cqb_hist_range(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int world, int rank, uint32_t* d_out,
+                   uint64_t cap, uint64_t* n_out);
 int cqb_quantize_sharded_samples(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, const uint32_t* d_samples,
                                  uint64_t n_unique, int k, const cqb_termination* term, uint64_t seed,
                                  uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range);

@@ -32,7 +32,7 @@ EXPORTS = (
     "cqb_loop_timeline", "cqb_block_times", "cqb_shard_prepare", "cqb_shard_step", "cqb_finalize_moments",
     "cqb_shard_reseed_candidate", "cqb_set_debug", "cqb_xch_window", "cqb_xch_open", "cqb_xch_emulate",
     "cqb_quantize_sharded", "cqb_xch_set_timeout", "cqb_init_centers", "cqb_points_tables", "cqb_points_assign",
-    "cqb_points_update", "cqb_points_sse", "cqb_run_wsm_points", "cqb_hist_rows", "cqb_hist_merge",
+    "cqb_points_update", "cqb_points_sse", "cqb_run_wsm_points", "cqb_hist_rows", "cqb_hist_merge", "cqb_hist_range",
     "cqb_quantize_sharded_samples",
 )
 IPC_HANDLE_BYTES = 64  # CQB_IPC_HANDLE_BYTES (cudaIpcMemHandle_t)
@@ -142,6 +142,7 @@ def load_library() -> C.CDLL:
         L.cqb_quantize_sharded.argtypes = [_vp, _vp, C.c_uint64, C.c_int, _T, C.c_uint64, _vp, _vp, _u64p]
         L.cqb_hist_rows.argtypes = [_vp, _vp, C.c_uint64, C.c_int, C.c_int, _vp, C.c_uint64, _u64p, _u64p]
         L.cqb_hist_merge.argtypes = [_vp, _vp, C.c_uint64, _vp, C.c_uint64, _u64p]
+        L.cqb_hist_range.argtypes = [_vp, _vp, C.c_uint64, C.c_int, C.c_int, _vp, C.c_uint64, _u64p]
         L.cqb_quantize_sharded_samples.argtypes = [_vp, _vp, C.c_uint64, _vp, C.c_uint64, C.c_int, _T, C.c_uint64,
                                                    _vp, _vp, _u64p]
         _lib = L

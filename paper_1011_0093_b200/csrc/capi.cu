@@ -2135,6 +2135,48 @@ int cqb_hist_merge(cqb_ctx* ctx, const uint32_t* d_in, uint64_t n_in, uint32_t* 
   return CQB_OK;
 }
 
+int cqb_hist_range(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, int world, int rank, uint32_t* d_out,
+                   uint64_t cap, uint64_t* n_out) {
+  if (!ctx) return CQB_ERR_INVALID_ARGUMENT;
+  if (world < 1 || world > XMAX || rank < 0 || rank >= world)
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_range: rank %d of world %d (1..%d ranks)", rank, world, XMAX);
+  if (!d_rgb || !d_out || !n_out) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_range: null buffer");
+  if (n_pixels == 0 || n_pixels >= 0xffffffffull)
+    return fail(ctx, CQB_ERR_UNSUPPORTED, "hist_range: 1 .. 2^32-2 pixels");
+  if (!aligned16(d_rgb)) return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_range: the raster must be 16-B aligned");
+  CK(cudaSetDevice(ctx->device));
+  // this rank's Morton range: whole K2b tiles [t0, t1)
+  const uint32_t t0 = (uint32_t)((uint64_t)N_BIN_TILES * rank / world), t1 = (uint32_t)((uint64_t)N_BIN_TILES * (rank + 1) / world);
+  const uint32_t mlo = t0 * BIN_TILE, mhi = t1 * BIN_TILE;
+  const uint64_t range = (uint64_t)(mhi - mlo);
+  if (cap < std::min<uint64_t>(n_pixels, range))
+    return fail(ctx, CQB_ERR_INVALID_ARGUMENT, "hist_range: capacity %llu < %llu", (unsigned long long)cap,
+                (unsigned long long)std::min<uint64_t>(n_pixels, range));
+  TRY(ensure_samples(ctx, std::min<uint64_t>(n_pixels, range)));
+  // K1 over every pixel, atomics only for this range, in L2-sized slices (32 MiB of bins each)
+  const uint64_t nchunk = (n_pixels + PX_PER_THREAD - 1) / PX_PER_THREAD;
+  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+  const int passes = (int)std::max<uint64_t>(1, (range * sizeof(uint2) + (32ull << 20) - 1) / (32ull << 20));
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t a = mlo + (uint32_t)(range * p / passes), b = mlo + (uint32_t)(range * (p + 1) / passes);
+    k_hist_count<<<std::max(g1, 1), HIST_THREADS, 0, ctx->stream>>>(d_rgb, n_pixels, ctx->bins, a, b, nullptr);
+    CKL();
+  }
+  CK(cudaMemsetAsync(ctx->bin_tile_state, 0, sizeof(unsigned long long) * (t1 - t0 + 1), ctx->stream));
+  k_bins_compact<<<t1 - t0, BC_THREADS, 0, ctx->stream>>>(
+      ctx->bins, ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->bin_tile_state,
+      reinterpret_cast<unsigned int*>(ctx->bin_tile_state + (t1 - t0)), ctx->d_n, nullptr, 1, t0);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_scalar, ctx->d_n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  const int gp = (int)std::min<uint64_t>((std::min<uint64_t>(n_pixels, range) + 255) / 256, (uint64_t)ctx->num_sms * 8);
+  k_pack_triplets<<<std::max(gp, 1), 256, 0, ctx->stream>>>(ctx->d_mkeys, ctx->d_mcounts, ctx->d_mrank, ctx->d_n,
+                                                            d_out, 0, nullptr);
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n_out = ctx->h_scalar[0];
+  return CQB_OK;
+}
+
 int cqb_quantize_sharded_samples(cqb_ctx* ctx, const uint8_t* d_rgb, uint64_t n_pixels, const uint32_t* d_samples,
                                  uint64_t n_unique, int k, const cqb_termination* term, uint64_t seed,
                                  uint8_t* d_index_out, uint8_t* d_rgb_out, uint64_t* px_range) {

@@ -112,7 +112,10 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
                                                              uint32_t* __restrict__ m_rank,
                                                              unsigned long long* tile_state, unsigned int* ticket,
                                                              unsigned long long* n_unique,
-                                                             uint32_t* __restrict__ bitmap, int first_mode) {
+                                                             uint32_t* __restrict__ bitmap, int first_mode,
+                                                             uint32_t tile_base = 0) {
+  // tile_base: the launch compacts tiles [tile_base, tile_base + gridDim.x)
+  // of the table (a Morton range), its output starting at index 0
   constexpr int NW = BC_THREADS / 32;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t wbase = tile * BIN_TILE + wid * (64 * BC_STEPS);
+  const uint32_t wbase = (tile_base + tile) * BIN_TILE + wid * (64 * BC_STEPS);
   const unsigned lt = (1u << lane) - 1u;
   uint4 v[BC_STEPS];
   uint32_t off[BC_STEPS];
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(BC_THREADS) k_bins_compact(uint2* __restrict__
       reinterpret_cast<uint4*>(bins + wbase + q * 64)[lane] = make_uint4(0u, 0u, 0u, 0u);
     }
   }
-  if (tile == N_BIN_TILES - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
+  if (tile == gridDim.x - 1 && tid == 0) *n_unique = (unsigned long long)(s_prefix + block_total);
 }
 
 // K2b for sparse tables (small images): the same Morton-order samples as

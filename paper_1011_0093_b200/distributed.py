@@ -266,21 +266,25 @@ class PeerShardedQuantizer:
         return int(rng[0]), int(rng[1])
 
     def enqueue_rows(self, img, n_pixels: int, k: int, term, seed: int = 1, d_index: int | None = None,
-                     d_rgb_out: int | None = None, group=None) -> tuple[int, int]:
-        """cqb_quantize_sharded with the histogram sharded by pixel rows too
-        (``img``: the raster as a CUDA uint8 tensor on every rank): this rank
-        counts only its rows, the owners merge, the whole histogram is
-        all-gathered (NCCL), then the loop and the map run as in enqueue."""
+                     d_rgb_out: int | None = None, group=None, split: str = "rows") -> tuple[int, int]:
+        """cqb_quantize_sharded with the histogram sharded too (``img``: the
+        raster as a CUDA uint8 tensor on every rank). split="rows": this rank
+        counts only its pixel rows, the owners merge (all-to-all);
+        split="morton": this rank counts every pixel into its own Morton range
+        of bins. Either way the whole histogram is then all-gathered (NCCL)
+        and the loop and the map run as in enqueue."""
         backend = DeviceHistBackend(self.ctx)
+        emu = sharded_histogram_emulated if split == "rows" else sharded_histogram_morton_emulated
+        real = sharded_histogram if split == "rows" else sharded_histogram_morton
         if self.emulated:
-            samples = sharded_histogram_emulated(backend, img, n_pixels, self.world)
+            samples = emu(backend, img, n_pixels, self.world)
         else:
             import torch.distributed as dist
 
             if dist.is_available() and dist.is_initialized():
-                samples = sharded_histogram(backend, img, n_pixels, TensorExchange(group))
+                samples = real(backend, img, n_pixels, TensorExchange(group))
             else:
-                samples = sharded_histogram_emulated(backend, img, n_pixels, 1)
+                samples = emu(backend, img, n_pixels, 1)
         self._samples = samples  # alive until the enqueued work has read it (fetch)
         rng = np.zeros(2, np.uint64)
         t = term.native()
@@ -348,6 +352,20 @@ class DeviceHistBackend:
                                               out.shape[0], C.byref(n), counts.ctypes.data_as(_u64p)))
         return out[: n.value], [int(c) for c in counts]
 
+    def range(self, img, n_pixels: int, world: int, rank: int):
+        """cqb_hist_range: every pixel counted into this rank's Morton range
+        only; returns its owner list (Morton-ordered triplets)."""
+        import torch
+
+        tiles = 2048
+        t0, t1 = tiles * rank // world, tiles * (rank + 1) // world
+        cap = max(1, min(n_pixels, (t1 - t0) * 8192))
+        out = torch.empty((cap, 3), dtype=torch.int32, device=img.device)
+        n = C.c_uint64()
+        self.ctx.check(self.lib.cqb_hist_range(self.ctx.h, img.data_ptr(), n_pixels, world, rank, out.data_ptr(),
+                                               cap, C.byref(n)))
+        return out[: n.value]
+
     def merge(self, recv, world: int):
         import torch
 
@@ -408,6 +426,27 @@ def sharded_histogram(backend, img, n_pixels: int, exchange):
     _sync(recv)
     own = backend.merge(recv, exchange.world)
     out = exchange.allgatherv(own)
+    _sync(out)
+    return out
+
+
+def sharded_histogram_morton(backend, img, n_pixels: int, exchange):
+    """Morton-range split: every rank holds the raster and counts all its
+    pixels, but only into the bins of its own Morton range (no all-to-all:
+    each owner list is complete); the lists are all-gathered (NCCL)."""
+    _sync(img)
+    own = backend.range(img, n_pixels, exchange.world, exchange.rank)
+    out = exchange.allgatherv(own)
+    _sync(out)
+    return out
+
+
+def sharded_histogram_morton_emulated(backend, img, n_pixels: int, world: int):
+    """The Morton-range split in one process (single-GPU check)."""
+    import torch
+
+    _sync(img)
+    out = torch.cat([backend.range(img, n_pixels, world, r) for r in range(world)])
     _sync(out)
     return out
 

@@ -436,6 +436,15 @@ class FakeHistBackend:
         bounds = [int(np.searchsorted(m, ((o << 24) // world))) for o in range(world)] + [len(m)]
         return t, [bounds[o + 1] - bounds[o] for o in range(world)]
 
+    def range(self, img, n_pixels, world, rank):
+        t0, t1 = 2048 * rank // world, 2048 * (rank + 1) // world
+        px = img.numpy().reshape(-1, 3).astype(np.uint32)
+        keys = (px[:, 0] << 16) | (px[:, 1] << 8) | px[:, 2]
+        u, first, counts = np.unique(keys, return_index=True, return_counts=True)
+        m = _morton(u)
+        sel = (m >= t0 * 8192) & (m < t1 * 8192)
+        return self._emit(u[sel], counts[sel], first[sel])
+
     def merge(self, recv, world):
         a = recv.numpy().view(np.uint32).astype(np.int64)
         if len(a) == 0:
@@ -454,25 +463,26 @@ def _full_histogram(img):
     return FakeHistBackend._emit(u, counts, first).numpy()
 
 
-def _hist_worker(rank, world, port, img, out_q):
+def _hist_worker(rank, world, port, img, out_q, split="rows"):
     import torch
     import torch.distributed as dist
 
-    from paper_1011_0093_b200.distributed import TensorExchange, sharded_histogram
+    from paper_1011_0093_b200.distributed import TensorExchange, sharded_histogram, sharded_histogram_morton
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         t = torch.from_numpy(img.reshape(-1).copy())
-        out = sharded_histogram(FakeHistBackend(), t, img.shape[0] * img.shape[1], TensorExchange())
+        fn = sharded_histogram if split == "rows" else sharded_histogram_morton
+        out = fn(FakeHistBackend(), t, img.shape[0] * img.shape[1], TensorExchange())
         out_q.put((rank, out.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_sharded_histogram_matches_full(world):
+@pytest.mark.parametrize("world,split", [(2, "rows"), (3, "rows"), (2, "morton"), (3, "morton")])
+def test_gloo_sharded_histogram_matches_full(world, split):
     """Pixel-row sharded histogram through the real exchange code
     (TensorExchange: all-to-all of the owners' runs, all-gather of the owner
     lists) over gloo: every rank ends with the whole image's Morton-ordered
@@ -483,7 +493,7 @@ def test_gloo_sharded_histogram_matches_full(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_hist_worker, args=(r, world, port, img, q)) for r in range(world)]
+    procs = [ctx.Process(target=_hist_worker, args=(r, world, port, img, q, split)) for r in range(world)]
     for p in procs:
         p.start()
     outs = sorted([q.get(timeout=240) for _ in procs], key=lambda o: o[0])

@@ -389,3 +389,60 @@ def test_hist_rows_argument_errors():
         assert int(n[0]) == 1 and int(cnt[0]) == 1
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("case", ["gmm", "uniform", "ragged"])
+def test_morton_range_histogram_matches_full(world, case):
+    """cqb_hist_range (every pixel counted into one rank's Morton range of
+    whole compaction tiles, L2-sized passes, range-only compaction), W ranks
+    emulated in one process: the owner lists concatenated are the whole
+    image's Morton-ordered histogram, entry for entry."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import DeviceHistBackend, sharded_histogram_morton_emulated
+
+    img = {"gmm": lambda: gmm_image(384, 256, 48, 5), "uniform": lambda: uniform_image(2048, 2048, 9),
+           "ragged": lambda: gmm_image(1531, 1373, 64, 77)}[case]()
+    P = img.shape[0] * img.shape[1]
+    ctx = _native.Context(0)
+    try:
+        d = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+        got = sharded_histogram_morton_emulated(DeviceHistBackend(ctx), d, P, world).cpu().numpy().view(np.uint32)
+    finally:
+        ctx.close()
+    np.testing.assert_array_equal(got, _full_triplets(img))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_quantize_from_morton_range_histogram(world):
+    """The Morton-range histogram feeding the emulated in-kernel exchange:
+    bit-identical to the single-GPU quantize."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import PeerShardedQuantizer
+
+    img = uniform_image(1024, 2048, 13)
+    k = 256
+    term = api.Termination.convergent(1e-4, 100)
+    single = api.quantize(img, k, term, seed=1)
+    P = img.shape[0] * img.shape[1]
+    ctx = _native.Context(0)
+    try:
+        d_img = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+        d_idx = torch.empty(P, dtype=torch.uint8, device="cuda")
+        d_rgb = torch.empty(3 * P, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        q = PeerShardedQuantizer(ctx=ctx, emulate=world)
+        lo, hi = q.enqueue_rows(d_img, P, k, term, 1, d_idx.data_ptr(), d_rgb.data_ptr(), split="morton")
+        centers, rep, hist = q.fetch()
+        assert (lo, hi) == (0, P)
+        np.testing.assert_array_equal(centers, single.palette)
+        assert rep.iterations == single.report.iterations and rep.dist_evals == single.report.dist_evals
+        assert rep.mse == single.report.mse
+        np.testing.assert_array_equal(d_idx.cpu().numpy().reshape(img.shape[:2]), single.index_map)
+        np.testing.assert_array_equal(d_rgb.cpu().numpy().reshape(img.shape), single.mapped)
+    finally:
+        ctx.close()

@@ -33,3 +33,10 @@ for rep in range(3):
     t3 = time.perf_counter()
 print(f"{cfg.name} W={W}: hist_rows per rank {(t1 - t0) / W * 1e3:.3f} ms (local samples {runs[0][0].shape[0]}), "
       f"merge of owner 0 ({recv.shape[0]} in -> {own.shape[0]} out) {(t3 - t2) * 1e3:.3f} ms")
+
+# the Morton-range split: every pixel, one range of bins per rank
+for rep in range(3):
+    t0 = time.perf_counter()
+    own = [be.range(d, P, W, r) for r in range(W)]
+    t1 = time.perf_counter()
+print(f"{cfg.name} W={W}: hist_range per rank {(t1 - t0) / W * 1e3:.3f} ms (rank 0 owns {own[0].shape[0]} samples)")
