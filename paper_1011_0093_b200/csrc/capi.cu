@@ -409,8 +409,12 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
   const uint32_t n_words = (uint32_t)((P + 31) / 32);
   const uint32_t ntiles = (n_words + BS_WORDS - 1) / BS_WORDS;
   const bool fused = fused_prep(ctx, P);
-  if (!(fused && zero_state)) CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
-  if (!fused) CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
+  // the dense quantize path (K2b without the bitmap + rank selection) uses
+  // neither the first-occurrence bitmap nor the bitmap-scan look-back state
+  const bool no_bitmap = !sparse_path(ctx, P) && !rank_order;
+  if (!(fused && zero_state) && !no_bitmap)
+    CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
+  if (!fused && !no_bitmap) CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
   const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
   // Sparse tables (small images) are compacted through the occupancy map;
