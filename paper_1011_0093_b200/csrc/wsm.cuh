@@ -839,7 +839,7 @@ __device__ void sched_sort(uint32_t my_ch) {
 // evaluate the candidates below it with no per-entry check: a deep scan is a
 // few L2 round trips instead of one per two entries.
 #ifndef CQB_DEEP_J
-#define CQB_DEEP_J 13
+#define CQB_DEEP_J 17
 #endif
 #ifndef CQB_DEEP_P
 #define CQB_DEEP_P 3
