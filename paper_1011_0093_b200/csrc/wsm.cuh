@@ -37,6 +37,9 @@
 #ifndef CQB_Q0
 #define CQB_Q0 1  // large path: first row quads staged in shared memory
 #endif
+#ifndef CQB_D1_PPT
+#define CQB_D1_PPT 4  // iteration 1 (dense, integer): samples per thread per step
+#endif
 #ifndef CQB_Q0_SMALL
 #define CQB_Q0_SMALL 0  // ... also on the small path
 #endif
@@ -576,7 +579,16 @@ __device__ __forceinline__ void acc_point_warp(uint2* acc, bool valid, int lab, 
 // integer arithmetic on integer centers: the candidate list always contains
 // the lexicographic (d, index) minimum. One block per cell, one thread per
 // center; a cell with more than CAND_CAP candidates falls back to all k.
-constexpr int CAND_CELLS = 16 * 16 * 16;
+#ifndef CQB_CAND_BITS
+#define CQB_CAND_BITS 4  // iteration-1 cells per axis = 2^bits (cell side 256 >> bits colors)
+#endif
+constexpr int CAND_AXIS = 1 << CQB_CAND_BITS, CAND_SIDE = 256 >> CQB_CAND_BITS;
+constexpr int CAND_CELLS = CAND_AXIS * CAND_AXIS * CAND_AXIS;
+__device__ __forceinline__ int cand_cell(uint32_t key) {
+  constexpr int sh = 8 - CQB_CAND_BITS, m = CAND_AXIS - 1;
+  return (int)((((key >> (16 + sh)) & m) << (2 * CQB_CAND_BITS)) | (((key >> (8 + sh)) & m) << CQB_CAND_BITS) |
+               ((key >> sh) & m));
+}
 constexpr int CAND_CAP = 64;
 constexpr uint16_t CAND_OVERFLOW = 0xFFFF;
 
@@ -586,13 +598,14 @@ __global__ void __launch_bounds__(KMAX) k_grid_cands(const WsmState* __restrict_
   __shared__ int s_cnt[KMAX / 32];
   const int cell = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   if (st->status != ST_OK) return;
-  const int lo[3] = {(cell >> 8) * 16, ((cell >> 4) & 15) * 16, (cell & 15) * 16};
+  const int lo[3] = {(cell >> (2 * CQB_CAND_BITS)) * CAND_SIDE, ((cell >> CQB_CAND_BITS) & (CAND_AXIS - 1)) * CAND_SIDE,
+                     (cell & (CAND_AXIS - 1)) * CAND_SIDE};
   int mind2 = 0, maxd2 = 0x7fffffff;
   if (t < k) {
     maxd2 = 0;
     for (int ch = 0; ch < 3; ++ch) {
       const int c = (int)st->C[0][3 * t + ch];  // initial centers are sample colors: integers
-      const int a = lo[ch], b = lo[ch] + 15;
+      const int a = lo[ch], b = lo[ch] + CAND_SIDE - 1;
       const int below = a - c, above = c - b;
       const int dn = below > 0 ? below : (above > 0 ? above : 0);
       const int fa = c - a, fb = b - c;
@@ -635,7 +648,7 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
   const int lane = threadIdx.x & 31;
   const int cc0 = S.cb[0].y >> 8;  // |c_0|^2
   const uint32_t c0 = (uint32_t)S.cb[0].x;
-  constexpr int PPT = 4;
+  constexpr int PPT = CQB_D1_PPT;
   for (unsigned long long base = lo + (unsigned long long)pb * blockDim.x + threadIdx.x; base - lane < bhi;
        base += PPT * T) {
     uint32_t x[PPT];
@@ -650,7 +663,7 @@ __device__ void assign_dense_first(LoopSmem& S, const LoopParams& L, unsigned lo
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         const uint32_t xk = x[q];
-        const int cell = (int)(((xk >> 20) & 15) << 8 | ((xk >> 12) & 15) << 4 | ((xk >> 4) & 15));
+        const int cell = cand_cell(xk);
         const int nc = L.cand_n[cell];
         if (nc == CAND_OVERFLOW) {
           for (int t = 0; t < k; ++t) {
