@@ -27,6 +27,9 @@ using namespace cqb;
 namespace {
 
 constexpr int XFER_CHUNKS = 8;
+#ifndef CQB_K1_GRID
+#define CQB_K1_GRID 32  // K1 blocks per SM (grid-stride over 16-pixel chunks; 4/8/16/32: 249/247/231/226 us on cfg4)
+#endif
 constexpr int DBG_NO_COARSE = 1 << 21;  // (see below)
 constexpr int DBG_K1_2PASS = 1 << 22;   // debug flag: K1 in two half-table passes (A/B)
 constexpr int DBG_K1_1PASS = 1 << 23;   // debug flag: K1 in one pass (A/B)  // debug flag: k_map_pixels with per-pixel LUT gathers only (A/B)
@@ -416,7 +419,7 @@ int enqueue_histogram(cqb_ctx* ctx, const uint8_t* d_img, uint64_t P, bool stamp
     CK(cudaMemsetAsync(ctx->d_bitmap, 0, sizeof(uint32_t) * n_words, ctx->stream));
   if (!fused && !no_bitmap) CK(cudaMemsetAsync(ctx->tile_state, 0, sizeof(unsigned long long) * (ntiles + 1), ctx->stream));
   if (stamps && ctx->profiling) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
-  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * 16);
+  const int g1 = (int)std::min<uint64_t>((nchunk + HIST_THREADS - 1) / HIST_THREADS, (uint64_t)ctx->num_sms * CQB_K1_GRID);
   // Sparse tables (small images) are compacted through the occupancy map;
   // dense ones by scanning all 128 MiB (k_bins_compact), whose K1 runs in
   // 4 Morton slices so each pass's atomics stay in L2.
