@@ -95,8 +95,14 @@ __global__ void k_bins_scatter(const uint32_t* __restrict__ keys, const uint32_t
 // A warp streams 512 consecutive bins as 8 coalesced 512-B steps (one 16-B
 // load = 2 bins per lane); in-order output offsets come from two ballots per
 // step. Tiles of 8192 bins (16 warps), decoupled look-back across tiles.
-constexpr int BC_THREADS = 512;
-constexpr int BC_STEPS = 8;
+#ifndef CQB_BC_THREADS
+#define CQB_BC_THREADS 512
+#endif
+constexpr int BC_THREADS = CQB_BC_THREADS;
+#ifndef CQB_BC_STEPS
+#define CQB_BC_STEPS 8
+#endif
+constexpr int BC_STEPS = CQB_BC_STEPS;
 constexpr int BIN_TILE = (BC_THREADS / 32) * 64 * BC_STEPS;
 constexpr int N_BIN_TILES = (1 << 24) / BIN_TILE;
 
