@@ -357,9 +357,8 @@ class DeviceHistBackend:
         only; returns its owner list (Morton-ordered triplets)."""
         import torch
 
-        tiles = 2048
-        t0, t1 = tiles * rank // world, tiles * (rank + 1) // world
-        cap = max(1, min(n_pixels, (t1 - t0) * 8192))
+        # the range is whole compaction tiles (<= 16384 bins each) around 2^24 / world bins
+        cap = max(1, min(n_pixels, (1 << 24) // world + (1 << 14)))
         out = torch.empty((cap, 3), dtype=torch.int32, device=img.device)
         n = C.c_uint64()
         self.ctx.check(self.lib.cqb_hist_range(self.ctx.h, img.data_ptr(), n_pixels, world, rank, out.data_ptr(),
