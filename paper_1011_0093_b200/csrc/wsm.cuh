@@ -37,6 +37,9 @@
 #ifndef CQB_Q0
 #define CQB_Q0 1  // large path: first row quads staged in shared memory
 #endif
+#ifndef CQB_DIAG_COUNTS
+#define CQB_DIAG_COUNTS 1  // per-iteration changed / active sample counts for the profiling timeline
+#endif
 #ifndef CQB_D1_PPT
 #define CQB_D1_PPT 4  // iteration 1 (dense, integer): samples per thread per step
 #endif
@@ -887,7 +890,7 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
   }
   // the common case: no candidate (kmeans.hpp:220-226 breaks at j = 1); k = 1: D.x = +inf
   if (D.x >= pl) return D.x >= pu ? 1 : 0;
-  n_active += 1;
+  if (CQB_DIAG_COUNTS) n_active += 1;
   float bd = prev, d2 = F32_INF;
   int best = p;
   auto eval = [&](uint32_t t) {
@@ -1112,7 +1115,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
 #if CQB_DIAG_FALLBACK  // diagnostics build: the timeline's "active" count = FP64 fallbacks of scan_f32
         n_active += use32 ? 1000000u : 0u;
 #else
-        n_active += (unsigned)(r >> 24) & 1u;
+        if (CQB_DIAG_COUNTS) n_active += (unsigned)(r >> 24) & 1u;
 #endif
       }
       ev += (uint32_t)J;  // prev + (J - 1) candidates: the reference's count
@@ -1142,7 +1145,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       }
       if (ch) {
         labels[i] = (uint8_t)nlab[q];
-        ++n_changed;
+        if (CQB_DIAG_COUNTS) ++n_changed;
       }
       if (full) {
         acc_point_warp(S.accp, v, nlab[q], key[q], cnt);
