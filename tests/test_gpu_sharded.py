@@ -446,3 +446,37 @@ def test_quantize_from_morton_range_histogram(world):
         np.testing.assert_array_equal(d_rgb.cpu().numpy().reshape(img.shape), single.mapped)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("split", ["rows", "morton"])
+def test_sharded_histogram_edge_cases(split):
+    """Both histogram splits on the edges: one pixel, fewer 16-pixel chunks than
+    ranks (empty row shards), one color everywhere, and every one of the 2^24
+    colors once (every Morton range full)."""
+    import torch
+
+    from paper_1011_0093_b200 import _native
+    from paper_1011_0093_b200.distributed import (DeviceHistBackend, sharded_histogram_emulated,
+                                                  sharded_histogram_morton_emulated)
+
+    fn = sharded_histogram_emulated if split == "rows" else sharded_histogram_morton_emulated
+    rng = np.random.default_rng(3)
+    allc = np.arange(1 << 24, dtype=np.uint32)
+    rng.shuffle(allc)
+    cases = [
+        rng.integers(0, 256, (1, 1, 3), dtype=np.uint8),
+        rng.integers(0, 256, (1, 17, 3), dtype=np.uint8),
+        np.full((64, 48, 3), 77, np.uint8),
+        np.stack([(allc >> 16) & 255, (allc >> 8) & 255, allc & 255], 1).astype(np.uint8).reshape(4096, 4096, 3),
+    ]
+    ctx = _native.Context(0)
+    try:
+        for img in cases:
+            P = img.shape[0] * img.shape[1]
+            d = torch.zeros(3 * P + 16, dtype=torch.uint8, device="cuda")  # (16-B aligned)
+            d[: 3 * P] = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+            for world in (1, 3, 8):
+                got = fn(DeviceHistBackend(ctx), d, P, world).cpu().numpy().view(np.uint32)
+                np.testing.assert_array_equal(got, _full_triplets(img))
+    finally:
+        ctx.close()
