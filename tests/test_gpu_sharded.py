@@ -1,6 +1,8 @@
 """GPU: the sharded device path (cqb_shard_* + cqb_finalize_moments) run as W
 virtual shards on one GPU equals the oracle / single-GPU run — the exactness
 that makes the N-GPU run bit-identical (integer moments, fixed finalize)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -480,3 +482,40 @@ def test_sharded_histogram_edge_cases(split):
                 np.testing.assert_array_equal(got, _full_triplets(img))
     finally:
         ctx.close()
+
+
+def test_sharded_histogram_over_nccl_world1(tmp_path):
+    """The NCCL leg of the sharded histograms (TensorExchange: all-to-all and
+    all-gather of CUDA int32 triplets) in a one-rank NCCL process group (a
+    subprocess): both splits return the full histogram. The multi-rank logic
+    of the same code runs over gloo in tests/test_distributed.py."""
+    import subprocess
+    import sys
+    import textwrap
+
+    code = textwrap.dedent("""
+        import os, sys, numpy as np, torch, torch.distributed as dist
+        sys.path.insert(0, os.getcwd())
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29000 + os.getpid() % 1000))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        from paper_1011_0093_b200 import _native
+        from paper_1011_0093_b200.configs import gmm_image
+        from paper_1011_0093_b200.distributed import (DeviceHistBackend, TensorExchange, sharded_histogram,
+                                                      sharded_histogram_morton)
+        img = gmm_image(1531, 1373, 64, 77)
+        P = img.shape[0] * img.shape[1]
+        d = torch.from_numpy(np.ascontiguousarray(img).reshape(-1)).cuda()
+        ctx = _native.Context(0)
+        for name, fn in (("rows", sharded_histogram), ("morton", sharded_histogram_morton)):
+            got = fn(DeviceHistBackend(ctx), d, P, TensorExchange()).cpu().numpy().view(np.uint32)
+            np.save(os.path.join(sys.argv[1], name + ".npy"), got)
+        ctx.close()
+        dist.destroy_process_group()
+        print("ok")
+    """)
+    r = subprocess.run([sys.executable, "-c", code, str(tmp_path)], capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+    ref = _full_triplets(gmm_image(1531, 1373, 64, 77))
+    for name in ("rows", "morton"):
+        np.testing.assert_array_equal(np.load(tmp_path / (name + ".npy")), ref)
