@@ -134,7 +134,8 @@ def test_run_wsm_matches_oracle(case, k, images, port):
     else:
         np.testing.assert_allclose(g.palette, o.centers, rtol=CENTER_RTOL)
         np.testing.assert_allclose(g.trajectory, o.trajectory, rtol=CENTER_RTOL)
-        assert abs(g.report.dist_evals - o.dist_evals) <= 1e-6 * o.dist_evals
+        # the ~1e-13 center differences never move a break decision here: exact
+        assert g.report.dist_evals == o.dist_evals
 
 
 def test_run_wsm_fixed_and_seeds(images, port):
