@@ -22,6 +22,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "colorq.hpp"
@@ -110,65 +111,89 @@ inline RgbImage read_ppm(std::span<const unsigned char> bytes) {
   return img;
 }
 
+namespace io_detail {
+
+// Whole-file reads and writes over C stdio (one fread / fwrite of the payload).
+inline std::vector<unsigned char> slurp(const std::filesystem::path& path, const char* mode) {
+  std::FILE* f = std::fopen(path.c_str(), mode);
+  if (!f) throw std::runtime_error("cannot open " + path.string());
+  std::vector<unsigned char> bytes;
+  unsigned char chunk[1 << 16];
+  for (std::size_t n; (n = std::fread(chunk, 1, sizeof chunk, f)) > 0;) bytes.insert(bytes.end(), chunk, chunk + n);
+  std::fclose(f);
+  return bytes;
+}
+
+inline void spill(const std::filesystem::path& path, const char* mode, const void* data, std::size_t n) {
+  std::FILE* f = std::fopen(path.c_str(), mode);
+  if (!f) throw std::runtime_error("cannot open " + path.string() + " for writing");
+  const bool ok = std::fwrite(data, 1, n, f) == n;
+  if (std::fclose(f) != 0 || !ok) throw std::runtime_error("write failed: " + path.string());
+}
+
+// One palette line: three stream-extracted doubles (the reference's reader accepts what
+// operator>> accepts and ignores anything after the third value).
+inline bool parse_center(std::string_view line, Vec3& c) {
+  std::istringstream ls{std::string(line)};
+  return bool(ls >> c[0] >> c[1] >> c[2]);
+}
+
+}  // namespace io_detail
+
+// "P6\n<w> <h>\n255\n" then the raw RGB bytes.
 inline std::vector<unsigned char> write_ppm(const RgbImage& img) {
-  const std::string head = "P6\n" + std::to_string(img.width) + " " + std::to_string(img.height) + "\n255\n";
-  std::vector<unsigned char> out(head.size() + img.size() * 3);
-  std::memcpy(out.data(), head.data(), head.size());
-  std::memcpy(out.data() + head.size(), img.pixels.data(), img.size() * 3);
+  char head[64];
+  const int hn = std::snprintf(head, sizeof head, "P6\n%d %d\n255\n", img.width, img.height);
+  std::vector<unsigned char> out(std::size_t(hn) + img.size() * 3);
+  std::memcpy(out.data(), head, std::size_t(hn));
+  std::memcpy(out.data() + hn, img.pixels.data(), img.size() * 3);
   return out;
 }
 
-inline RgbImage load_ppm(const std::filesystem::path& path) {
-  std::ifstream f(path, std::ios::binary);
-  if (!f) throw std::runtime_error("cannot open " + path.string());
-  const std::vector<unsigned char> bytes((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
-  return read_ppm(bytes);
-}
+inline RgbImage load_ppm(const std::filesystem::path& path) { return read_ppm(io_detail::slurp(path, "rb")); }
 
 inline void save_ppm(const RgbImage& img, const std::filesystem::path& path) {
   const std::vector<unsigned char> bytes = write_ppm(img);
-  std::ofstream f(path, std::ios::binary);
-  if (!f) throw std::runtime_error("cannot open " + path.string() + " for writing");
-  f.write(reinterpret_cast<const char*>(bytes.data()), std::streamsize(bytes.size()));
-  if (!f) throw std::runtime_error("write failed: " + path.string());
+  io_detail::spill(path, "wb", bytes.data(), bytes.size());
 }
 
+// One "%.10g %.10g %.10g" line per center, in palette-index order.
 inline std::string palette_to_text(const Palette& p) {
-  std::string s;
-  char line[96];
-  for (const Vec3& c : p.centers) {
-    std::snprintf(line, sizeof line, "%.10g %.10g %.10g\n", c[0], c[1], c[2]);
-    s += line;
-  }
+  std::string s(p.centers.size() * 96, '\0');
+  std::size_t at = 0;
+  for (const Vec3& c : p.centers)
+    at += std::size_t(std::snprintf(s.data() + at, 96, "%.10g %.10g %.10g\n", c[0], c[1], c[2]));
+  s.resize(at);
   return s;
 }
 
+// Inverse of palette_to_text: newline-separated lines, empty lines skipped, a line
+// without three numbers is an error.
 inline Palette palette_from_text(const std::string& text) {
   Palette p;
-  std::istringstream in(text);
-  std::string line;
-  while (std::getline(in, line)) {
+  const std::string_view all(text);
+  for (std::size_t b = 0; b < all.size();) {
+    std::size_t e = all.find('\n', b);
+    if (e == std::string_view::npos) e = all.size();
+    const std::string_view line = all.substr(b, e - b);
+    b = e + 1;
     if (line.empty()) continue;
-    std::istringstream ls(line);
     Vec3 c{};
-    if (!(ls >> c[0] >> c[1] >> c[2])) throw std::runtime_error("malformed palette line: '" + line + "'");
+    if (!io_detail::parse_center(line, c))
+      throw std::runtime_error("malformed palette line: '" + std::string(line) + "'");
     p.centers.push_back(c);
   }
   return p;
 }
 
 inline void save_palette(const Palette& p, const std::filesystem::path& path) {
-  std::ofstream f(path);
-  if (!f) throw std::runtime_error("cannot open " + path.string() + " for writing");
-  f << palette_to_text(p);
+  const std::string text = palette_to_text(p);
+  io_detail::spill(path, "w", text.data(), text.size());
 }
 
 inline Palette load_palette(const std::filesystem::path& path) {
-  std::ifstream f(path);
-  if (!f) throw std::runtime_error("cannot open " + path.string());
-  std::ostringstream ss;
-  ss << f.rdbuf();
-  return palette_from_text(ss.str());
+  const std::vector<unsigned char> bytes = io_detail::slurp(path, "r");
+  return palette_from_text(std::string(bytes.begin(), bytes.end()));
 }
 
 // 255 - min(255, 4|orig - quant|) per channel, computed on the device.
