@@ -49,6 +49,15 @@
 #ifndef CQB_NQ
 #define CQB_NQ 4  // ... how many (entries 1..4*NQ)
 #endif
+#ifndef CQB_EDIFF
+#define CQB_EDIFF 1  // large path: candidates evaluated in difference form from per-row-entry tables (rowE)
+#endif
+#ifndef CQB_EDIFF_SMALL
+#define CQB_EDIFF_SMALL 0  // ... also on the small path
+#endif
+#ifndef CQB_NQE
+#define CQB_NQE 4  // quads of rowE entries staged in shared memory with the first row quads (<= CQB_NQ)
+#endif
 
 
 namespace cqb {
@@ -67,6 +76,11 @@ struct WsmState {
   // entries) and stops at the row's end without a bounds check.
   alignas(16) float rowD32[KMAX * ROW32];
   alignas(16) uint8_t rowO[KMAX * ROW32];
+  // Difference form of the same entries (scan_f32<kE>): position i of row p
+  // holds {m, w} of entry i + 1 = center t, with D(x, c_t) - D(x, c_p) =
+  // w + (x - fl32(c_p)) . m exactly for m = -2 (c_t - c_p), w = |c_t -
+  // fl32(c_p)|^2 - |c_p - fl32(c_p)|^2 (computed in FP64, rounded to FP32).
+  alignas(16) float4 rowE[KMAX * KMAX];
   uint8_t order[KMAX * KMAX];             // row p: [p, others by (d, index)]
   double final_C[3 * KMAX];
   uint32_t chosen[KMAX];                  // init: chosen sample indices
@@ -358,6 +372,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Entry (p -> e) of WsmState::rowE from the FP64 centers (FP64 throughout; the
+// FP32 roundings of the four results are the only errors scan_f32 accounts for).
+__device__ __forceinline__ float4 ediff_entry(const LoopSmem& S, int p, int e) {
+  const double fx = (double)__double2float_rn(S.cx[p]), fy = (double)__double2float_rn(S.cy[p]),
+               fz = (double)__double2float_rn(S.cz[p]);
+  const double gx = S.cx[e] - fx, gy = S.cy[e] - fy, gz = S.cz[e] - fz;
+  const double hx = S.cx[p] - fx, hy = S.cy[p] - fy, hz = S.cz[p] - fz;
+  const double w = (gx * gx + gy * gy + gz * gz) - (hx * hx + hy * hy + hz * hz);
+  return make_float4(__double2float_rn(-2.0 * (S.cx[e] - S.cx[p])), __double2float_rn(-2.0 * (S.cy[e] - S.cy[p])),
+                     __double2float_rn(-2.0 * (S.cz[e] - S.cz[p])), __double2float_rn(w));
+}
+
 // Rows pa (and pb, or -1) of the center tables (kmeans.hpp:147-168):
 // d[p][t] = dist2(c_p, c_t) and the order row [p, others sorted by
 // (d, index)]. The block's 1024 threads take two rows per pass.
@@ -421,6 +447,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
       if (t > 0) {
         st->rowD32[p * ROW32 + t - 1] = __double2float_rn(S.rowd[r][e]);
         st->rowO[p * ROW32 + t - 1] = (uint8_t)e;
+        if (CQB_EDIFF || CQB_EDIFF_SMALL) st->rowE[p * KMAX + t - 1] = ediff_entry(S, p, e);
       }
       st->order[p * KMAX + t] = (uint8_t)e;
     }
@@ -445,6 +472,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
       if (rank > 0) {
         st->rowD32[p * ROW32 + rank - 1] = __double2float_rn(S.rowd[r][t]);
         st->rowO[p * ROW32 + rank - 1] = (uint8_t)t;
+        if (CQB_EDIFF || CQB_EDIFF_SMALL) st->rowE[p * KMAX + rank - 1] = ediff_entry(S, p, t);
       }
       st->order[p * KMAX + rank] = (uint8_t)t;
       S.rowo[r][rank] = (uint8_t)t;
@@ -794,6 +822,12 @@ struct LoopDyn {
   float4 c4[KMAX];  // centers of the current assignment rounded to FP32
   float4 q0[CQB_NQ][KMAX];  // large path: entries 1..4*NQ of every FP32 row (staged per pass)
   uint32_t o0[CQB_NQ][KMAX];
+#if CQB_EDIFF || CQB_EDIFF_SMALL
+  // ... and entries 1..4*NQE of every rowE row, row-major with one entry of
+  // padding per row (coalesced staging copy; lanes on neighbouring rows hit
+  // different banks)
+  float4 e0[KMAX * (4 * CQB_NQE + 1)];
+#endif
   ChunkSched sched;
 };
 constexpr size_t LOOP_DYN_SMEM = sizeof(LoopDyn);
@@ -956,6 +990,115 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
   return j;
 }
 
+// The same scan with the candidates evaluated in DIFFERENCE form: for the
+// point's own center p and row entry j -> center t,
+//   Delta_t = D(x, c_t) - D(x, c_p) = w + a . m,  a = x - fl32(c_p),
+// with {m, w} = WsmState::rowE[p][j - 1] (ediff_entry). One 16-B load and three
+// FFMAs per candidate (no order byte, no center gather, no subtractions), on
+// the differences a_i the own-center distance already produced. The break
+// tests are those of scan_f32 (prev in the six-operation form, same pl / pu).
+//
+// Error bound of diff = fma(a0, m0, fma(a1, m1, fma(a2, m2, w))), u = 2^-24:
+// a_i, m_i, w carry one FP32 rounding each and the three FFMAs one each, every
+// partial sum bounded by M = |w*| + sum |a_i m_i|, so |diff - Delta| <=
+// 4u M (1 + O(u)) + 1e-9 (the FP64 roundings of the table and of the
+// reference's own dist2). An evaluated entry has D(c_p, c_t) < 4 prev (its
+// fl32 is below pl), hence |w*| <= D(c_p, c_t) + 0.012 and sum |a_i m_i| <=
+// |a| |m| = 2 sqrt(prev' D(c_p, c_t)) with prev' = |a*|^2 <= prev (1 + 6u):
+// M <= 8 prev (1 + 1e-6) + 0.02 and |diff - Delta| <= E = 1.91e-6 prev + 1e-8.
+// The own center has Delta = 0 exactly. The FP32 best (index 0 = own) is the
+// reference's lexicographic (d, index) minimum when the second smallest
+// difference exceeds the smallest by more than 2 E; the test below uses
+// 4.1e-6 prev + 2.5e-6 (> 2 E (1 + u) plus the subtraction's rounding). A tie
+// never certifies.
+constexpr float F32_E_A = 4.1e-6f, F32_E_B = 2.5e-6f;
+template <bool kDeep, int DEEP_J_, int DEEP_P_, bool kQ0 = false>
+__device__ __forceinline__ int scan_f32e(const float4* __restrict__ c4, const float4* __restrict__ rq,
+                                         const uint32_t* __restrict__ oq, const float4* __restrict__ re, int k,
+                                         uint32_t key, int p, int& best_out, unsigned int& n_active) {
+#if CQB_EDIFF || CQB_EDIFF_SMALL
+  const float4 cp = c4[p];
+  const float a0 = __fsub_rn(u8_to_float(key_r(key)), cp.x), a1 = __fsub_rn(u8_to_float(key_g(key)), cp.y),
+              a2 = __fsub_rn(u8_to_float(key_b(key)), cp.z);
+  const float prev = __fmaf_rn(a2, a2, __fmaf_rn(a1, a1, __fmul_rn(a0, a0)));  // = dist32(x, c4[p])
+  const float pu = __fmaf_rn(prev, F32_PU_A, F32_P_B);
+  const float pl = __fmaf_rn(prev, F32_PL_A, -F32_P_B);
+  best_out = p;
+  float4 D;  // entries 1..4
+  if constexpr (kQ0) D = loop_dyn_smem().q0[0][p];
+  else D = rq[0];
+  if (D.x >= pl) return D.x >= pu ? 1 : 0;
+  if (CQB_DIAG_COUNTS) n_active += 1;
+  float bd = 0.f, d2 = F32_INF;  // smallest / second smallest difference (own center: 0)
+  int best = 0;                  // row entry of the smallest (0 = own center)
+  auto eval = [&](const float4 E, int e) {
+    const float d = __fmaf_rn(a0, E.x, __fmaf_rn(a1, E.y, __fmaf_rn(a2, E.z, E.w)));
+    d2 = fminf(d2, fmaxf(bd, d));
+    best = d < bd ? e : best;
+    bd = fminf(bd, d);
+  };
+  int j = 1;  // the next entry to test; entry j is a certain candidate at the loop head
+  int qi = 0;
+  float Db;   // the break entry's distance
+  // one quad of entries j .. j+3 (ld(c): the rowE entry of j + c); true = the scan broke
+  auto quad = [&](auto ld) -> bool {
+    eval(ld(0), j);
+    if (D.y >= pl) { Db = D.y; j += 1; return true; }
+    eval(ld(1), j + 1);
+    if (D.z >= pl) { Db = D.z; j += 2; return true; }
+    eval(ld(2), j + 2);
+    if (D.w >= pl) { Db = D.w; j += 3; return true; }
+    eval(ld(3), j + 3);
+    j += 4;
+    return false;
+  };
+  for (;;) {
+    if (kQ0 && qi < CQB_NQE) {
+      const float4* es = &loop_dyn_smem().e0[p * (4 * CQB_NQE + 1) + 4 * qi];
+      if (quad([&](int c) { return es[c]; })) break;
+    } else {
+      const float4* eg = re + 4 * qi;
+      if (quad([&](int c) { return eg[c]; })) break;
+    }
+    ++qi;
+    if (kQ0 && qi < CQB_NQ) D = loop_dyn_smem().q0[qi][p];
+    else D = rq[qi];
+    if (D.x >= pl) { Db = D.x; break; }
+    if (kDeep && j > DEEP_J_) {  // deep scan (as in scan_f32)
+      const float* rf = reinterpret_cast<const float*>(rq) - 1;  // rf[e] = entry e
+      int a = j, b = k;
+      while (a < b) {
+        int na = a, nb = b;
+#pragma unroll
+        for (int u = DEEP_P_; u >= 1; --u) {
+          const int m = a + ((b - a) * u) / (DEEP_P_ + 1);
+          if (m >= a && m < b) {
+            if (rf[m] >= pl) nb = m;
+            else if (m + 1 > na) na = m + 1;
+          }
+        }
+        if (na == a && nb == b) {
+          if (rf[a] >= pl) nb = a;
+          else na = a + 1;
+        }
+        a = na < nb ? na : nb;
+        b = nb;
+      }
+      for (int i2 = j; i2 < b; ++i2) eval(re[i2 - 1], i2);
+      j = b;
+      Db = rf[b];  // +inf at the row's end (b = k)
+      break;
+    }
+  }
+  if (Db < pu) return 0;  // the break itself is uncertain
+  if (!(__fsub_rn(d2, bd) > __fmaf_rn(prev, F32_E_A, F32_E_B))) return 0;
+  if (best) best_out = (int)(reinterpret_cast<const uint8_t*>(oq) - 1)[best];
+  return j;
+#else
+  return 0;
+#endif
+}
+
 // One point's sort-means scan in FP64 with the reference's exact semantics
 // (kmeans.hpp:211-236). Out of line: it is the rare path (scan_f32 not
 // certified, or centers outside its range) and keeps its registers out of the
@@ -1045,6 +1188,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   constexpr bool kSched = PPT == 1;
   constexpr bool kDeep = true;
   constexpr bool kQ0 = (PPT >= 2 || CQB_Q0_SMALL) && CQB_Q0;
+  constexpr bool kE = PPT >= 2 ? CQB_EDIFF != 0 : CQB_EDIFF_SMALL != 0;
   const uint32_t my_ch = nch > pb ? (nch - 1u - pb) / G + 1u : 0u;
   const double* __restrict__ gd = L.st->sortedD;
   const float4* __restrict__ rq32 = reinterpret_cast<const float4*>(L.st->rowD32);
@@ -1057,8 +1201,15 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
     for (int u = threadIdx.x; u < CQB_NQ * L.k; u += blockDim.x) {
       const int t = u % L.k, qq = u / L.k;
       loop_dyn_smem().q0[qq][t] = __ldcg(rq32 + t * (ROW32 / 4) + qq);
-      loop_dyn_smem().o0[qq][t] = __ldcg(oq32 + t * (ROW32 / 4) + qq);
+      if (!kE) loop_dyn_smem().o0[qq][t] = __ldcg(oq32 + t * (ROW32 / 4) + qq);
     }
+#if CQB_EDIFF || CQB_EDIFF_SMALL
+    if (kE)
+      for (int u = threadIdx.x; u < 4 * CQB_NQE * L.k; u += blockDim.x) {
+        const int t = u / (4 * CQB_NQE), e = u % (4 * CQB_NQE);
+        loop_dyn_smem().e0[t * (4 * CQB_NQE + 1) + e] = __ldcg(L.st->rowE + t * KMAX + e);
+      }
+#endif
     __syncthreads();
   }
   const uint32_t* __restrict__ keys = L.keys;
@@ -1105,9 +1256,14 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       const uint8_t* ro = go + p * KMAX;
       int best = p;
       int J = 0;
-      if (use32)
+      if (use32) {
+        if constexpr (kE)
+          J = scan_f32e<kDeep, DEEP_J, DEEP_P, kQ0>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4),
+                                                    L.st->rowE + p * KMAX, k, key[q], p, best, n_active);
+        else
           J = scan_f32<kDeep, DEEP_J, DEEP_P, kQ0>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4), k, key[q], p,
                                                    best, n_active);
+      }
       if (J == 0) {  // FP64: uncertified FP32 screens, or screening off (rare)
         const int r = scan_fp64(S, gd + p * KMAX, ro, k, key[q], p, L.debug_flags);
         J = r & 0xFFF;
