@@ -394,7 +394,7 @@ __device__ __forceinline__ float4 ediff_entry(const LoopSmem& S, int p, int e) {
 // only the distances are rewritten. Otherwise (early iterations) the row is
 // re-sorted by rank counting, half of the block per row, u-range split in 2.
 __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, bool incremental, bool keep,
-                             bool tail_sync = true) {
+                             bool want_e, bool tail_sync = true) {
   static_assert(LOOP_THREADS == 4 * KMAX || LOOP_THREADS == 2 * KMAX, "tables layout: 512 or 1024 threads");
   const int tid = threadIdx.x;
   const int r = tid >> 9;                     // which row of the pair
@@ -447,7 +447,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
       if (t > 0) {
         st->rowD32[p * ROW32 + t - 1] = __double2float_rn(S.rowd[r][e]);
         st->rowO[p * ROW32 + t - 1] = (uint8_t)e;
-        if (CQB_EDIFF || CQB_EDIFF_SMALL) st->rowE[p * KMAX + t - 1] = ediff_entry(S, p, e);
+        if (want_e) st->rowE[p * KMAX + t - 1] = ediff_entry(S, p, e);
       }
       st->order[p * KMAX + t] = (uint8_t)e;
     }
@@ -472,7 +472,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
       if (rank > 0) {
         st->rowD32[p * ROW32 + rank - 1] = __double2float_rn(S.rowd[r][t]);
         st->rowO[p * ROW32 + rank - 1] = (uint8_t)t;
-        if (CQB_EDIFF || CQB_EDIFF_SMALL) st->rowE[p * KMAX + rank - 1] = ediff_entry(S, p, t);
+        if (want_e) st->rowE[p * KMAX + rank - 1] = ediff_entry(S, p, t);
       }
       st->order[p * KMAX + rank] = (uint8_t)t;
       S.rowo[r][rank] = (uint8_t)t;
@@ -487,7 +487,7 @@ __device__ void tables_rows2(LoopSmem& S, WsmState* st, int pa, int pb, int k, b
 
 // Rows are owned by blocks 1..G-1 (block 0 runs the SSE / termination
 // finalize meanwhile); a single-block grid does everything itself.
-__device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, bool incremental) {
+__device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, bool incremental, bool want_e) {
   const int G = (int)gridDim.x;
   const int first = G == 1 ? 0 : (int)blockIdx.x - 1;
   const int stride = G == 1 ? 1 : G - 1;
@@ -499,10 +499,10 @@ __device__ __forceinline__ void tables_all(LoopSmem& S, WsmState* st, int k, boo
     if (LOOP_THREADS == 4 * KMAX) {
       // the last pass skips its trailing barrier: the grid barrier (or
       // grid.sync) after tables_all starts with one
-      tables_rows2(S, st, p, q < k ? q : -1, k, incremental, keep, p + 2 * stride < k);
+      tables_rows2(S, st, p, q < k ? q : -1, k, incremental, keep, want_e, p + 2 * stride < k);
     } else {  // 512 threads: one row per pass
-      tables_rows2(S, st, p, -1, k, incremental, false);
-      if (q < k) tables_rows2(S, st, q, -1, k, incremental, false);
+      tables_rows2(S, st, p, -1, k, incremental, false, want_e);
+      if (q < k) tables_rows2(S, st, q, -1, k, incremental, false, want_e);
     }
   }
 }
@@ -795,6 +795,12 @@ constexpr float F32_INF = __builtin_huge_valf();
 constexpr float F32_PU_A = 4.0f + 0x1p-16f, F32_PL_A = 4.0f - 0x1p-16f, F32_P_B = 8.52e-4f;
 constexpr float F32_C_LO = 1.0f - 0x1p-19f, F32_C_HI = 1.0f + 0x1p-19f, F32_C_B = 2.12e-4f;
 
+// Channel C (0 = blue .. 2 = red) of a packed key as a float: one PRMT builds
+// 0x4B0000xx = 2^23 + x, one FADD removes 2^23 (exact, no shift / mask / I2F).
+template <int C>
+__device__ __forceinline__ float key_chan_f32(uint32_t key) {
+  return __fsub_rn(__uint_as_float(__byte_perm(key, 0x4B000000u, 0x7440u | (unsigned)C)), 8388608.0f);
+}
 __device__ __forceinline__ float u8_to_float(uint32_t v) {  // exact, no I2F
   return __fsub_rn(__uint_as_float(0x4B000000u | v), 8388608.0f);
 }
@@ -908,7 +914,7 @@ template <bool kDeep, int DEEP_J_, int DEEP_P_, bool kQ0 = false>
 __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const float4* __restrict__ rq,
                                         const uint32_t* __restrict__ oq, int k, uint32_t key, int p, int& best_out,
                                         unsigned int& n_active) {
-  const float x0 = u8_to_float(key_r(key)), x1 = u8_to_float(key_g(key)), x2 = u8_to_float(key_b(key));
+  const float x0 = key_chan_f32<2>(key), x1 = key_chan_f32<1>(key), x2 = key_chan_f32<0>(key);
   const float prev = dist32(x0, x1, x2, c4[p]);
   const float pu = __fmaf_rn(prev, F32_PU_A, F32_P_B);
   const float pl = __fmaf_rn(prev, F32_PL_A, -F32_P_B);
@@ -1012,20 +1018,31 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
 // 4.1e-6 prev + 2.5e-6 (> 2 E (1 + u) plus the subtraction's rounding). A tie
 // never certifies.
 constexpr float F32_E_A = 4.1e-6f, F32_E_B = 2.5e-6f;
+// 16-B load from a 32-bit shared-window address (the dynamic block's base is
+// converted once per assign pass; addressing through generic pointers made the
+// compiler rebuild the window base, S2R + three more instructions, per point)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 template <bool kDeep, int DEEP_J_, int DEEP_P_, bool kQ0 = false>
-__device__ __forceinline__ int scan_f32e(const float4* __restrict__ c4, const float4* __restrict__ rq,
+__device__ __forceinline__ int scan_f32e(const uint32_t sb, const float4* __restrict__ rq,
                                          const uint32_t* __restrict__ oq, const float4* __restrict__ re, int k,
                                          uint32_t key, int p, int& best_out, unsigned int& n_active) {
 #if CQB_EDIFF || CQB_EDIFF_SMALL
-  const float4 cp = c4[p];
-  const float a0 = __fsub_rn(u8_to_float(key_r(key)), cp.x), a1 = __fsub_rn(u8_to_float(key_g(key)), cp.y),
-              a2 = __fsub_rn(u8_to_float(key_b(key)), cp.z);
+  // sb: shared-window address of the loop's dynamic block (LoopDyn)
+  const uint32_t sp = sb + (uint32_t)p * 16u;  // + row p of c4 / q0[.]
+  const uint32_t se = sb + (uint32_t)offsetof(LoopDyn, e0) + (uint32_t)p * (16u * (4 * CQB_NQE + 1));
+  const float4 cp = lds128(sp + (uint32_t)offsetof(LoopDyn, c4));
+  const float a0 = __fsub_rn(key_chan_f32<2>(key), cp.x), a1 = __fsub_rn(key_chan_f32<1>(key), cp.y),
+              a2 = __fsub_rn(key_chan_f32<0>(key), cp.z);
   const float prev = __fmaf_rn(a2, a2, __fmaf_rn(a1, a1, __fmul_rn(a0, a0)));  // = dist32(x, c4[p])
   const float pu = __fmaf_rn(prev, F32_PU_A, F32_P_B);
   const float pl = __fmaf_rn(prev, F32_PL_A, -F32_P_B);
   best_out = p;
   float4 D;  // entries 1..4
-  if constexpr (kQ0) D = loop_dyn_smem().q0[0][p];
+  if constexpr (kQ0) D = lds128(sp + (uint32_t)offsetof(LoopDyn, q0));
   else D = rq[0];
   if (D.x >= pl) return D.x >= pu ? 1 : 0;
   if (CQB_DIAG_COUNTS) n_active += 1;
@@ -1037,36 +1054,42 @@ __device__ __forceinline__ int scan_f32e(const float4* __restrict__ c4, const fl
     best = d < bd ? e : best;
     bd = fminf(bd, d);
   };
-  int j = 1;  // the next entry to test; entry j is a certain candidate at the loop head
+  // Quad qi = entries 4 qi + 1 .. 4 qi + 4, its distances in D; the first is a
+  // certain candidate at the loop head; every exit records the break index
+  // and the break entry's distance.
   int qi = 0;
-  float Db;   // the break entry's distance
-  // one quad of entries j .. j+3 (ld(c): the rowE entry of j + c); true = the scan broke
+  int j;
+  float Db;
+  auto leave = [&](int jv, float dv) {
+    j = jv;
+    Db = dv;
+  };
+  // ld(c): the rowE entry of 4 qi + 1 + c; true = the scan broke inside the quad
   auto quad = [&](auto ld) -> bool {
-    eval(ld(0), j);
-    if (D.y >= pl) { Db = D.y; j += 1; return true; }
-    eval(ld(1), j + 1);
-    if (D.z >= pl) { Db = D.z; j += 2; return true; }
-    eval(ld(2), j + 2);
-    if (D.w >= pl) { Db = D.w; j += 3; return true; }
-    eval(ld(3), j + 3);
-    j += 4;
+    eval(ld(0), 4 * qi + 1);
+    if (D.y >= pl) { leave(4 * qi + 2, D.y); return true; }
+    eval(ld(1), 4 * qi + 2);
+    if (D.z >= pl) { leave(4 * qi + 3, D.z); return true; }
+    eval(ld(2), 4 * qi + 3);
+    if (D.w >= pl) { leave(4 * qi + 4, D.w); return true; }
+    eval(ld(3), 4 * qi + 4);
     return false;
   };
   for (;;) {
     if (kQ0 && qi < CQB_NQE) {
-      const float4* es = &loop_dyn_smem().e0[p * (4 * CQB_NQE + 1) + 4 * qi];
-      if (quad([&](int c) { return es[c]; })) break;
+      const uint32_t es = se + 64u * (uint32_t)qi;
+      if (quad([&](int c) { return lds128(es + 16u * (uint32_t)c); })) break;
     } else {
       const float4* eg = re + 4 * qi;
       if (quad([&](int c) { return eg[c]; })) break;
     }
     ++qi;
-    if (kQ0 && qi < CQB_NQ) D = loop_dyn_smem().q0[qi][p];
+    if (kQ0 && qi < CQB_NQ) D = lds128(sp + (uint32_t)offsetof(LoopDyn, q0) + (uint32_t)qi * (16u * KMAX));
     else D = rq[qi];
-    if (D.x >= pl) { Db = D.x; break; }
-    if (kDeep && j > DEEP_J_) {  // deep scan (as in scan_f32)
+    if (D.x >= pl) { leave(4 * qi + 1, D.x); break; }
+    if (kDeep && 4 * qi + 1 > DEEP_J_) {  // deep scan (as in scan_f32)
       const float* rf = reinterpret_cast<const float*>(rq) - 1;  // rf[e] = entry e
-      int a = j, b = k;
+      int a = 4 * qi + 1, b = k;
       while (a < b) {
         int na = a, nb = b;
 #pragma unroll
@@ -1084,9 +1107,8 @@ __device__ __forceinline__ int scan_f32e(const float4* __restrict__ c4, const fl
         a = na < nb ? na : nb;
         b = nb;
       }
-      for (int i2 = j; i2 < b; ++i2) eval(re[i2 - 1], i2);
-      j = b;
-      Db = rf[b];  // +inf at the row's end (b = k)
+      for (int i2 = 4 * qi + 1; i2 < b; ++i2) eval(re[i2 - 1], i2);
+      leave(b, rf[b]);  // +inf at the row's end (b = k)
       break;
     }
   }
@@ -1194,6 +1216,9 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   const float4* __restrict__ rq32 = reinterpret_cast<const float4*>(L.st->rowD32);
   const uint32_t* __restrict__ oq32 = reinterpret_cast<const uint32_t*>(L.st->rowO);
   const float4* c4 = loop_c4();
+  // (through an opaque move: the compiler would otherwise rebuild it from S2R per point)
+  uint32_t dyn_sb;
+  asm volatile("mov.u32 %0, %1;" : "=r"(dyn_sb) : "r"((uint32_t)__cvta_generic_to_shared(&loop_dyn_smem())));
   const uint8_t* __restrict__ go = L.st->order;
   // FP32 screening (scan_f32): sort-means scans whose centers all satisfy |c| < 256
   const bool use32 = S.f32ok;
@@ -1258,7 +1283,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       int J = 0;
       if (use32) {
         if constexpr (kE)
-          J = scan_f32e<kDeep, DEEP_J, DEEP_P, kQ0>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4),
+          J = scan_f32e<kDeep, DEEP_J, DEEP_P, kQ0>(dyn_sb, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4),
                                                     L.st->rowE + p * KMAX, k, key[q], p, best, n_active);
         else
           J = scan_f32<kDeep, DEEP_J, DEEP_P, kQ0>(c4, rq32 + p * (ROW32 / 4), oq32 + p * (ROW32 / 4), k, key[q], p,
@@ -1719,6 +1744,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
   __shared__ LoopSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
   cg::grid_group grid = cg::this_grid();
+  constexpr bool kLoopE = PPT >= 2 ? CQB_EDIFF != 0 : CQB_EDIFF_SMALL != 0;  // assign_sort_means reads rowE
   WsmState* st = L.st;
   const int tid = threadIdx.x;
   const int k = L.k;
@@ -1807,7 +1833,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
         st->rowD32[p * ROW32 + i] = F32_INF;
         st->rowO[p * ROW32 + i] = 0;
       }
-  tables_all(S, st, k, false);
+  tables_all(S, st, k, false, kLoopE);
   unsigned long long evals = 0;  // this thread's point evaluations (flushed once at exit)
   // pair evaluations of the center tables (block 0 only); none in naive mode
   // (sharded over processes: counted by rank 0 only)
@@ -2071,7 +2097,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     if (rec_it) tl[(it - 1) * 8 + 5] = globaltimer();
     BLOCK_STAMP(4);
     if (tid == 0) S.stamp = (L.block_times && it == L.stamp_iter) ? L.block_times : nullptr;
-    tables_all(S, st, k, true);  // wasted work on the final iteration only
+    tables_all(S, st, k, true, kLoopE);  // wasted work on the final iteration only
     if (rec_it) tl[(it - 1) * 8 + 6] = globaltimer();
     BLOCK_STAMP(5);
     if (CQB_LOOP_BARRIER) {
