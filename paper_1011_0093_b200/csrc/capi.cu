@@ -575,7 +575,7 @@ int launch_loop(cqb_ctx* ctx, int k, const cqb_termination* term, int dense_firs
   const void* kern = X == 1   ? (small ? (const void*)k_wsm_loop<1, 1> : (const void*)k_wsm_loop<CQB_PPT_LARGE, 1>)
                      : X == 2 ? (small ? (const void*)k_wsm_loop<1, 2> : (const void*)k_wsm_loop<CQB_PPT_LARGE, 2>)
                               : (small ? (const void*)k_wsm_loop<1, 0> : (const void*)k_wsm_loop<CQB_PPT_LARGE, 0>);
-  size_t dyn = LOOP_DYN_SMEM;
+  size_t dyn = small ? LOOP_DYN_SMALL : LOOP_DYN_LARGE;
   if (X == 0 && small && !(ctx->debug_flags & 512)) {
     // resident samples when the block's share (bounded by P) fits in shared memory
     const uint64_t cap = ((total + 31) / 32 + grid - 1) / grid * 32;
@@ -811,13 +811,15 @@ int cqb_create(int device, cqb_ctx** out) {
     if (!prop.cooperativeLaunch) return fail(ctx, CQB_ERR_UNSUPPORTED, "cooperative launch unsupported");
     ctx->num_sms = prop.multiProcessorCount;
     int nb = 0;
-    for (const void* f : {(const void*)k_wsm_loop<1, 0>, (const void*)k_wsm_loop<CQB_PPT_LARGE, 0>, (const void*)k_wsm_loop<1, 1>,
-                          (const void*)k_wsm_loop<CQB_PPT_LARGE, 1>, (const void*)k_wsm_loop<1, 2>, (const void*)k_wsm_loop<CQB_PPT_LARGE, 2>})
-      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMEM));
+    for (const void* f : {(const void*)k_wsm_loop<1, 0>, (const void*)k_wsm_loop<1, 1>, (const void*)k_wsm_loop<1, 2>})
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_SMALL));
+    for (const void* f : {(const void*)k_wsm_loop<CQB_PPT_LARGE, 0>, (const void*)k_wsm_loop<CQB_PPT_LARGE, 1>,
+                          (const void*)k_wsm_loop<CQB_PPT_LARGE, 2>})
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOOP_DYN_LARGE));
     CK(cudaFuncSetAttribute((const void*)k_wsm_loop<1, 0, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RES_DYN_MAX));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_wsm_loop<CQB_PPT_LARGE, 0>, LOOP_THREADS,
-                                                     LOOP_DYN_SMEM));
+                                                     LOOP_DYN_LARGE));
     if (nb < 1) return fail(ctx, CQB_ERR_INTERNAL, "WSM loop kernel cannot be resident");
     ctx->loop_blocks_max = std::min(nb, CQB_LOOP_MINB) * ctx->num_sms;
     CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));

@@ -55,6 +55,12 @@
 #ifndef CQB_EDIFF_SMALL
 #define CQB_EDIFF_SMALL 0  // ... also on the small path
 #endif
+#ifndef CQB_MOVEQ
+#define CQB_MOVEQ 1  // large path: moment deltas of moving samples queued per warp and applied 32 at a time
+#endif
+#ifndef CQB_MOVEQ_SMALL
+#define CQB_MOVEQ_SMALL 0  // ... also on the small path
+#endif
 #ifndef CQB_NQE
 #define CQB_NQE 4  // quads of rowE entries staged in shared memory with the first row quads (<= CQB_NQ)
 #endif
@@ -827,19 +833,32 @@ struct ChunkSched {
 struct LoopDyn {
   float4 c4[KMAX];  // centers of the current assignment rounded to FP32
   float4 q0[CQB_NQ][KMAX];  // large path: entries 1..4*NQ of every FP32 row (staged per pass)
-  uint32_t o0[CQB_NQ][KMAX];
-#if CQB_EDIFF || CQB_EDIFF_SMALL
-  // ... and entries 1..4*NQE of every rowE row, row-major with one entry of
-  // padding per row (coalesced staging copy; lanes on neighbouring rows hit
-  // different banks)
-  float4 e0[KMAX * (4 * CQB_NQE + 1)];
+#if !CQB_EDIFF || CQB_Q0_SMALL
+  uint32_t o0[CQB_NQ][KMAX];  // (scan_f32 only: scan_f32e reads no order bytes)
 #endif
   ChunkSched sched;
 };
-constexpr size_t LOOP_DYN_SMEM = sizeof(LoopDyn);
+// ... followed, in the kernels whose scan is scan_f32e / whose moves are queued, by
+struct LoopDynLarge {
+  LoopDyn base;
+  // entries 1..4*NQE of every rowE row, row-major with one entry of padding
+  // per row (coalesced staging copy; lanes on neighbouring rows hit different
+  // banks)
+  float4 e0[KMAX * (4 * CQB_NQE + 1)];
+  // per-warp list of moving samples awaiting their moment deltas:
+  // {count index | new label << 24, key | old label << 24}
+  uint32_t mq[LOOP_THREADS / 32][32][2];
+};
+constexpr bool kSmallUsesLarge = CQB_EDIFF_SMALL || CQB_MOVEQ_SMALL;
+constexpr size_t LOOP_DYN_LARGE = sizeof(LoopDynLarge);                                  // PPT >= 2 kernels
+constexpr size_t LOOP_DYN_SMALL = kSmallUsesLarge ? sizeof(LoopDynLarge) : sizeof(LoopDyn);  // PPT == 1 kernels
 __device__ __forceinline__ LoopDyn& loop_dyn_smem() {
   extern __shared__ __align__(16) unsigned char loop_dyn[];
   return *reinterpret_cast<LoopDyn*>(loop_dyn);
+}
+__device__ __forceinline__ LoopDynLarge& loop_dyn_large() {
+  extern __shared__ __align__(16) unsigned char loop_dyn[];
+  return *reinterpret_cast<LoopDynLarge*>(loop_dyn);
 }
 __device__ __forceinline__ ChunkSched& chunk_sched() { return loop_dyn_smem().sched; }
 __device__ __forceinline__ float4* loop_c4() { return loop_dyn_smem().c4; }
@@ -856,12 +875,12 @@ struct ResSamples {
 };
 __device__ __forceinline__ ResSamples res_samples(int cap) {
   extern __shared__ __align__(16) unsigned char loop_dyn[];
-  unsigned char* b = loop_dyn + ((sizeof(LoopDyn) + 15) & ~size_t(15));
+  unsigned char* b = loop_dyn + ((LOOP_DYN_SMALL + 15) & ~size_t(15));
   return {reinterpret_cast<uint32_t*>(b), reinterpret_cast<uint32_t*>(b) + cap,
           reinterpret_cast<uint8_t*>(reinterpret_cast<uint32_t*>(b) + 2 * cap)};
 }
 __host__ __device__ constexpr size_t res_smem_bytes(int cap) {
-  return ((sizeof(LoopDyn) + 15) & ~size_t(15)) + (size_t)cap * 9;
+  return ((LOOP_DYN_SMALL + 15) & ~size_t(15)) + (size_t)cap * 9;
 }
 
 // Counting sort of this block's chunks by cost, descending (block-wide).
@@ -921,10 +940,13 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
   best_out = p;
   float4 D;  // entries 1..4
   uint32_t T;
+#if !CQB_EDIFF || CQB_Q0_SMALL
   if constexpr (kQ0) {  // staged in shared memory
     D = loop_dyn_smem().q0[0][p];
     T = loop_dyn_smem().o0[0][p];
-  } else {
+  } else
+#endif
+  {
     D = rq[0];
     T = oq[0];
   }
@@ -952,10 +974,13 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
     eval(T >> 24);
     j += 4;
     ++qi;
+#if !CQB_EDIFF || CQB_Q0_SMALL
     if (kQ0 && qi < CQB_NQ) {
       D = loop_dyn_smem().q0[qi][p];
       T = loop_dyn_smem().o0[qi][p];
-    } else {
+    } else
+#endif
+    {
       D = rq[qi];
       T = oq[qi];
     }
@@ -1030,10 +1055,9 @@ template <bool kDeep, int DEEP_J_, int DEEP_P_, bool kQ0 = false>
 __device__ __forceinline__ int scan_f32e(const uint32_t sb, const float4* __restrict__ rq,
                                          const uint32_t* __restrict__ oq, const float4* __restrict__ re, int k,
                                          uint32_t key, int p, int& best_out, unsigned int& n_active) {
-#if CQB_EDIFF || CQB_EDIFF_SMALL
   // sb: shared-window address of the loop's dynamic block (LoopDyn)
   const uint32_t sp = sb + (uint32_t)p * 16u;  // + row p of c4 / q0[.]
-  const uint32_t se = sb + (uint32_t)offsetof(LoopDyn, e0) + (uint32_t)p * (16u * (4 * CQB_NQE + 1));
+  const uint32_t se = sb + (uint32_t)offsetof(LoopDynLarge, e0) + (uint32_t)p * (16u * (4 * CQB_NQE + 1));
   const float4 cp = lds128(sp + (uint32_t)offsetof(LoopDyn, c4));
   const float a0 = __fsub_rn(key_chan_f32<2>(key), cp.x), a1 = __fsub_rn(key_chan_f32<1>(key), cp.y),
               a2 = __fsub_rn(key_chan_f32<0>(key), cp.z);
@@ -1116,9 +1140,6 @@ __device__ __forceinline__ int scan_f32e(const uint32_t sb, const float4* __rest
   if (!(__fsub_rn(d2, bd) > __fmaf_rn(prev, F32_E_A, F32_E_B))) return 0;
   if (best) best_out = (int)(reinterpret_cast<const uint8_t*>(oq) - 1)[best];
   return j;
-#else
-  return 0;
-#endif
 }
 
 // One point's sort-means scan in FP64 with the reference's exact semantics
@@ -1226,15 +1247,15 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
     for (int u = threadIdx.x; u < CQB_NQ * L.k; u += blockDim.x) {
       const int t = u % L.k, qq = u / L.k;
       loop_dyn_smem().q0[qq][t] = __ldcg(rq32 + t * (ROW32 / 4) + qq);
+#if !CQB_EDIFF || CQB_Q0_SMALL
       if (!kE) loop_dyn_smem().o0[qq][t] = __ldcg(oq32 + t * (ROW32 / 4) + qq);
+#endif
     }
-#if CQB_EDIFF || CQB_EDIFF_SMALL
     if (kE)
       for (int u = threadIdx.x; u < 4 * CQB_NQE * L.k; u += blockDim.x) {
         const int t = u / (4 * CQB_NQE), e = u % (4 * CQB_NQE);
-        loop_dyn_smem().e0[t * (4 * CQB_NQE + 1) + e] = __ldcg(L.st->rowE + t * KMAX + e);
+        loop_dyn_large().e0[t * (4 * CQB_NQE + 1) + e] = __ldcg(L.st->rowE + t * KMAX + e);
       }
-#endif
     __syncthreads();
   }
   const uint32_t* __restrict__ keys = L.keys;
@@ -1244,6 +1265,29 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   uint32_t ev = 0;
   (void)W;
   (void)w;
+  // Moving samples (label changed) are a few % of a pass, scattered over the
+  // warps: applying their ten moment atomics on the spot runs ~70 warp
+  // instructions for one or two lanes. They are queued per warp instead (two
+  // words in a 32-slot shared list, positions from one ballot) and applied
+  // together, one record per lane, when the next chunk's moves would not fit
+  // (the counts are gathered then). The sums are exact integers, so the order
+  // of the additions does not matter.
+  constexpr bool kMQ = PPT >= 2 ? CQB_MOVEQ != 0 : CQB_MOVEQ_SMALL != 0;
+  uint32_t qn = 0;  // queued records (warp-uniform)
+  uint32_t(*mq)[2] = loop_dyn_large().mq[threadIdx.x >> 5];
+  auto apply_moves = [&]() {  // all qn (<= 32) queued records
+    __syncwarp();
+    if ((uint32_t)lane < qn) {
+      const uint32_t a = mq[lane][0], b = mq[lane][1];
+      const uint32_t ci = a & 0xFFFFFFu;
+      uint32_t cnt;
+      if constexpr (R) cnt = res_samples(L.res_cap).cnt[ci];
+      else cnt = counts[ci];
+      acc_move(S.accm, S.accp, (int)(b >> 24), (int)(a >> 24), b & 0xFFFFFFu, cnt);
+    }
+    __syncwarp();
+    qn = 0;
+  };
   for (;;) {
     uint32_t j = 0;
     if (lane == 0) j = atomicAdd(&S.wq, (unsigned)PPT);
@@ -1316,13 +1360,16 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       const bool v = i < hi;
       const bool ch = v && nlab[q] != lab[q];
       uint32_t cnt = 0;
+      const bool now = full || !kMQ;  // the count is needed here (else when the queue is applied)
+      uint32_t ci = i;  // where the sample's count lives
       if constexpr (R) {
         const ResSamples rs = res_samples(L.res_cap);
         const uint32_t li = (chunk[q] << 5) + lane;
-        if (v && (full || ch)) cnt = rs.cnt[li];
+        ci = li;
+        if (v && (full || ch) && now) cnt = rs.cnt[li];
         if (ch) rs.lab[li] = (uint8_t)nlab[q];
       } else {
-        if (v && (full || ch)) cnt = counts[i];
+        if (v && (full || ch) && now) cnt = counts[i];
       }
       if (ch) {
         labels[i] = (uint8_t)nlab[q];
@@ -1330,11 +1377,23 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
       }
       if (full) {
         acc_point_warp(S.accp, v, nlab[q], key[q], cnt);
+      } else if constexpr (kMQ) {
+        const unsigned m = __ballot_sync(0xffffffffu, ch);
+        if (m) {
+          if (qn + (uint32_t)__popc(m) > 32u) apply_moves();
+          if (ch) {
+            const uint32_t slot = qn + __popc(m & ((1u << lane) - 1u));
+            mq[slot][0] = ci | ((uint32_t)nlab[q] << 24);
+            mq[slot][1] = key[q] | ((uint32_t)lab[q] << 24);
+          }
+          qn += __popc(m);
+        }
       } else if (ch) {
         acc_move(S.accm, S.accp, lab[q], nlab[q], key[q], cnt);
       }
     }
   }
+  if (kMQ && qn) apply_moves();
   evals += ev;
 }
 
