@@ -61,6 +61,12 @@
 #ifndef CQB_MOVEQ_SMALL
 #define CQB_MOVEQ_SMALL 0  // ... also on the small path
 #endif
+#ifndef CQB_SCHED_LARGE
+#define CQB_SCHED_LARGE 1  // longest-first chunk order on the large path too, for sparse sample sets (LoopSmem::sched_on)
+#endif
+#ifndef CQB_C4W
+#define CQB_C4W 1  // scan_f32e: the first row entry's distance rides in c4[p].w (no row-quad load for points without candidates)
+#endif
 #ifndef CQB_NQE
 #define CQB_NQE 4  // quads of rowE entries staged in shared memory with the first row quads (<= CQB_NQ)
 #endif
@@ -359,6 +365,7 @@ struct LoopSmem {
   unsigned int part_b, part_g;           // emulated ranks (X == 2): block index in its group, group size
   int debug;                             // LoopParams::debug_flags
   int f32ok;                             // FP32 screening valid: every center |c| < 256
+  int sched_on;                          // large path: longest-first chunk order in use (sparse sample sets)
 };
 #define SUB_STAMP(phase)                                                         \
   do {                                                                           \
@@ -767,6 +774,7 @@ __device__ __forceinline__ void lex_min(double& md, int& mb, double d, int t) {
 }
 
 constexpr int DBG_NO_F32 = 1 << 17;   // debug flag: FP64 scans only (A/B of the FP32 screening)
+constexpr int DBG_NO_SCHED_LARGE = 1 << 24;  // debug flag: large path without the longest-first chunk order (A/B)
 
 // ---------------------------------------------------------------------------
 // FP32 screening of the sort-means scan (iterations >= 2), certified against
@@ -1066,9 +1074,14 @@ __device__ __forceinline__ int scan_f32e(const uint32_t sb, const float4* __rest
   const float pl = __fmaf_rn(prev, F32_PL_A, -F32_P_B);
   best_out = p;
   float4 D;  // entries 1..4
-  if constexpr (kQ0) D = lds128(sp + (uint32_t)offsetof(LoopDyn, q0));
-  else D = rq[0];
-  if (D.x >= pl) return D.x >= pu ? 1 : 0;
+  if (CQB_C4W && kQ0) {
+    if (cp.w >= pl) return cp.w >= pu ? 1 : 0;
+    D = lds128(sp + (uint32_t)offsetof(LoopDyn, q0));
+  } else {
+    if constexpr (kQ0) D = lds128(sp + (uint32_t)offsetof(LoopDyn, q0));
+    else D = rq[0];
+    if (D.x >= pl) return D.x >= pu ? 1 : 0;
+  }
   if (CQB_DIAG_COUNTS) n_active += 1;
   float bd = 0.f, d2 = F32_INF;  // smallest / second smallest difference (own center: 0)
   int best = 0;                  // row entry of the smallest (0 = own center)
@@ -1207,8 +1220,12 @@ __device__ __noinline__ int scan_fp64(const LoopSmem& S, const double* __restric
   return J | (best << 12) | (active << 24);
 }
 
-template <int PPT, int X, bool R>
-__device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned long long lo64,
+// SCHED: longest-first chunk order (always for PPT == 1). The large path has
+// both forms as separate copies of this function inside one kernel, chosen per
+// launch by LoopSmem::sched_on: compiled into a single copy, the order's
+// bookkeeping cost the other case 7% even when switched off (spills).
+template <int PPT, int X, bool R, bool SCHED>
+__device__ __forceinline__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned long long lo64,
                                   unsigned long long hi64, bool full, unsigned long long& evals,
                                   unsigned int& n_changed, unsigned int& n_active) {
   const unsigned int pb = part_block<X>(S), pG = part_size<X>(S);
@@ -1228,7 +1245,7 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
   const uint32_t G = pG, W = blockDim.x >> 5, w = threadIdx.x >> 5;
   const uint32_t nch = (hi - lo + 31u) >> 5;
   // small sample sets: chunk costs recorded for the longest-first order
-  constexpr bool kSched = PPT == 1;
+  constexpr bool kSched = SCHED;
   constexpr bool kDeep = true;
   constexpr bool kQ0 = (PPT >= 2 || CQB_Q0_SMALL) && CQB_Q0;
   constexpr bool kE = PPT >= 2 ? CQB_EDIFF != 0 : CQB_EDIFF_SMALL != 0;
@@ -1257,6 +1274,10 @@ __device__ void assign_sort_means(LoopSmem& S, const LoopParams& L, unsigned lon
         loop_dyn_large().e0[t * (4 * CQB_NQE + 1) + e] = __ldcg(L.st->rowE + t * KMAX + e);
       }
     __syncthreads();
+    if (CQB_C4W && kE) {
+      for (int t = threadIdx.x; t < L.k; t += blockDim.x) loop_dyn_smem().c4[t].w = loop_dyn_smem().q0[0][t].x;
+      __syncthreads();
+    }
   }
   const uint32_t* __restrict__ keys = L.keys;
   const uint32_t* __restrict__ counts = L.counts;
@@ -1859,6 +1880,11 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     S.wq = 0u;
     S.debug = L.debug_flags;
     S.f32ok = !big && !(L.debug_flags & DBG_NO_F32);
+    // Longest-first chunk order on the large path: it pays when chunk costs
+    // are uneven (photo-like images: cfg3 -9%) and costs when they are even
+    // (a sample set that fills color space, cfg4: +9%). Unique colors per
+    // pixel tell the two apart: below 1/2 the samples are sparse in the cube.
+    S.sched_on = CQB_SCHED_LARGE && n * 2 < L.total && !(L.debug_flags & DBG_NO_SCHED_LARGE);
 
     S.rowo_row[0] = S.rowo_row[1] = -1;
   }
@@ -1925,7 +1951,13 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
       if (rec_it) tl[(it - 1) * 8 + 1] = globaltimer();
       unsigned int n_changed = 0, n_deep = 0;
       const unsigned long long ev0 = evals;
-      assign_sort_means<PPT, X, R>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
+      if constexpr (PPT == 1) {
+        assign_sort_means<PPT, X, R, true>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
+      } else if (CQB_SCHED_LARGE && S.sched_on) {
+        assign_sort_means<PPT, X, R, CQB_SCHED_LARGE != 0>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
+      } else {
+        assign_sort_means<PPT, X, R, false>(S, L, lo, hi, it == 1, evals, n_changed, n_deep);
+      }
       if (L.block_times && it == L.stamp_iter) {
         const unsigned long long v = warp_sum(evals - ev0);
         if ((tid & 31) == 0) atomicAdd(&L.block_times[7 * gridDim.x + blockIdx.x], v);
@@ -1943,7 +1975,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     // next iteration's longest-first chunk order (this block's chunks are
     // done); small sample sets only (latency-bound), re-sorted at iterations
     // 2, 4, 8, ... (costs drift slowly; the sort is not free)
-    if (PPT == 1 && it >= 2 && (it & (it - 1)) == 0) {
+    if ((PPT == 1 || (CQB_SCHED_LARGE && S.sched_on)) && it >= 2 && (it & (it - 1)) == 0) {
       const unsigned long long nn = hi - lo, nch = (nn + 31) >> 5;
       const uint32_t pb = part_block<X>(S), pG = part_size<X>(S);
       const uint32_t my_ch = nch > pb ? (uint32_t)((nch - 1 - pb) / pG + 1) : 0u;
