@@ -527,7 +527,8 @@ def _roofline(stage, ms, P, n_unique, iters, k, peaks, evals):
 # profiles/r01/microbench_primitives.txt): 111.4 FADD per SM per clock.
 F32_ISSUE_PER_S = 32.41e12
 FLOP_PER_EVAL = 8    # 3 sub, 3 mul, 2 add per distance evaluation
-SLOTS_PER_EVAL = 6   # scan_f32: 3 FSUB + FMUL + 2 FFMA issue slots per evaluation
+SLOTS_PER_EVAL = 6   # SURVEY.md §8(d)'s model: 3 FSUB + FMUL + 2 FFMA issue slots per evaluation (the kernel's own
+                     # candidate evaluations are 3 FFMA each in difference form, scan_f32e; its own-center ones are 6)
 
 
 def first_iteration_evals(lib, ctx, torch, d_img, P, k, stream):
@@ -574,7 +575,8 @@ def _loop_roofline(ms, P, n_unique, iters, k, peaks, evals, evals1, phases):
         "frac": achieved / peak, "traffic": _ncu_traffic("wsm_loop", P), "kernel_ms": ms,
         "peak_source": "measured FADD issue rate 32.41e12/s (tools/microbench.cu) x 8 FLOP / 6 slots",
         "note": (f"iterations 2..{iters}: {e_rest} reference distance evaluations (8 FLOP each) in "
-                 f"{t_rest * 1e3:.3f} ms; the loop is latency-bound (dependent L1/L2 loads per scan step), "
+                 f"{t_rest * 1e3:.3f} ms; candidates are evaluated in difference form (one 16-B shared load + 3 FFMA), "
+                 f"the loop is issue/latency-bound (ncu: 70% of the SM issue rate, 24 of 32 threads active), "
                  f"its working set ({10 * n_unique / 1e6:.0f} MB per iteration) stays in L2"),
         "iteration1": {"evals": e1, "us": t1 * 1e6,
                        "reference_evals_per_s": e1 / t1 if t1 > 0 else None,
