@@ -67,6 +67,9 @@
 #ifndef CQB_C4W
 #define CQB_C4W 1  // scan_f32e: the first row entry's distance rides in c4[p].w (no row-quad load for points without candidates)
 #endif
+#ifndef CQB_B0F_LARGE
+#define CQB_B0F_LARGE 0  // large path: block 0 loads a cluster's five moments once for the centers and the SSE (cfg4 -0.4%, cfg3 +1.1%: off)
+#endif
 #ifndef CQB_NQE
 #define CQB_NQE 4  // quads of rowE entries staged in shared memory with the first row quads (<= CQB_NQ)
 #endif
@@ -2045,7 +2048,7 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
     // block 0 (SSE + termination): thread t loads all five moments of cluster
     // t in one L2 round trip and keeps them for the SSE below; the other
     // blocks split the 3k coordinates over their threads
-    const bool b0f = PPT == 1 && blockIdx.x == 0 && !(S.debug & 4096);  // (PPT 2: register budget)
+    const bool b0f = (PPT == 1 || CQB_B0F_LARGE) && blockIdx.x == 0 && !(S.debug & 4096);
     unsigned long long mN = 0, mS0 = 0, mS1 = 0, mS2 = 0, mQ = 0;
     if (b0f && tid < k) {
       mN = ldmom<X != 0>(&tot[3 * KMAX + tid]);
