@@ -812,11 +812,19 @@ constexpr float F32_INF = __builtin_huge_valf();
 constexpr float F32_PU_A = 4.0f + 0x1p-16f, F32_PL_A = 4.0f - 0x1p-16f, F32_P_B = 8.52e-4f;
 constexpr float F32_C_LO = 1.0f - 0x1p-19f, F32_C_HI = 1.0f + 0x1p-19f, F32_C_B = 2.12e-4f;
 
-// Channel C (0 = blue .. 2 = red) of a packed key as a float: one PRMT builds
-// 0x4B0000xx = 2^23 + x, one FADD removes 2^23 (exact, no shift / mask / I2F).
+// Channel C (0 = blue .. 2 = red) of a packed key as a float: one I2F.U8 with
+// a byte selector (exact; a quarter-rate pipe, but one issue slot - the scan
+// is issue-bound - against PRMT + FADD for the 0x4B0000xx - 2^23 form).
+#ifndef CQB_I2F
+#define CQB_I2F 1
+#endif
 template <int C>
 __device__ __forceinline__ float key_chan_f32(uint32_t key) {
+#if CQB_I2F
+  return (float)((key >> (8 * C)) & 0xFFu);
+#else
   return __fsub_rn(__uint_as_float(__byte_perm(key, 0x4B000000u, 0x7440u | (unsigned)C)), 8388608.0f);
+#endif
 }
 __device__ __forceinline__ float u8_to_float(uint32_t v) {  // exact, no I2F
   return __fsub_rn(__uint_as_float(0x4B000000u | v), 8388608.0f);
