@@ -70,6 +70,9 @@
 #ifndef CQB_B0F_LARGE
 #define CQB_B0F_LARGE 0  // large path: block 0 loads a cluster's five moments once for the centers and the SSE (cfg4 -0.4%, cfg3 +1.1%: off)
 #endif
+#ifndef CQB_MAP_STAGE
+#define CQB_MAP_STAGE 1  // large path: the map epilogue's first row entries staged in shared memory
+#endif
 #ifndef CQB_NQE
 #define CQB_NQE 4  // quads of rowE entries staged in shared memory with the first row quads (<= CQB_NQ)
 #endif
@@ -1795,7 +1798,7 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 }
 
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
-template <int X>
+template <int X, bool STAGE>
 __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
                              unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs);
 
@@ -2229,10 +2232,10 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
   if constexpr (X != 0)
     if (part_block<X>(S) == 0 && tid == 0) L.xbox[part][XB_SEQ] = xs + (L.map_lut ? 1ull : 0ull);  // + the epilogue's exchange
   if constexpr (X != 0) {
-    if (L.map_lut) map_epilogue<X>(S, L, grid, n, lo, hi, part, xs);
+    if (L.map_lut) map_epilogue<X, (PPT >= 2) && CQB_MAP_STAGE>(S, L, grid, n, lo, hi, part, xs);
   } else {
     unsigned long long none = 0;
-    if (L.map_lut) map_epilogue<0>(S, L, grid, hi, 0, 0, 0, none);
+    if (L.map_lut) map_epilogue<0, (PPT >= 2) && CQB_MAP_STAGE>(S, L, grid, hi, 0, 0, 0, none);
   }
   if (L.block_times && tid == 0) L.block_times[14 * gridDim.x + blockIdx.x] = globaltimer();  // kernel exit
 }
@@ -2245,17 +2248,24 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
 // color's exact argmin over the rounded palette from its final label with the
 // strict break d(R_p, R_t) > 4 prev, the key -> index LUT and the exact
 // u64 sum of count x error. Saves two launches on the quantize path.
-template <int X>
+// STAGE (large-image kernels, whose dynamic shared block has the room): the
+// first MAPQ entries of every integer row are copied to shared memory after
+// the rows' grid barrier, and a sample's scan reads them there (the rows are
+// otherwise read entry by entry from L2: the epilogue took 180 us on cfg4).
+constexpr int MAPQ = 16;
+template <int X, bool STAGE>
 __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
                              unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs) {
   const int k = L.k, tid = threadIdx.x;
   const double* C = L.st->final_C;
   uint32_t* s_key = S.row0;        // rounded palette keys
   int* s_cc = S.empty_list;        // |R_t|^2
+  int2* s_kc = S.cb;               // {key, |R_t|^2} (one load per evaluation)
   for (int t = tid; t < k; t += blockDim.x) {
     const uint32_t key = (round_chan(C[3 * t]) << 16) | (round_chan(C[3 * t + 1]) << 8) | round_chan(C[3 * t + 2]);
     s_key[t] = key;
     s_cc[t] = key_dot(key, key);
+    s_kc[t] = make_int2((int)key, key_dot(key, key));
     if (blockIdx.x == 0) L.map_palkey[t] = key;
   }
   __syncthreads();
@@ -2290,6 +2300,23 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
     }
   }
   grid.sync();
+  // staged rows: entries 1..MAPQ of row p at q_d[p * (MAPQ + 1) + e] (padded: lanes on
+  // neighbouring rows hit different banks), their order bytes at q_o[p * MAPQ + e]
+  int* q_d = nullptr;
+  uint8_t* q_o = nullptr;
+  if constexpr (STAGE) {
+    q_d = reinterpret_cast<int*>(loop_dyn_large().e0);
+    q_o = reinterpret_cast<uint8_t*>(q_d + KMAX * (MAPQ + 1));
+    static_assert(sizeof(LoopDynLarge::e0) >= KMAX * (MAPQ + 1) * 4 + KMAX * MAPQ, "staged map rows fit in the rowE stage");
+    for (int u = tid; u < MAPQ * k; u += blockDim.x) {
+      const int p = u / MAPQ, e = u % MAPQ;
+      if (1 + e < k) {
+        q_d[p * (MAPQ + 1) + e] = __ldcg(L.map_sortedDr + p * KMAX + 1 + e);
+        q_o[p * MAPQ + e] = __ldcg(L.map_orderR + p * KMAX + 1 + e);
+      }
+    }
+    __syncthreads();
+  }
   // Sharded: each rank (part) maps its own samples [lo, hi). X = 1 sends the
   // palette indices into every rank's window (its label region, contiguous
   // stores), exchanges the partial error sums, and every rank then fills its
@@ -2317,15 +2344,30 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
       best = p;
       const int* rowd = L.map_sortedDr + p * KMAX;
       const uint8_t* rowo = L.map_orderR + p * KMAX;
-      for (int j = 1; j < k; ++j) {
-        if (rowd[j] > bound) break;
-        const int t = rowo[j];
-        const int d = xx + s_cc[t] - 2 * key_dot(x, s_key[t]);
+      auto eval = [&](int t) {
+        const int2 kc = s_kc[t];
+        const int d = xx + kc.y - 2 * key_dot(x, (uint32_t)kc.x);
         if (d < mind || (d == mind && t < best)) {
           mind = d;
           best = t;
         }
+      };
+      int j = 1;
+      bool open = true;  // the scan has not met its break entry yet
+      if constexpr (STAGE) {
+        const int* qd = q_d + p * (MAPQ + 1);
+        const uint8_t* qo = q_o + p * MAPQ;
+        const int jm = min(k, MAPQ + 1);
+        for (; j < jm; ++j) {
+          if (qd[j - 1] > bound) { open = false; break; }
+          eval(qo[j - 1]);
+        }
       }
+      if (open)
+        for (; j < k; ++j) {
+          if (rowd[j] > bound) break;
+          eval(rowo[j]);
+        }
       if constexpr (X == 1) {
         for (int r = 0; r < L.xw; ++r) (reinterpret_cast<uint8_t*>(L.xbox[r]) + XB_LAB_OFF)[i] = (uint8_t)best;
       } else {
