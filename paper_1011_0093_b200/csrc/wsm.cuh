@@ -1800,7 +1800,8 @@ __device__ void flush_moments(LoopSmem& S, unsigned long long* gacc, int k) {
 // The persistent, cooperative WSM loop (run_weighted_kmeans, kmeans.hpp:336-376).
 template <int X, bool STAGE>
 __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
-                             unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs);
+                                          unsigned long long lo, unsigned long long hi, int part,
+                                          unsigned long long& xs);
 
 // One instantiation per assignment variant (WSM, KM, FKM): a single kernel
 // with a runtime switch cost the WSM loop ~1.5% (register allocation).
@@ -2255,7 +2256,8 @@ __global__ void __launch_bounds__(LOOP_THREADS, CQB_LOOP_MINB) k_wsm_loop(LoopPa
 constexpr int MAPQ = 16;
 template <int X, bool STAGE>
 __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& grid, unsigned long long n,
-                             unsigned long long lo, unsigned long long hi, int part, unsigned long long& xs) {
+                                          unsigned long long lo, unsigned long long hi, int part,
+                                          unsigned long long& xs) {
   const int k = L.k, tid = threadIdx.x;
   const double* C = L.st->final_C;
   uint32_t* s_key = S.row0;        // rounded palette keys
@@ -2328,16 +2330,33 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
   unsigned long long err = 0;
   // whole warps per step (consecutive Morton samples per warp: the coarse table's cell segments)
   const int lane = tid & 31;
-  for (unsigned long long base = a + (unsigned long long)pb * blockDim.x + (tid & ~31); base < b;
-       base += (unsigned long long)pG * blockDim.x) {
+  // the next step's sample (key, label, count) is loaded before this step's
+  // scan: one L2 round trip per step hidden behind the previous scan
+  const unsigned long long step = (unsigned long long)pG * blockDim.x;
+  uint32_t nx = 0, ncnt = 0;
+  int np = 0;
+  auto fetch = [&](unsigned long long bs) {
+    const unsigned long long i2 = bs + lane;
+    if (i2 < b) {
+      nx = L.keys[i2];
+      np = X ? (int)__ldcg(&L.labels[i2]) : (int)L.labels[i2];
+      ncnt = L.counts[i2];
+    }
+  };
+  {
+    const unsigned long long b0 = a + (unsigned long long)pb * blockDim.x + (tid & ~31);
+    if (b0 < b) fetch(b0);
+  }
+  for (unsigned long long base = a + (unsigned long long)pb * blockDim.x + (tid & ~31); base < b; base += step) {
     const unsigned long long i = base + lane;
     const bool v = i < b;
-    uint32_t x = 0;
+    uint32_t x = nx;
+    const int p = np;
+    const uint32_t cnt = ncnt;
+    if (base + step < b) fetch(base + step);
     int best = 0;
     if (v) {
-      x = L.keys[i];
       const int xx = key_dot(x, x);
-      const int p = X ? (int)__ldcg(&L.labels[i]) : (int)L.labels[i];
       const int prev = xx + s_cc[p] - 2 * key_dot(x, s_key[p]);
       const int bound = 4 * prev;
       int mind = prev;
@@ -2373,7 +2392,7 @@ __device__ void map_epilogue(LoopSmem& S, const LoopParams& L, cg::grid_group& g
       } else {
         L.map_lut[x] = (uint8_t)best;
       }
-      err += (unsigned long long)L.counts[i] * (unsigned long long)mind;
+      err += (unsigned long long)cnt * (unsigned long long)mind;
     }
     if (X != 1 && L.map_cellw) {
       const unsigned am = __ballot_sync(0xffffffffu, v);
