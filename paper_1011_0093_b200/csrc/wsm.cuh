@@ -1052,19 +1052,21 @@ __device__ __forceinline__ int scan_f32(const float4* __restrict__ c4, const flo
 // tests are those of scan_f32 (prev in the six-operation form, same pl / pu).
 //
 // Error bound of diff = fma(a0, m0, fma(a1, m1, fma(a2, m2, w))), u = 2^-24:
-// a_i, m_i, w carry one FP32 rounding each and the three FFMAs one each, every
-// partial sum bounded by M = |w*| + sum |a_i m_i|, so |diff - Delta| <=
-// 4u M (1 + O(u)) + 1e-9 (the FP64 roundings of the table and of the
-// reference's own dist2). An evaluated entry has D(c_p, c_t) < 4 prev (its
-// fl32 is below pl), hence |w*| <= D(c_p, c_t) + 0.012 and sum |a_i m_i| <=
-// |a| |m| = 2 sqrt(prev' D(c_p, c_t)) with prev' = |a*|^2 <= prev (1 + 6u):
-// M <= 8 prev (1 + 1e-6) + 0.02 and |diff - Delta| <= E = 1.91e-6 prev + 1e-8.
-// The own center has Delta = 0 exactly. The FP32 best (index 0 = own) is the
-// reference's lexicographic (d, index) minimum when the second smallest
-// difference exceeds the smallest by more than 2 E; the test below uses
-// 4.1e-6 prev + 2.5e-6 (> 2 E (1 + u) plus the subtraction's rounding). A tie
-// never certifies.
-constexpr float F32_E_A = 4.1e-6f, F32_E_B = 2.5e-6f;
+// w carries one FP32 rounding (u |w*|), every product a_i m_i two (a_i and
+// m_i: 2u S, S = sum |a_i m_i|), and each of the three FFMAs rounds a partial
+// sum of magnitude <= |w*| + S: |diff - Delta| <= (4 |w*| + 5 S) u (1 + O(u))
+// + 1e-9 (the FP64 roundings of the table and of the reference's own dist2).
+// An evaluated entry has D(c_p, c_t) < 4 prev (its fl32 is below pl), hence
+// |w*| <= D(c_p, c_t) + 0.012 and S <= |a| |m| = 2 sqrt(prev' D(c_p, c_t))
+// with prev' = |a*|^2 <= prev (1 + 6u): both are at most 4 prev (1 + 1e-6) +
+// 0.012, and |diff - Delta| <= E = 36 u prev + 1e-8 = 2.15e-6 prev + 1e-8
+// (tests/test_ediff_bound_cpu.py samples it: random and reflected-center
+// inputs stay below 0.75 E). The own center has Delta = 0 exactly. The FP32
+// best (index 0 = own) is the reference's lexicographic (d, index) minimum
+// when the second smallest difference exceeds the smallest by more than 2 E;
+// the test below uses 4.4e-6 prev + 2.5e-6 (> 2 E (1 + u) plus the
+// subtraction's rounding). A tie never certifies.
+constexpr float F32_E_A = 4.4e-6f, F32_E_B = 2.5e-6f;
 // 16-B load from a 32-bit shared-window address (the dynamic block's base is
 // converted once per assign pass; addressing through generic pointers made the
 // compiler rebuild the window base, S2R + three more instructions, per point)
